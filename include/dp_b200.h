@@ -1,0 +1,203 @@
+/*
+ * dp_b200.h — C-ABI of the B200-native Deep Potential force evaluation.
+ *
+ * Drop-in boundary for the reference's hot path:
+ *   compute_energy_forces_virial_tabulated   /root/reference/proj/include/dpmd/fused.hpp:70-73
+ *   build_neighbor_list                      /root/reference/proj/include/dpmd/neighbor.hpp:31-36
+ *   run_md (+ MDConfig/ThermoRecord/MDResult) /root/reference/proj/include/dpmd/md.hpp:14-60
+ *   FusedCounters                            /root/reference/proj/include/dpmd/fused.hpp:10-21
+ * plus the host-side fixture generators the reference's tests and CLI use to make inputs
+ * (gen_model/gen_config model_io.hpp:39-47, build_tables table.hpp:46-50, init_velocities
+ * md.hpp:41-44, testutil::make_test_model/make_random_config tests/helpers.hpp:21-99).
+ *
+ * Conventions (same as the reference):
+ *   - positions: 3n doubles, Angstrom, cartesian, raw (unwrapped);
+ *   - box: 9 doubles, ROWS are the cell vectors (geom.hpp:14-16);
+ *   - virial[3x+y] = sum over pairs of d_x * dE/dd_y (exact.cpp:22-38);
+ *   - forces: 3n doubles, eV/A.
+ * Return codes mirror the reference CLI (tools/dpmd.cpp:434-443):
+ *   0 ok, 1 NumericalError class, 2 InputError class, 3 CUDA/runtime failure.
+ * Threading: one dp_handle per host thread; every device buffer is owned by its handle.
+ * No torch types cross this boundary; the library has no CPU fallback for the compute path.
+ */
+#ifndef DP_B200_H
+#define DP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DP_OK 0
+#define DP_NUMERICAL_ERROR 1
+#define DP_INPUT_ERROR 2
+#define DP_RUNTIME_ERROR 3
+
+/* Fitting net of one center type (model.hpp:22-36). Layer k maps widths[k] -> widths[k+1],
+ * weights row-major in x out; identity shortcut when in == out. */
+typedef struct {
+  int n_layers;
+  const int* widths;        /* n_layers + 1 */
+  const double* const* w;   /* n_layers pointers, widths[k]*widths[k+1] */
+  const double* const* b;   /* n_layers pointers, widths[k+1] */
+  const double* w_out;      /* widths[n_layers] */
+  double b_out;
+} dp_fitting_desc;
+
+/* DPModel (model.hpp:38-58) as seen by the tabulated path: the embedding nets are replaced
+ * by the compression tables, so only cutoffs, capacities, m_lt and fitting nets remain. */
+typedef struct {
+  int n_types;
+  double r_cut;
+  double r_smooth;
+  int d1;                          /* feature width M = 4*d1 */
+  int m_lt;
+  const double* masses;            /* n_types, g/mol */
+  const int* max_nbr;              /* n_types slot capacity per neighbor type */
+  const dp_fitting_desc* fitting;  /* n_types, one per center type */
+} dp_model_desc;
+
+/* CompressionTable (table.hpp:20-35); header fields are those of the DPTB file
+ * (table_io.hpp:10-21). Coefficient layout per interval: [block][k=0..5][f<B]. */
+typedef struct {
+  int n_tables;                /* == n_types, one per neighbor type */
+  double x0;
+  double h;
+  uint64_t n;                  /* intervals */
+  int m;                       /* features, == 4*d1 */
+  int block;                   /* B */
+  const double* const* coeffs; /* n_tables pointers, n * ceil(m/B) * 6 * B doubles */
+} dp_table_desc;
+
+typedef struct {
+  uint64_t rows_forward;
+  uint64_t rows_backward;
+  uint64_t extrapolations;
+} dp_counters;
+
+/* MDConfig (md.hpp:14-21). n_workers has no meaning on the GPU and is ignored. */
+typedef struct {
+  int64_t n_steps;
+  double dt;
+  double buffer;
+  int rebuild_every;
+  int thermo_every;
+} dp_md_config;
+
+/* ThermoRecord (md.hpp:23-29). */
+typedef struct {
+  int64_t step;
+  double ke, pe, temperature, pressure;
+} dp_thermo;
+
+/* MDResult (md.hpp:31-39), thermo records returned separately. */
+typedef struct {
+  uint64_t force_evals;
+  uint64_t staleness_checks;
+  double max_drift_seen;
+  dp_counters counters;
+  double final_ke, final_pe, final_total;
+} dp_md_result;
+
+typedef struct dp_handle dp_handle;
+
+/* ---- evaluation handle -------------------------------------------------------------------- */
+
+/* precision: 0 = FP64 (parity mode, 1e-10), 1 = mixed (FP32 tabulate, TF32 fitting, tanh table). */
+int dp_create(const dp_model_desc* model, const dp_table_desc* tables, int device, int precision,
+              dp_handle** out);
+int dp_destroy(dp_handle* h);
+const char* dp_last_error(const dp_handle* h);
+const char* dp_version(void);
+
+/* Neighbor-list skin for dp_compute: lists are built at r_cut + skin and reused while every atom
+ * stayed within skin/2 of its build position (same staleness rule as run_md, md.cpp:211-217).
+ * skin = 0 (default) rebuilds on every call, i.e. list = build_neighbor_list(cfg, r_cut). */
+int dp_set_skin(dp_handle* h, double skin);
+
+/* compute_energy_forces_virial_tabulated (fused.cpp:245-288) on the GPU. Host buffers in and out.
+ * atom_energy may be NULL. Counters of the last call are available from dp_counters_get. */
+int dp_compute(dp_handle* h, int64_t n, const double* pos, const int32_t* types,
+               const double box[9], const uint8_t pbc[3], double* energy, double* forces,
+               double* virial, double* atom_energy);
+int dp_counters_get(const dp_handle* h, dp_counters* out);
+
+/* build_neighbor_list (neighbor.cpp:162-179) on the GPU, canonical order (ascending j, then
+ * shift lexicographic). Two calls: dp_neighbor_list_build returns the total entry count, then
+ * dp_neighbor_list_get copies offsets[n+1], j[total] and shift[3*total] to host. */
+int dp_neighbor_list_build(dp_handle* h, int64_t n, const double* pos, const int32_t* types,
+                           const double box[9], const uint8_t pbc[3], double cutoff,
+                           int64_t* total);
+int dp_neighbor_list_get(dp_handle* h, int64_t* offsets, int32_t* j, int32_t* shift);
+
+/* run_md (md.cpp:151-231) fully device resident. pos/vel are updated in place. thermo receives
+ * up to thermo_cap records (n_steps/thermo_every + 1 are produced); *n_thermo is the count. */
+int dp_md_run(dp_handle* h, int64_t n, double* pos, double* vel, const int32_t* types,
+              const double box[9], const uint8_t pbc[3], const dp_md_config* cfg,
+              dp_thermo* thermo, int64_t thermo_cap, int64_t* n_thermo, dp_md_result* result);
+
+/* Split form of dp_md_run for benchmarking with device-resident state: begin uploads and
+ * evaluates step 0, step advances k Verlet steps asynchronously on the handle's stream,
+ * end synchronizes and copies state back. */
+int dp_md_begin(dp_handle* h, int64_t n, const double* pos, const double* vel,
+                const int32_t* types, const double box[9], const uint8_t pbc[3],
+                const dp_md_config* cfg);
+int dp_md_step(dp_handle* h, int64_t k);
+int dp_md_end(dp_handle* h, double* pos, double* vel, dp_thermo* thermo, int64_t thermo_cap,
+              int64_t* n_thermo, dp_md_result* result);
+
+/* cudaStream_t of the handle (for CUDA-event timing on the launching stream). */
+void* dp_stream(dp_handle* h);
+/* Number of kernels this handle has launched since creation. */
+uint64_t dp_launch_count(const dp_handle* h);
+
+/* ---- host-side fixture generators (CPU, deterministic, bit-identical to the reference) ---- */
+
+/* Model flat layout ("model blob"), per type t in order:
+ *   embedding: w0[d1] b0[d1] w1[d1*2d1] b1[2d1] w2[2d1*4d1] b2[4d1]
+ * then per type t: fitting layers k: w[in*out] b[out], then w_out[width], b_out[1].
+ * dp_model_blob_size gives the length for the shape below. */
+typedef struct {
+  int n_types;
+  double r_cut, r_smooth;
+  int d1, m_lt;
+  int fit_width, fit_hidden;
+  double masses[8];
+  int max_nbr[8];
+  double lattice_a;
+  int site_pattern[8];
+  int n_sites;
+} dp_preset;
+
+int dp_preset_get(const char* name, dp_preset* out);                     /* model_io.cpp:16-61 */
+int64_t dp_model_blob_size(const dp_preset* shape);
+int dp_gen_model(const char* preset, uint64_t seed, double* blob);      /* model_io.cpp:129-188 */
+int dp_gen_test_model(const dp_preset* shape, uint64_t seed, double fit_scale,
+                      double* blob);                                     /* helpers.hpp:21-72 */
+/* Table build from a model blob (table.cpp:77-162): n_intervals first (coeffs NULL) then fill. */
+int dp_build_tables(const dp_preset* shape, const double* blob, double h, uint64_t* n_intervals,
+                    double* x_end, double* coeffs);
+int dp_gen_config(const char* preset, int nx, int ny, int nz, double jitter, uint64_t seed,
+                  double* pos, int32_t* types, double box[9]);           /* model_io.cpp:190-224 */
+int dp_gen_random_config(int n, int n_types, double box_len, double min_sep, uint64_t seed,
+                         double* pos, int32_t* types);                  /* helpers.hpp:75-99 */
+int dp_init_velocities(int64_t n, const int32_t* types, const double* masses, double t_init,
+                       uint64_t seed, double* vel);                     /* md.cpp:14-55 */
+uint64_t dp_mix_seed(uint64_t seed, uint64_t k);                        /* rng.hpp:44-49 */
+
+/* DPTB container (table_io.cpp:32-89). */
+int dp_write_tables(const char* path, const dp_table_desc* tables);
+int dp_read_tables_header(const char* path, int* n_tables, int* m, int* block, uint64_t* n,
+                          double* x0, double* h);
+int dp_read_tables(const char* path, double* coeffs /* n_tables * n * stride */);
+
+/* TanhTable (tanh_table.cpp:5-21) coefficients, 3 * 8193 doubles; mixed-precision mode only. */
+int dp_tanh_table(double* coef);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DP_B200_H */

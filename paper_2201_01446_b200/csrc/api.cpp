@@ -1,0 +1,150 @@
+// C-ABI of dp_b200 (include/dp_b200.h). Every entry point maps exceptions to the reference
+// CLI's exit codes (tools/dpmd.cpp:434-443): InputError -> 2, NumericalError -> 1.
+#include <cstring>
+
+#include "engine.hpp"
+
+struct dp_handle {
+  dpb::Engine eng;
+  double skin = 0.0;
+};
+
+using dpb::guard_call;
+using dpb::InputErr;
+
+extern "C" {
+
+const char* dp_version(void) { return "dp_b200 0.1 (sm_100a, fp64 DMMA)"; }
+
+int dp_create(const dp_model_desc* model, const dp_table_desc* tables, int device, int precision,
+              dp_handle** out) {
+  if (!out) return DP_INPUT_ERROR;
+  *out = nullptr;
+  dp_handle* h = new dp_handle();
+  const int rc = guard_call(nullptr, [&] { h->eng.create(model, tables, device, precision); });
+  if (rc != DP_OK) {
+    h->eng.destroy();
+    delete h;
+    return rc;
+  }
+  *out = h;
+  return DP_OK;
+}
+
+int dp_destroy(dp_handle* h) {
+  if (!h) return DP_OK;
+  h->eng.destroy();
+  delete h;
+  return DP_OK;
+}
+
+const char* dp_last_error(const dp_handle* h) {
+  return h ? h->eng.last_error.c_str() : dpb::global_error().c_str();
+}
+
+int dp_set_skin(dp_handle* h, double skin) {
+  if (!h) return DP_INPUT_ERROR;
+  return guard_call(&h->eng.last_error, [&] {
+    if (!(skin >= 0.0)) throw InputErr("skin must be non-negative");
+    h->skin = skin;
+    h->eng.list_valid = false;
+  });
+}
+
+int dp_compute(dp_handle* h, int64_t n, const double* pos, const int32_t* types, const double box[9],
+               const uint8_t pbc[3], double* energy, double* forces, double* virial,
+               double* atom_energy) {
+  if (!h) return DP_INPUT_ERROR;
+  return guard_call(&h->eng.last_error, [&] {
+    dpb::Engine& E = h->eng;
+    if (!energy || !forces || !virial) throw InputErr("null output array");
+    E.set_config(n, pos, types, box, pbc);
+    const double cutoff = E.r_cut + h->skin;
+    bool rebuild = !E.list_valid || E.list_cutoff != cutoff;
+    if (!rebuild && h->skin > 0.0) rebuild = E.max_drift() > 0.5 * h->skin;
+    if (h->skin == 0.0) rebuild = true;
+    if (rebuild) E.build_list(cutoff);
+    E.reset_counters();
+    E.evaluate();
+    E.check_err();
+    E.fetch_results(energy, forces, virial, atom_energy);
+    E.read_counters();
+  });
+}
+
+int dp_counters_get(const dp_handle* h, dp_counters* out) {
+  if (!h || !out) return DP_INPUT_ERROR;
+  *out = h->eng.host_counters;
+  return DP_OK;
+}
+
+int dp_neighbor_list_build(dp_handle* h, int64_t n, const double* pos, const int32_t* types,
+                           const double box[9], const uint8_t pbc[3], double cutoff,
+                           int64_t* total) {
+  if (!h) return DP_INPUT_ERROR;
+  return guard_call(&h->eng.last_error, [&] {
+    dpb::Engine& E = h->eng;
+    E.set_config(n, pos, types, box, pbc);
+    E.build_list(cutoff);
+    E.check_err();
+    if (total) *total = E.n_entries;
+  });
+}
+
+int dp_neighbor_list_get(dp_handle* h, int64_t* offsets, int32_t* j, int32_t* shift) {
+  if (!h) return DP_INPUT_ERROR;
+  return guard_call(&h->eng.last_error, [&] {
+    if (!h->eng.list_valid) throw InputErr("no neighbour list built");
+    h->eng.download_list(offsets, j, shift);
+  });
+}
+
+int dp_md_begin(dp_handle* h, int64_t n, const double* pos, const double* vel,
+                const int32_t* types, const double box[9], const uint8_t pbc[3],
+                const dp_md_config* cfg) {
+  if (!h || !cfg || !vel) return DP_INPUT_ERROR;
+  return guard_call(&h->eng.last_error, [&] {
+    dpb::Engine& E = h->eng;
+    if (n < 1) throw InputErr("configuration has no atoms");
+    E.set_config(n, pos, types, box, pbc);
+    E.md_begin(pos, vel, cfg);
+  });
+}
+
+int dp_md_step(dp_handle* h, int64_t k) {
+  if (!h) return DP_INPUT_ERROR;
+  return guard_call(&h->eng.last_error, [&] { h->eng.md_steps(k); });
+}
+
+int dp_md_end(dp_handle* h, double* pos, double* vel, dp_thermo* thermo, int64_t thermo_cap,
+              int64_t* n_thermo, dp_md_result* result) {
+  if (!h) return DP_INPUT_ERROR;
+  return guard_call(&h->eng.last_error, [&] {
+    dpb::Engine& E = h->eng;
+    E.md_end(pos, vel);
+    const int64_t nr = static_cast<int64_t>(E.thermo.size());
+    if (thermo)
+      for (int64_t k = 0; k < nr && k < thermo_cap; ++k) thermo[k] = E.thermo[k];
+    if (n_thermo) *n_thermo = nr;
+    if (result) *result = E.md_res;
+  });
+}
+
+int dp_md_run(dp_handle* h, int64_t n, double* pos, double* vel, const int32_t* types,
+              const double box[9], const uint8_t pbc[3], const dp_md_config* cfg,
+              dp_thermo* thermo, int64_t thermo_cap, int64_t* n_thermo, dp_md_result* result) {
+  int rc = dp_md_begin(h, n, pos, vel, types, box, pbc, cfg);
+  if (rc) return rc;
+  rc = dp_md_step(h, cfg->n_steps);
+  if (rc) {
+    h->eng.md_active = false;
+    return rc;
+  }
+  return dp_md_end(h, pos, vel, thermo, thermo_cap, n_thermo, result);
+}
+
+void* dp_stream(dp_handle* h) { return h ? static_cast<void*>(h->eng.stream) : nullptr; }
+
+uint64_t dp_launch_count(const dp_handle* h) { return h ? h->eng.launches : 0; }
+
+} // extern "C"

@@ -1,0 +1,100 @@
+// Device-side building blocks shared by the dp_b200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "host_common.hpp"
+
+#define DPB_CUDA(x)                                                                        \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess)                                                                 \
+      throw ::dpb::CudaErr(std::string(#x) + ": " + cudaGetErrorString(e_));             \
+  } while (0)
+
+namespace dpb {
+
+// Error codes raised by kernels into Workspace::err (first writer wins).
+enum DevErr : int {
+  DEV_OK = 0,
+  DEV_OVERLAP = 1,     // r^2 < 1e-12 inside r_cut (env_mat.cpp:33)
+  DEV_OVERFLOW = 2,    // more real neighbours of a type than max_nbr (env_mat.cpp:37-39)
+  DEV_TABLE_LOW = 3,   // table input below x0 (table.cpp:21); cannot happen for s >= 0
+  DEV_SHIFT_RANGE = 4, // image shift outside the packed key range
+  DEV_ROW_CAP = 5,     // neighbour row longer than the sort capacity
+  DEV_STALE = 6,       // list stale in MD (md.cpp:211-217)
+};
+
+// Cell as the kernels see it (geom.hpp:14-44).
+struct DevCell {
+  double h[9];
+  double hinv[9];
+  double vol;
+  int per[3];
+};
+
+// Neighbour key: [type:6][j:28][s0+512:10][s1+512:10][s2+512:10]. Sorting keys ascending gives
+// the stable type partition of the canonical (j, shift) order (env_mat.cpp:25, neighbor.cpp:10-17).
+constexpr int KEY_SHIFT_BIAS = 512;
+__host__ __device__ inline uint64_t make_key(int type, int j, int s0, int s1, int s2) {
+  return (static_cast<uint64_t>(type) << 58) | (static_cast<uint64_t>(j) << 30) |
+         (static_cast<uint64_t>(s0 + KEY_SHIFT_BIAS) << 20) |
+         (static_cast<uint64_t>(s1 + KEY_SHIFT_BIAS) << 10) |
+         static_cast<uint64_t>(s2 + KEY_SHIFT_BIAS);
+}
+__host__ __device__ inline int key_type(uint64_t k) { return static_cast<int>(k >> 58); }
+__host__ __device__ inline int key_j(uint64_t k) {
+  return static_cast<int>((k >> 30) & ((1u << 28) - 1));
+}
+__host__ __device__ inline void key_shift(uint64_t k, int* s) {
+  s[0] = static_cast<int>((k >> 20) & 1023) - KEY_SHIFT_BIAS;
+  s[1] = static_cast<int>((k >> 10) & 1023) - KEY_SHIFT_BIAS;
+  s[2] = static_cast<int>(k & 1023) - KEY_SHIFT_BIAS;
+}
+// Key of the reverse entry (j -> i, -s) as seen in row j.
+__host__ __device__ inline uint64_t reverse_key(uint64_t k, int type_i, int i) {
+  int s[3];
+  key_shift(k, s);
+  return make_key(type_i, i, -s[0], -s[1], -s[2]);
+}
+
+#ifdef __CUDACC__
+// d = (r_j + s0 h0 + s1 h1 + s2 h2) - r_i evaluated exactly as the reference does: left to
+// right, every product and sum rounded separately, no fused multiply-add (geom.hpp:61-69).
+__device__ __forceinline__ void disp_exact(const DevCell& c, double3 ri, double3 rj, int s0,
+                                           int s1, int s2, double* d) {
+  const double rjv[3] = {rj.x, rj.y, rj.z};
+  const double riv[3] = {ri.x, ri.y, ri.z};
+#pragma unroll
+  for (int x = 0; x < 3; ++x) {
+    double img = __dadd_rn(rjv[x], __dmul_rn(static_cast<double>(s0), c.h[x]));
+    img = __dadd_rn(img, __dmul_rn(static_cast<double>(s1), c.h[3 + x]));
+    img = __dadd_rn(img, __dmul_rn(static_cast<double>(s2), c.h[6 + x]));
+    d[x] = __dsub_rn(img, riv[x]);
+  }
+}
+
+__device__ __forceinline__ double norm2_exact(const double* d) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])), __dmul_rn(d[2], d[2]));
+}
+
+__device__ __forceinline__ double3 ld_pos(const double4* p, int j) {
+  const double2* q = reinterpret_cast<const double2*>(p + j);
+  const double2 a = __ldg(q);
+  const double2 b = __ldg(q + 1);
+  return make_double3(a.x, a.y, b.x);
+}
+
+__device__ __forceinline__ void raise_err(int* err, int code) { atomicCAS(err, 0, code); }
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+#endif // __CUDACC__
+
+} // namespace dpb

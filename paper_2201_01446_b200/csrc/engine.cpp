@@ -1,0 +1,407 @@
+// Host side of the Engine: model upload, configuration handling, evaluation sequencing and the
+// device-resident MD loop. Mirrors the reference orchestration:
+//   compute_energy_forces_virial_tabulated   fused.cpp:245-288
+//   run_md / rebuild / evaluate              md.cpp:70-134, 151-231
+#include <cstring>
+
+#include "engine.hpp"
+
+namespace dpb {
+
+std::string& global_error() {
+  static thread_local std::string e;
+  return e;
+}
+
+namespace {
+
+int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+void raise_device_error(int code) {
+  switch (code) {
+    case DEV_OK: return;
+    case DEV_OVERLAP: throw NumErr("overlapping atoms in neighbor environment");
+    case DEV_OVERFLOW: throw NumErr("neighbor slot capacity exceeded");
+    case DEV_TABLE_LOW: throw InputErr("table input below domain start");
+    case DEV_SHIFT_RANGE: throw InputErr("image shift outside +-511 cells (positions too far from the box)");
+    case DEV_ROW_CAP: throw NumErr("neighbour row exceeds the kernel capacity");
+    case DEV_STALE: throw NumErr("neighbor list stale: an atom moved more than half the buffer since the last rebuild");
+    default: throw CudaErr("unknown device error " + std::to_string(code));
+  }
+}
+
+} // namespace
+
+void Engine::create(const dp_model_desc* md, const dp_table_desc* td, int dev, int prec) {
+  if (!md || !td) throw InputErr("null model or table descriptor");
+  if (md->n_types < 1 || md->n_types > 63) throw InputErr("model needs 1..63 species");
+  if (!(md->r_cut > 0.0) || !(md->r_smooth >= 0.0) || !(md->r_smooth < md->r_cut))
+    throw InputErr("model cutoffs must satisfy 0 <= r_smooth < r_cut");
+  if (md->d1 < 1) throw InputErr("embedding width must be positive");
+  if (md->m_lt < 1 || md->m_lt > 4 * md->d1) throw InputErr("m_lt must lie in [1, 4*d1]");
+  if (td->n_tables != md->n_types) throw InputErr("need one table per neighbor type");
+  if (td->m != 4 * md->d1) throw InputErr("table feature width does not match 4*d1");
+  if (td->block < 1 || td->n < 1 || !(td->h > 0.0)) throw InputErr("table header is inconsistent");
+  if (prec != 0 && prec != 1) throw InputErr("precision must be 0 (fp64) or 1 (mixed)");
+  precision = prec;
+  device = dev;
+  DPB_CUDA(cudaSetDevice(dev));
+  DPB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  n_types = md->n_types;
+  r_cut = md->r_cut;
+  r_smooth = md->r_smooth;
+  d1 = md->d1;
+  M = 4 * d1;
+  Mp = round_up(M, 32);
+  if (Mp > 256) throw InputErr("feature width 4*d1 must be at most 256");
+  mlt = md->m_lt;
+  K0 = mlt * M;
+  K0p = round_up(K0, 64);
+  masses.assign(md->masses, md->masses + n_types);
+  max_nbr.assign(md->max_nbr, md->max_nbr + n_types);
+  for (int t = 0; t < n_types; ++t) {
+    if (max_nbr[t] <= 0) throw InputErr("model max_nbr entries must be positive");
+    if (!(masses[t] > 0.0)) throw InputErr("model masses must be positive");
+  }
+  // fitting structure (identical across centre types)
+  const dp_fitting_desc& f0 = md->fitting[0];
+  if (f0.n_layers < 1) throw InputErr("fitting net needs at least one hidden layer");
+  if (f0.widths[0] != K0) throw InputErr("fitting input width does not match descriptor");
+  for (int t = 1; t < n_types; ++t) {
+    const dp_fitting_desc& f = md->fitting[t];
+    if (f.n_layers != f0.n_layers) throw InputErr("fitting nets of all types must share a shape");
+    for (int k = 0; k <= f.n_layers; ++k)
+      if (f.widths[k] != f0.widths[k]) throw InputErr("fitting nets of all types must share a shape");
+  }
+  const int L = f0.n_layers;
+  layers.resize(L);
+  widthp_max = 64;
+  for (int k = 0; k < L; ++k) {
+    FitLayer& fl = layers[k];
+    fl.in = f0.widths[k];
+    fl.out = f0.widths[k + 1];
+    if (fl.out <= 0) throw InputErr("fitting layer widths are inconsistent");
+    fl.inp = k == 0 ? K0p : round_up(fl.in, 64);
+    fl.outp = round_up(fl.out, 64);
+    fl.shortcut = fl.in == fl.out;
+    widthp_max = std::max(widthp_max, fl.outp);
+  }
+  // tables -> [type][interval][6][Mp]
+  tab_x0 = td->x0;
+  tab_h = td->h;
+  tab_n = td->n;
+  const int B = td->block;
+  const int nb = (td->m + B - 1) / B;
+  const size_t src_stride = static_cast<size_t>(nb) * 6 * B;
+  const size_t dst_stride = static_cast<size_t>(6) * Mp;
+  std::vector<double> tbuf(static_cast<size_t>(n_types) * tab_n * dst_stride, 0.0);
+  for (int t = 0; t < n_types; ++t)
+    for (uint64_t th = 0; th < tab_n; ++th) {
+      const double* src = td->coeffs[t] + th * src_stride;
+      double* dst = tbuf.data() + (static_cast<size_t>(t) * tab_n + th) * dst_stride;
+      for (int p = 0; p < M; ++p)
+        for (int m = 0; m < 6; ++m)
+          dst[m * Mp + p] = src[static_cast<size_t>(p / B) * 6 * B + m * B + (p % B)];
+    }
+  tab.ensure(tbuf.size());
+  DPB_CUDA(cudaMemcpy(tab.p, tbuf.data(), tbuf.size() * sizeof(double), cudaMemcpyHostToDevice));
+  // fitting weights, zero padded
+  fit_wt.resize(n_types * L);
+  fit_w.resize(n_types * L);
+  fit_b.resize(n_types * L);
+  fit_wout.resize(n_types);
+  b_out.resize(n_types);
+  for (int t = 0; t < n_types; ++t) {
+    const dp_fitting_desc& f = md->fitting[t];
+    for (int k = 0; k < L; ++k) {
+      const FitLayer& fl = layers[k];
+      std::vector<double> w(static_cast<size_t>(fl.inp) * fl.outp, 0.0), wt(w.size(), 0.0),
+          b(fl.outp, 0.0);
+      for (int u = 0; u < fl.in; ++u)
+        for (int v = 0; v < fl.out; ++v) {
+          const double x = f.w[k][static_cast<size_t>(u) * fl.out + v];
+          w[static_cast<size_t>(u) * fl.outp + v] = x;
+          wt[static_cast<size_t>(v) * fl.inp + u] = x;
+        }
+      for (int v = 0; v < fl.out; ++v) b[v] = f.b[k][v];
+      DevBuf<double>& dw = fit_w[t * L + k];
+      DevBuf<double>& dwt = fit_wt[t * L + k];
+      DevBuf<double>& db = fit_b[t * L + k];
+      dw.ensure(w.size());
+      dwt.ensure(wt.size());
+      db.ensure(b.size());
+      DPB_CUDA(cudaMemcpy(dw.p, w.data(), w.size() * 8, cudaMemcpyHostToDevice));
+      DPB_CUDA(cudaMemcpy(dwt.p, wt.data(), wt.size() * 8, cudaMemcpyHostToDevice));
+      DPB_CUDA(cudaMemcpy(db.p, b.data(), b.size() * 8, cudaMemcpyHostToDevice));
+    }
+    const int last = layers[L - 1].out;
+    std::vector<double> wo(layers[L - 1].outp, 0.0);
+    for (int v = 0; v < last; ++v) wo[v] = f.w_out[v];
+    fit_wout[t].ensure(wo.size());
+    DPB_CUDA(cudaMemcpy(fit_wout[t].p, wo.data(), wo.size() * 8, cudaMemcpyHostToDevice));
+    b_out[t] = f.b_out;
+  }
+  d_max_nbr.ensure(n_types);
+  DPB_CUDA(cudaMemcpy(d_max_nbr.p, max_nbr.data(), n_types * sizeof(int), cudaMemcpyHostToDevice));
+  err.ensure(1);
+  counters.ensure(3);
+  red.ensure(256 * 10 + 64);
+  DPB_CUDA(cudaMemset(err.p, 0, sizeof(int)));
+  DPB_CUDA(cudaMemset(counters.p, 0, 3 * sizeof(unsigned long long)));
+  DPB_CUDA(cudaMemset(red.p, 0, 64 * sizeof(double)));
+}
+
+void Engine::destroy() {
+  if (stream) cudaStreamSynchronize(stream);
+  auto rel = [](auto& v) {
+    for (auto& b : v) b.release();
+  };
+  tab.release(); tab32.release(); rel(fit_wt); rel(fit_w); rel(fit_b); rel(fit_wout);
+  d_max_nbr.release(); tanh_tab.release(); pos4.release(); pos3.release(); vel3.release();
+  types.release(); slot_of.release(); atom_of.release(); row_off.release(); keys.release();
+  rev.release(); bin_of.release(); bin_start.release(); bin_atoms.release(); bin_fill.release();
+  frac.release(); ref_pos.release(); row_len.release(); nl_len.release(); scan_tmp.release();
+  skeys.release(); n_real.release(); T.release(); D.release(); dD.release(); rel(act_t);
+  rel(act_y); dz.release(); dy.release(); dz2.release(); dy2.release(); e_slot.release();
+  e_atom.release(); g.release(); fcenter.release(); vpart.release(); forces.release();
+  red.release(); counters.release(); err.release(); acc_fac.release();
+  if (stream) cudaStreamDestroy(stream);
+  stream = nullptr;
+}
+
+void Engine::set_config(int64_t nn, const double* pos, const int32_t* ty, const double* box,
+                        const uint8_t* pbc) {
+  // validate_config (geom.cpp:40-56) and Cell::refresh (geom.cpp:7-29)
+  if (nn <= 0) throw InputErr("configuration has no atoms");
+  if (!pos || !ty || !box || !pbc) throw InputErr("null configuration array");
+  for (int64_t i = 0; i < nn; ++i)
+    if (ty[i] < 0 || ty[i] >= n_types) throw InputErr("atom type id out of range");
+  for (int64_t k = 0; k < 3 * nn; ++k)
+    if (!std::isfinite(pos[k])) throw InputErr("non-finite atom position");
+  DevCell c{};
+  for (int k = 0; k < 9; ++k) c.h[k] = box[k];
+  for (int k = 0; k < 3; ++k) c.per[k] = pbc[k] ? 1 : 0;
+  const double* a = c.h;
+  const double* b = c.h + 3;
+  const double* cc = c.h + 6;
+  const double bxc[3] = {b[1] * cc[2] - b[2] * cc[1], b[2] * cc[0] - b[0] * cc[2], b[0] * cc[1] - b[1] * cc[0]};
+  double vol = a[0] * bxc[0] + a[1] * bxc[1] + a[2] * bxc[2];
+  if (!(std::fabs(vol) > 1e-12)) throw InputErr("cell is singular or has near-zero volume");
+  const double cxa[3] = {cc[1] * a[2] - cc[2] * a[1], cc[2] * a[0] - cc[0] * a[2], cc[0] * a[1] - cc[1] * a[0]};
+  const double axb[3] = {a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0]};
+  for (int x = 0; x < 3; ++x) {
+    c.hinv[3 * x + 0] = bxc[x] / vol;
+    c.hinv[3 * x + 1] = cxa[x] / vol;
+    c.hinv[3 * x + 2] = axb[x] / vol;
+  }
+  c.vol = vol < 0.0 ? -vol : vol;
+  bool same = nn == n && std::memcmp(c.h, cell.h, sizeof(c.h)) == 0 &&
+              std::memcmp(c.per, cell.per, sizeof(c.per)) == 0 &&
+              static_cast<int64_t>(h_types.size()) == nn &&
+              std::memcmp(h_types.data(), ty, nn * sizeof(int32_t)) == 0;
+  cell = c;
+  if (!same) {
+    n = nn;
+    list_valid = false;
+    h_types.assign(ty, ty + nn);
+    types.ensure(n);
+    DPB_CUDA(cudaMemcpyAsync(types.p, ty, n * sizeof(int32_t), cudaMemcpyHostToDevice, stream));
+    // slots: atoms grouped by centre type, each segment padded to the GEMM tile (64 rows)
+    seg_count.assign(n_types, 0);
+    for (int64_t i = 0; i < n; ++i) ++seg_count[ty[i]];
+    seg_start.assign(n_types, 0);
+    seg_rows.assign(n_types, 0);
+    int64_t at = 0;
+    for (int t = 0; t < n_types; ++t) {
+      seg_start[t] = static_cast<int>(at);
+      seg_rows[t] = round_up(seg_count[t], 64);
+      at += seg_rows[t];
+    }
+    n_slots = at;
+    std::vector<int32_t> so(n), ao(n_slots, -1);
+    std::vector<int> fill(n_types, 0);
+    for (int64_t i = 0; i < n; ++i) {
+      const int t = ty[i];
+      const int s = seg_start[t] + fill[t]++;
+      so[i] = s;
+      ao[s] = static_cast<int32_t>(i);
+    }
+    slot_of.ensure(n);
+    atom_of.ensure(n_slots);
+    DPB_CUDA(cudaMemcpyAsync(slot_of.p, so.data(), n * 4, cudaMemcpyHostToDevice, stream));
+    DPB_CUDA(cudaMemcpyAsync(atom_of.p, ao.data(), n_slots * 4, cudaMemcpyHostToDevice, stream));
+    ensure_step_buffers();
+    DPB_CUDA(cudaStreamSynchronize(stream));
+  }
+  upload_positions(pos);
+}
+
+void Engine::ensure_step_buffers() {
+  const int L = static_cast<int>(layers.size());
+  T.ensure(static_cast<size_t>(n) * 4 * Mp);
+  const size_t dsz = static_cast<size_t>(n_slots) * K0p;
+  const bool grow = D.n < dsz;
+  D.ensure(dsz);
+  dD.ensure(dsz);
+  if (grow || true) DPB_CUDA(cudaMemsetAsync(D.p, 0, D.n * sizeof(double), stream));
+  act_t.resize(L);
+  act_y.resize(L);
+  const size_t asz = static_cast<size_t>(n_slots) * widthp_max;
+  for (int k = 0; k < L; ++k) {
+    act_t[k].ensure(asz);
+    act_y[k].ensure(asz);
+  }
+  dz.ensure(asz); dy.ensure(asz); dz2.ensure(asz); dy2.ensure(asz);
+  e_slot.ensure(n_slots);
+  e_atom.ensure(n);
+  fcenter.ensure(3 * n);
+  vpart.ensure(9 * n);
+  forces.ensure(3 * n);
+  n_real.ensure(n);
+  pos4.ensure(n);
+  pos3.ensure(3 * n);
+}
+
+void Engine::upload_positions(const double* pos) {
+  DPB_CUDA(cudaMemcpyAsync(pos3.p, pos, 3 * n * sizeof(double), cudaMemcpyHostToDevice, stream));
+  launch_pos4(*this);
+}
+
+void Engine::build_list(double cutoff) {
+  launch_nlist(cutoff);
+  skeys.ensure(n_entries + 1);
+  g.ensure(3 * n_entries + 3);
+}
+
+void Engine::evaluate() {
+  if (!list_valid) throw InputErr("no neighbour list");
+  launch_tab_fwd();
+  launch_fitting();
+  launch_tab_bwd();
+  launch_forces();
+}
+
+void Engine::check_err() {
+  int code = 0;
+  DPB_CUDA(cudaMemcpyAsync(&code, err.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  DPB_CUDA(cudaStreamSynchronize(stream));
+  DPB_CUDA(cudaGetLastError());
+  if (code) {
+    DPB_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), stream));
+    list_valid = false;
+    raise_device_error(code);
+  }
+}
+
+void Engine::reset_counters() {
+  DPB_CUDA(cudaMemsetAsync(counters.p, 0, 3 * sizeof(unsigned long long), stream));
+}
+
+void Engine::read_counters() {
+  unsigned long long c[3];
+  DPB_CUDA(cudaMemcpyAsync(c, counters.p, sizeof(c), cudaMemcpyDeviceToHost, stream));
+  DPB_CUDA(cudaStreamSynchronize(stream));
+  host_counters.rows_forward = c[0];
+  host_counters.rows_backward = c[1];
+  host_counters.extrapolations = c[2];
+}
+
+void Engine::fetch_results(double* energy, double* f, double* virial, double* atom_energy) {
+  double r[10];
+  DPB_CUDA(cudaMemcpyAsync(r, red.p, sizeof(r), cudaMemcpyDeviceToHost, stream));
+  if (f) DPB_CUDA(cudaMemcpyAsync(f, forces.p, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, stream));
+  if (atom_energy)
+    DPB_CUDA(cudaMemcpyAsync(atom_energy, e_atom.p, n * sizeof(double), cudaMemcpyDeviceToHost, stream));
+  DPB_CUDA(cudaStreamSynchronize(stream));
+  if (energy) *energy = r[0];
+  if (virial)
+    for (int k = 0; k < 9; ++k) virial[k] = r[1 + k];
+}
+
+double Engine::max_drift() { return host_max_drift(*this); }
+
+// ---------------------------------------------------------------- MD (md.cpp:151-231)
+
+void Engine::md_begin(const double* pos, const double* vel, const dp_md_config* cfg) {
+  (void)pos;
+  if (!(cfg->dt > 0.0)) throw InputErr("time step must be positive");
+  if (cfg->n_steps < 0) throw InputErr("step count must be non-negative");
+  if (cfg->rebuild_every < 1 || cfg->thermo_every < 1)
+    throw InputErr("rebuild and thermo intervals must be at least 1");
+  if (!(cfg->buffer >= 0.0)) throw InputErr("buffer must be non-negative");
+  md = *cfg;
+  MdScratch& S = scratch;
+  std::vector<double> m(n), af(n);
+  for (int64_t i = 0; i < n; ++i) {
+    m[i] = masses[h_types[i]];
+    af[i] = units::EVA_PER_MASS_TO_ACC / m[i];
+  }
+  S.mass_atom.ensure(n);
+  S.ke.ensure(n);
+  acc_fac.ensure(n);
+  vel3.ensure(3 * n);
+  DPB_CUDA(cudaMemcpyAsync(S.mass_atom.p, m.data(), n * 8, cudaMemcpyHostToDevice, stream));
+  DPB_CUDA(cudaMemcpyAsync(acc_fac.p, af.data(), n * 8, cudaMemcpyHostToDevice, stream));
+  DPB_CUDA(cudaMemcpyAsync(vel3.p, vel, 3 * n * 8, cudaMemcpyHostToDevice, stream));
+  const int64_t n_rec = cfg->n_steps / cfg->thermo_every + 1;
+  S.rec.ensure(n_rec + 1);
+  S.n_rec = 0;
+  md_res = dp_md_result{};
+  DPB_CUDA(cudaMemsetAsync(red.p + 11, 0, sizeof(double), stream)); // max drift seen
+  reset_counters();
+  build_list(r_cut + md.buffer);
+  evaluate();
+  md_res.force_evals = 1;
+  launch_thermo(*this, 0, S.rec.p + S.n_rec++, S.mass_atom.p, S.ke.p);
+  md_step = 0;
+  md_active = true;
+  check_err();
+}
+
+void Engine::md_steps(int64_t k) {
+  if (!md_active) throw InputErr("no MD run in progress");
+  MdScratch& S = scratch;
+  const double half = 0.5 * md.dt;
+  for (int64_t it = 0; it < k; ++it) {
+    const int64_t s = ++md_step;
+    launch_kick_drift(*this, half, md.dt);
+    if (s % md.rebuild_every == 0) build_list(r_cut + md.buffer);
+    launch_stale_check(*this, 0.5 * md.buffer);
+    ++md_res.staleness_checks;
+    evaluate();
+    ++md_res.force_evals;
+    launch_kick(*this, half);
+    if (s % md.thermo_every == 0) launch_thermo(*this, s, S.rec.p + S.n_rec++, S.mass_atom.p, S.ke.p);
+  }
+}
+
+void Engine::md_record(int64_t, bool) {}
+
+void Engine::md_end(double* pos, double* vel) {
+  MdScratch& S = scratch;
+  md_active = false;
+  check_err();
+  thermo.resize(S.n_rec);
+  if (S.n_rec)
+    DPB_CUDA(cudaMemcpyAsync(thermo.data(), S.rec.p, S.n_rec * sizeof(dp_thermo), cudaMemcpyDeviceToHost, stream));
+  if (pos) DPB_CUDA(cudaMemcpyAsync(pos, pos3.p, 3 * n * 8, cudaMemcpyDeviceToHost, stream));
+  if (vel) DPB_CUDA(cudaMemcpyAsync(vel, vel3.p, 3 * n * 8, cudaMemcpyDeviceToHost, stream));
+  // final KE/PE (md.cpp:227-229)
+  DevBuf<dp_thermo> fin;
+  fin.ensure(1);
+  launch_thermo(*this, md_step, fin.p, S.mass_atom.p, S.ke.p);
+  dp_thermo ft;
+  double seen = 0.0;
+  DPB_CUDA(cudaMemcpyAsync(&ft, fin.p, sizeof(ft), cudaMemcpyDeviceToHost, stream));
+  DPB_CUDA(cudaMemcpyAsync(&seen, red.p + 11, sizeof(double), cudaMemcpyDeviceToHost, stream));
+  DPB_CUDA(cudaStreamSynchronize(stream));
+  fin.release();
+  read_counters();
+  md_res.max_drift_seen = seen;
+  md_res.counters = host_counters;
+  md_res.final_ke = ft.ke;
+  md_res.final_pe = ft.pe;
+  md_res.final_total = ft.ke + ft.pe;
+}
+
+} // namespace dpb

@@ -1,0 +1,181 @@
+// Engine: device-resident state of one dp_handle and the launchers of every kernel.
+// HBM layout:
+//   pos4[n]            double4 (x, y, z, 0): one 32-byte sector per neighbour gather
+//   types[n]           int32
+//   row_off[n+1]       int64 CSR offsets of the neighbour rows (list cutoff = r_cut + skin)
+//   keys[E]            uint64 packed (type_j, j, shift) -- rows sorted = type-sectored canonical
+//   rev[E]             int32 position of the reverse entry (j -> i, -s) inside row j
+//   skeys[E]           uint64 per-step real neighbours of each row sorted by (type, interval)
+//   T[n][4][Mp]        contraction T = sum_k R_k (x) G(s_k)
+//   D/dD[slots][K0p]   descriptor rows (fitting input / its gradient), slot = type-sorted atom
+//   act[...]           fitting activations (t_k, y_k) and adjoints (dz_k, dy_k) per layer
+//   g[E]               double3 pair gradient dE_i/dd_ij at the list entry (0 if not real)
+//   vpart[n][9]        per-centre virial partials, reduced in a fixed order
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "dp_b200.h"
+
+namespace dpb {
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void ensure(size_t count) {
+    if (count <= n) return;
+    release();
+    size_t want = count + count / 8 + 64;
+    DPB_CUDA(cudaMalloc(&p, want * sizeof(T)));
+    n = want;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+struct FitLayer {
+  int in = 0, out = 0;   // real widths
+  int inp = 0, outp = 0; // padded widths
+  bool shortcut = false;
+};
+
+struct Engine {
+  // ---- model (immutable after create) ----
+  int precision = 0;
+  int device = 0;
+  int n_types = 0;
+  double r_cut = 0, r_smooth = 0;
+  int d1 = 0, M = 0, Mp = 0, mlt = 0, K0 = 0, K0p = 0;
+  std::vector<double> masses;
+  std::vector<int> max_nbr;
+  std::vector<FitLayer> layers; // same structure for every centre type
+  int widthp_max = 0;
+  // tables, device layout [type][interval][6][Mp]
+  double tab_x0 = 0, tab_h = 0;
+  uint64_t tab_n = 0;
+  DevBuf<double> tab;
+  DevBuf<float> tab32; // mixed mode copy
+  // fitting weights per type and layer: wt = W^T [outp][inp], w = W [inp][outp]
+  std::vector<DevBuf<double>> fit_wt, fit_w, fit_b;
+  std::vector<DevBuf<double>> fit_wout;
+  std::vector<double> b_out;
+  DevBuf<int> d_max_nbr;
+  DevBuf<double> tanh_tab;
+
+  // ---- configuration ----
+  int64_t n = 0;
+  DevCell cell{};
+  DevBuf<double4> pos4;
+  DevBuf<double> pos3; // AoS host layout mirror (MD state)
+  DevBuf<double> vel3;
+  DevBuf<int32_t> types;
+  std::vector<int32_t> h_types;
+  std::vector<int> seg_start, seg_count, seg_rows; // slots per centre type (padded to 64)
+  int64_t n_slots = 0;
+  DevBuf<int32_t> slot_of; // atom -> slot
+  DevBuf<int32_t> atom_of; // slot -> atom (-1 for padding)
+
+  // ---- neighbour list ----
+  double list_cutoff = 0;
+  bool list_valid = false;
+  int64_t n_entries = 0;
+  int max_row = 0;
+  DevBuf<int64_t> row_off;
+  DevBuf<uint64_t> keys;
+  DevBuf<int32_t> rev;
+  DevBuf<int32_t> bin_of, bin_start, bin_atoms, bin_fill;
+  DevBuf<double> frac;
+  DevBuf<double> ref_pos;
+  DevBuf<int> row_len;
+  DevBuf<int64_t> nl_len;
+  DevBuf<unsigned char> scan_tmp;
+
+  // ---- per-step buffers ----
+  DevBuf<uint64_t> skeys;
+  DevBuf<int32_t> n_real;
+  DevBuf<double> T;
+  DevBuf<double> D, dD;
+  std::vector<DevBuf<double>> act_t, act_y; // per layer [slots][outp]
+  DevBuf<double> dz, dy, dz2, dy2;
+  DevBuf<double> e_slot, e_atom;
+  DevBuf<double> g;
+  DevBuf<double> fcenter;
+  DevBuf<double> vpart;
+  DevBuf<double> forces;
+  DevBuf<double> red; // reduction scratch: energy, virial[9], drift...
+  DevBuf<unsigned long long> counters; // rows_forward, rows_backward, extrapolations
+  DevBuf<int> err;
+
+  cudaStream_t stream = nullptr;
+  uint64_t launches = 0;
+  std::string last_error;
+  dp_counters host_counters{};
+
+  // ---- MD state ----
+  dp_md_config md{};
+  bool md_active = false;
+  int64_t md_step = 0;
+  std::vector<dp_thermo> thermo;
+  dp_md_result md_res{};
+  DevBuf<double> acc_fac;
+  struct MdScratch {
+    DevBuf<double> mass_atom, ke;
+    DevBuf<dp_thermo> rec;
+    int64_t n_rec = 0;
+  } scratch;
+
+  // lifecycle
+  void create(const dp_model_desc* md, const dp_table_desc* td, int device, int precision);
+  void destroy();
+  // configuration upload (host AoS positions); resets the list when n/types/box change
+  void set_config(int64_t n, const double* pos, const int32_t* types, const double* box,
+                  const uint8_t* pbc);
+  void upload_positions(const double* pos);
+  // neighbour list at `cutoff`, device resident
+  void build_list(double cutoff);
+  void download_list(int64_t* offsets, int32_t* j, int32_t* shift);
+  // one evaluation on the current positions/list; results stay on device
+  void evaluate();
+  void fetch_results(double* energy, double* forces, double* virial, double* atom_energy);
+  double max_drift(); // device reduction, synchronizes
+  void check_err();   // synchronizes and raises on device error
+  void reset_counters();
+  void read_counters();
+  // kernels (defined in the .cu files)
+  void launch_nlist(double cutoff);
+  void launch_tab_fwd();
+  void launch_fitting();
+  void launch_tab_bwd();
+  void launch_forces();
+  // MD
+  void md_begin(const double* pos, const double* vel, const dp_md_config* cfg);
+  void md_steps(int64_t k);
+  void md_record(int64_t step, bool sync_read);
+  void md_end(double* pos, double* vel);
+  void ensure_step_buffers();
+};
+
+// Small launch helpers.
+inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+// force.cu
+void launch_pos4(Engine& E);
+void launch_kick_drift(Engine& E, double half, double dt);
+void launch_kick(Engine& E, double half);
+void launch_stale_check(Engine& E, double half_buffer);
+double host_max_drift(Engine& E);
+void launch_thermo(Engine& E, int64_t step, dp_thermo* dst, double* mass_atom, double* ke_scratch);
+
+} // namespace dpb

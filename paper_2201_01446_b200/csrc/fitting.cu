@@ -1,0 +1,284 @@
+// Fitting net forward + backward on the FP64 tensor pipe.
+//
+// Reference: fitting_forward model.cpp:151-180 (z = b + x W, t = tanh z, y = [in==out] x + t,
+// E = b_out + y . w_out) and fitting_backward model.cpp:182-203 (dz = dy (1 - t^2),
+// dx = [in==out] dy + W dz). The reference walks one centre at a time as GEMVs; here all
+// centres of one type form the M dimension of dense GEMMs:
+//   forward layer k   Y_k = X_k W_k        [slots x in] . [in x out]     epilogue: +b, tanh, shortcut
+//   readout           E = Y_L w_out + b_out, dZ_L = w_out (1 - T_L^2)
+//   backward layer k  dY_{k-1} = dZ_k W_k^T (+ dY_k)                      epilogue: * (1 - T_{k-1}^2)
+//   layer 0           dD = dZ_0 W_0^T
+// FP64 has no tcgen05 kind, so the MMA is the FP64 tensor instruction (mma.sync m8n8k4 f64 ->
+// SASS DMMA.8x8x4), measured at 37.1 TFLOP/s on this B200 (profiles/r01_fp64_peak_microbench.log).
+// Tiles: CTA 64x64, BK 16, 4 warps of 32x32 (4x4 DMMA tiles), 3-stage cp.async pipeline; both
+// operands K-contiguous in shared memory with a 20-double row pitch (bank-conflict free).
+#include "engine.hpp"
+
+namespace dpb {
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16, PITCH = BK + 4, STAGES = 3;
+
+enum Epi : int { EPI_FWD = 0, EPI_BWD = 1 };
+
+struct GemmArgs {
+  const double* A;  // [M][lda], K-contiguous
+  const double* Bt; // [N][ldb], K-contiguous
+  int lda, ldb, K;
+  // forward epilogue
+  const double* bias; // [N]
+  const double* xin;  // shortcut source [M][ldx] or null
+  double* tout;       // tanh output [M][ldc]
+  double* yout;       // layer output [M][ldc]
+  // backward epilogue
+  const double* dyin; // shortcut adjoint [M][ldc] or null
+  const double* tprev;// tanh output of the previous layer [M][ldc] or null
+  double* dyout;      // [M][ldc]
+  double* dzout;      // [M][ldc] or null
+  int ldc, ldx, ldd; // ldd: pitch of dyin / tprev / dzout
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(128) k_gemm(GemmArgs g) {
+  extern __shared__ __align__(16) double sm[];
+  double* As = sm;                                // [STAGES][BM][PITCH]
+  double* Bs = sm + STAGES * BM * PITCH;          // [STAGES][BN][PITCH]
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const double* A = g.A + static_cast<size_t>(m0) * g.lda;
+  const double* B = g.Bt + static_cast<size_t>(n0) * g.ldb;
+  const int KT = g.K / BK;
+
+  auto load_stage = [&](int stage, int kt) {
+    const int k0 = kt * BK;
+    double* as = As + stage * BM * PITCH;
+    double* bs = Bs + stage * BN * PITCH;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int idx = tid + c * 128; // 512 chunks of 2 doubles per operand
+      const int row = idx >> 3, col = (idx & 7) * 2;
+      cp_async16(as + row * PITCH + col, A + static_cast<size_t>(row) * g.lda + k0 + col);
+      cp_async16(bs + row * PITCH + col, B + static_cast<size_t>(row) * g.ldb + k0 + col);
+    }
+  };
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) load_stage(s, s);
+    cp_commit();
+  }
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    const int nk = kt + STAGES - 1;
+    if (nk < KT) load_stage(nk % STAGES, nk);
+    cp_commit();
+    const double* as = As + (kt % STAGES) * BM * PITCH + (wm * 32 + gid) * PITCH + tig;
+    const double* bs = Bs + (kt % STAGES) * BN * PITCH + (wn * 32 + gid) * PITCH + tig;
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = as[i * 8 * PITCH + kk * 4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = bs[j * 8 * PITCH + kk * 4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_wait<0>();
+
+  // Epilogue: thread holds rows (m0 + wm*32 + i*8 + gid), cols (n0 + wn*32 + j*8 + 2*tig + {0,1}).
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = m0 + wm * 32 + i * 8 + gid;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int col = n0 + wn * 32 + j * 8 + 2 * tig;
+      const size_t o = static_cast<size_t>(row) * g.ldc + col;
+      if (EPI == EPI_FWD) {
+        const double2 b = *reinterpret_cast<const double2*>(g.bias + col);
+        const double t0 = tanh(acc[i][j][0] + b.x);
+        const double t1 = tanh(acc[i][j][1] + b.y);
+        double2 y = make_double2(t0, t1);
+        if (g.xin) {
+          const double2 x = *reinterpret_cast<const double2*>(g.xin + static_cast<size_t>(row) * g.ldx + col);
+          y.x = x.x + t0;
+          y.y = x.y + t1;
+        }
+        *reinterpret_cast<double2*>(g.tout + o) = make_double2(t0, t1);
+        *reinterpret_cast<double2*>(g.yout + o) = y;
+      } else {
+        double v0 = acc[i][j][0], v1 = acc[i][j][1];
+        if (g.dyin) {
+          const double2 d = *reinterpret_cast<const double2*>(g.dyin + static_cast<size_t>(row) * g.ldd + col);
+          v0 = d.x + v0;
+          v1 = d.y + v1;
+        }
+        *reinterpret_cast<double2*>(g.dyout + o) = make_double2(v0, v1);
+        if (g.dzout) {
+          const size_t od = static_cast<size_t>(row) * g.ldd + col;
+          const double2 t = *reinterpret_cast<const double2*>(g.tprev + od);
+          *reinterpret_cast<double2*>(g.dzout + od) =
+              make_double2(v0 * (1.0 - t.x * t.x), v1 * (1.0 - t.y * t.y));
+        }
+      }
+    }
+  }
+}
+
+// Readout: E = b_out + y . w_out (warp per row); dZ_L = w_out (1 - t^2); dY_L = w_out.
+__global__ void k_readout(int rows, int ld, int width, const double* __restrict__ y,
+                          const double* __restrict__ t, const double* __restrict__ wout,
+                          double bout, double* __restrict__ e, double* __restrict__ dz,
+                          double* __restrict__ dy) {
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const double* yr = y + static_cast<size_t>(r) * ld;
+  const double* tr = t + static_cast<size_t>(r) * ld;
+  double acc = 0.0;
+  for (int c = lane; c < ld; c += 32) {
+    const double w = c < width ? wout[c] : 0.0;
+    acc += yr[c] * w;
+    const double tt = tr[c];
+    dz[static_cast<size_t>(r) * ld + c] = w * (1.0 - tt * tt);
+    dy[static_cast<size_t>(r) * ld + c] = w;
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) e[r] = bout + acc;
+}
+
+__global__ void k_scatter_energy(int64_t slots, const int32_t* __restrict__ atom_of,
+                                 const double* __restrict__ e_slot, double* __restrict__ e_atom) {
+  const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (s >= slots) return;
+  const int a = atom_of[s];
+  if (a >= 0) e_atom[a] = e_slot[s];
+}
+
+void run_gemm(int epi, const GemmArgs& a, int rows, int N, cudaStream_t st) {
+  const size_t bytes = static_cast<size_t>(STAGES) * (BM + BN) * PITCH * sizeof(double);
+  dim3 grid(N / BN, rows / BM);
+  if (epi == EPI_FWD) {
+    static bool init = false;
+    if (!init) {
+      DPB_CUDA(cudaFuncSetAttribute(k_gemm<EPI_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(bytes)));
+      init = true;
+    }
+    k_gemm<EPI_FWD><<<grid, 128, bytes, st>>>(a);
+  } else {
+    static bool init = false;
+    if (!init) {
+      DPB_CUDA(cudaFuncSetAttribute(k_gemm<EPI_BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(bytes)));
+      init = true;
+    }
+    k_gemm<EPI_BWD><<<grid, 128, bytes, st>>>(a);
+  }
+  DPB_CUDA(cudaGetLastError());
+}
+
+} // namespace
+
+void Engine::launch_fitting() {
+  const int L = static_cast<int>(layers.size());
+  const int wpm = widthp_max;
+  for (int t = 0; t < n_types; ++t) {
+    const int rows = seg_rows[t];
+    if (rows == 0) continue;
+    const size_t r0 = static_cast<size_t>(seg_start[t]);
+    // forward
+    const double* x = D.p + r0 * K0p;
+    int ldx = K0p;
+    for (int k = 0; k < L; ++k) {
+      const FitLayer& fl = layers[k];
+      GemmArgs a{};
+      a.A = x;
+      a.lda = ldx;
+      a.Bt = fit_wt[t * L + k].p;
+      a.ldb = fl.inp;
+      a.K = fl.inp;
+      a.bias = fit_b[t * L + k].p;
+      a.xin = fl.shortcut ? x : nullptr;
+      a.ldx = ldx;
+      a.tout = act_t[k].p + r0 * wpm;
+      a.yout = act_y[k].p + r0 * wpm;
+      a.ldc = wpm;
+      run_gemm(EPI_FWD, a, rows, fl.outp, stream);
+      ++launches;
+      x = a.yout;
+      ldx = wpm;
+    }
+    // readout
+    const FitLayer& last = layers[L - 1];
+    double* dzc = dz.p + r0 * wpm;
+    double* dyc = dy.p + r0 * wpm;
+    double* dzn = dz2.p + r0 * wpm;
+    double* dyn = dy2.p + r0 * wpm;
+    k_readout<<<ceil_div(rows, 4), 128, 0, stream>>>(rows, wpm, last.out, act_y[L - 1].p + r0 * wpm,
+                                                     act_t[L - 1].p + r0 * wpm, fit_wout[t].p,
+                                                     b_out[t], e_slot.p + r0, dzc, dyc);
+    ++launches;
+    // backward
+    for (int k = L - 1; k >= 0; --k) {
+      const FitLayer& fl = layers[k];
+      GemmArgs a{};
+      a.A = dzc;
+      a.lda = wpm;
+      a.Bt = fit_w[t * L + k].p; // W [inp][outp]: K = outp contiguous
+      a.ldb = fl.outp;
+      a.K = fl.outp;
+      a.dyin = fl.shortcut ? dyc : nullptr;
+      a.ldd = wpm;
+      if (k > 0) {
+        a.tprev = act_t[k - 1].p + r0 * wpm;
+        a.dyout = dyn;
+        a.dzout = dzn;
+        a.ldc = wpm;
+      } else {
+        a.tprev = nullptr;
+        a.dyout = dD.p + r0 * K0p;
+        a.dzout = nullptr;
+        a.ldc = K0p;
+      }
+      run_gemm(EPI_BWD, a, rows, fl.inp, stream);
+      ++launches;
+      std::swap(dzc, dzn);
+      std::swap(dyc, dyn);
+    }
+  }
+  k_scatter_energy<<<ceil_div(n_slots, 256), 256, 0, stream>>>(n_slots, atom_of.p, e_slot.p, e_atom.p);
+  ++launches;
+}
+
+} // namespace dpb

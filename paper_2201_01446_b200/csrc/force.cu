@@ -1,0 +1,232 @@
+// prod_force / prod_virial with scatter-free ownership, fixed-order reductions, and the
+// device-resident velocity-Verlet pieces.
+//
+// Reference scatter (exact.cpp:22-38): for every centre i and real slot k with neighbour j,
+//   F_i += g, F_j -= g, Xi[3x+y] += d_x g_y.
+// Every list entry (i -> j, s) has its mirror (j -> i, -s) in row j (the list is symmetric,
+// neighbor.cpp:76-79, :147-150), and g is stored per list entry (0 when the env-mat filter
+// dropped it), so each atom can GATHER its force without atomics:
+//   F_i = sum_{e in row i} g[e] - sum_{e in row i} g[rev(e)]
+// in a fixed order. The centre term is summed inside the tabulate backward kernel.
+#include "engine.hpp"
+
+namespace dpb {
+
+namespace {
+
+__global__ void k_forces(int n, const int64_t* __restrict__ row_off, const uint64_t* __restrict__ keys,
+                         const int32_t* __restrict__ rev, const double* __restrict__ g,
+                         const double* __restrict__ fcenter, double* __restrict__ f) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double fx = 0.0, fy = 0.0, fz = 0.0;
+  for (int64_t e = row_off[i]; e < row_off[i + 1]; ++e) {
+    const int j = key_j(keys[e]);
+    const int64_t m = row_off[j] + rev[e];
+    fx += g[3 * m];
+    fy += g[3 * m + 1];
+    fz += g[3 * m + 2];
+  }
+  f[3 * i] = fcenter[3 * i] - fx;
+  f[3 * i + 1] = fcenter[3 * i + 1] - fy;
+  f[3 * i + 2] = fcenter[3 * i + 2] - fz;
+}
+
+// Deterministic two-level reduction of `width` interleaved columns over n rows.
+constexpr int RED_BLOCKS = 256;
+constexpr int RED_THREADS = 256;
+
+__global__ void k_reduce_cols(int64_t n, int width, const double* __restrict__ x, int ld,
+                              double* __restrict__ partial) {
+  __shared__ double sh[RED_THREADS];
+  const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = blockIdx.x * chunk;
+  const int64_t hi = min(n, lo + chunk);
+  for (int c = 0; c < width; ++c) {
+    double s = 0.0;
+    for (int64_t r = lo + threadIdx.x; r < hi; r += blockDim.x) s += x[r * ld + c];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = blockDim.x >> 1; o > 0; o >>= 1) {
+      if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x * width + c] = sh[0];
+    __syncthreads();
+  }
+}
+
+__global__ void k_reduce_final(int nb, int width, const double* __restrict__ partial,
+                               double* __restrict__ out) {
+  __shared__ double sh[RED_BLOCKS];
+  for (int c = 0; c < width; ++c) {
+    sh[threadIdx.x] = threadIdx.x < nb ? partial[threadIdx.x * width + c] : 0.0;
+    __syncthreads();
+    for (int o = blockDim.x >> 1; o > 0; o >>= 1) {
+      if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[c] = sh[0];
+    __syncthreads();
+  }
+}
+
+__global__ void k_pos4(int64_t n, const double* __restrict__ p3, double4* __restrict__ p4) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  p4[i] = make_double4(p3[3 * i], p3[3 * i + 1], p3[3 * i + 2], 0.0);
+}
+
+// First half kick and drift (md.cpp:205-208): v += (dt/2 F) acc, x += dt v.
+__global__ void k_kick_drift(int64_t n, double half, double dt, const double* __restrict__ f,
+                             const double* __restrict__ accf, double* __restrict__ v,
+                             double* __restrict__ x, double4* __restrict__ p4) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  double r[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const double vv = __dadd_rn(v[3 * i + c], __dmul_rn(__dmul_rn(half, f[3 * i + c]), accf[i]));
+    v[3 * i + c] = vv;
+    r[c] = __dadd_rn(x[3 * i + c], __dmul_rn(dt, vv));
+    x[3 * i + c] = r[c];
+  }
+  p4[i] = make_double4(r[0], r[1], r[2], 0.0);
+}
+
+// Second half kick (md.cpp:220-222).
+__global__ void k_kick(int64_t n, double half, const double* __restrict__ f,
+                       const double* __restrict__ accf, double* __restrict__ v) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+    v[3 * i + c] = __dadd_rn(v[3 * i + c], __dmul_rn(__dmul_rn(half, f[3 * i + c]), accf[i]));
+}
+
+// max_i |x_i - x_i^ref|^2 (md.cpp:136-147) via integer max on the non-negative bit pattern.
+__global__ void k_drift2(int64_t n, const double* __restrict__ x, const double* __restrict__ ref,
+                         unsigned long long* out) {
+  unsigned long long best = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double d2 = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double d = __dsub_rn(x[3 * i + c], ref[3 * i + c]);
+      d2 = __dadd_rn(d2, __dmul_rn(d, d));
+    }
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(d2));
+    best = b > best ? b : best;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+    best = t > best ? t : best;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(out, best);
+}
+
+// Staleness guard (md.cpp:211-217): drift = sqrt(max d2); track the maximum; flag if stale.
+__global__ void k_stale_check(const unsigned long long* d2bits, double half_buffer,
+                              double* max_seen, int* err) {
+  const double drift = sqrt(__longlong_as_double(static_cast<long long>(*d2bits)));
+  if (drift > *max_seen) *max_seen = drift;
+  if (drift > half_buffer) raise_err(err, DEV_STALE);
+}
+
+// Kinetic energy per atom: 0.5 m v^2 MVV (md.cpp:172-178).
+__global__ void k_ke_atoms(int64_t n, const double* __restrict__ v, const double* __restrict__ mass,
+                           double mvv, double* __restrict__ ke) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double v2 = v[3 * i] * v[3 * i] + v[3 * i + 1] * v[3 * i + 1] + v[3 * i + 2] * v[3 * i + 2];
+  ke[i] = 0.5 * mass[i] * v2 * mvv;
+}
+
+// Thermo record (md.cpp:179-189) from device reductions: red = [E, Xi(9)], ke_sum.
+__global__ void k_thermo(int64_t step, int64_t n, double vol, const double* __restrict__ red,
+                         const double* __restrict__ ke_sum, dp_thermo* out) {
+  const double kB = 8.617333262e-5;
+  const double bar = 1.602176634e6;
+  dp_thermo t;
+  t.step = step;
+  t.ke = ke_sum[0];
+  t.pe = red[0];
+  t.temperature = 2.0 * t.ke / (3.0 * static_cast<double>(n) * kB);
+  const double trv = red[1] + red[5] + red[9];
+  t.pressure = (2.0 * t.ke + trv) / (3.0 * vol) * bar;
+  *out = t;
+}
+
+} // namespace
+
+void Engine::launch_forces() {
+  const int N = static_cast<int>(n);
+  forces.ensure(3 * n);
+  k_forces<<<ceil_div(N, 128), 128, 0, stream>>>(N, row_off.p, keys.p, rev.p, g.p, fcenter.p, forces.p);
+  ++launches;
+  // energy (1 column) then virial (9 columns) with fixed-order tree reductions
+  red.ensure(RED_BLOCKS * 10 + 64);
+  double* partial = red.p + 64;
+  const int nb = static_cast<int>(std::min<int64_t>(RED_BLOCKS, std::max<int64_t>(1, n / 64)));
+  k_reduce_cols<<<nb, RED_THREADS, 0, stream>>>(n, 1, e_atom.p, 1, partial);
+  k_reduce_final<<<1, RED_BLOCKS, 0, stream>>>(nb, 1, partial, red.p);
+  k_reduce_cols<<<nb, RED_THREADS, 0, stream>>>(n, 9, vpart.p, 9, partial);
+  k_reduce_final<<<1, RED_BLOCKS, 0, stream>>>(nb, 9, partial, red.p + 1);
+  launches += 4;
+}
+
+void launch_pos4(Engine& E) {
+  k_pos4<<<ceil_div(E.n, 256), 256, 0, E.stream>>>(E.n, E.pos3.p, E.pos4.p);
+  ++E.launches;
+}
+
+void launch_kick_drift(Engine& E, double half, double dt) {
+  k_kick_drift<<<ceil_div(E.n, 256), 256, 0, E.stream>>>(E.n, half, dt, E.forces.p, E.acc_fac.p,
+                                                         E.vel3.p, E.pos3.p, E.pos4.p);
+  ++E.launches;
+}
+
+void launch_kick(Engine& E, double half) {
+  k_kick<<<ceil_div(E.n, 256), 256, 0, E.stream>>>(E.n, half, E.forces.p, E.acc_fac.p, E.vel3.p);
+  ++E.launches;
+}
+
+// red layout: [0] E, [1..9] virial, [10] ke, [11] max drift seen, [12..13] drift bits scratch,
+// [14..63] free; partials after 64.
+void launch_stale_check(Engine& E, double half_buffer) {
+  unsigned long long* bits = reinterpret_cast<unsigned long long*>(E.red.p + 12);
+  DPB_CUDA(cudaMemsetAsync(bits, 0, sizeof(unsigned long long), E.stream));
+  const int blocks = std::max(1, std::min(ceil_div(E.n, 256), 1184));
+  k_drift2<<<blocks, 256, 0, E.stream>>>(E.n, E.pos3.p, E.ref_pos.p, bits);
+  k_stale_check<<<1, 1, 0, E.stream>>>(bits, half_buffer, E.red.p + 11, E.err.p);
+  E.launches += 2;
+}
+
+double host_max_drift(Engine& E) {
+  E.red.ensure(RED_BLOCKS * 10 + 64);
+  unsigned long long* bits = reinterpret_cast<unsigned long long*>(E.red.p + 12);
+  DPB_CUDA(cudaMemsetAsync(bits, 0, sizeof(unsigned long long), E.stream));
+  const int blocks = std::max(1, std::min(ceil_div(E.n, 256), 1184));
+  k_drift2<<<blocks, 256, 0, E.stream>>>(E.n, E.pos3.p, E.ref_pos.p, bits);
+  ++E.launches;
+  unsigned long long h = 0;
+  DPB_CUDA(cudaMemcpyAsync(&h, bits, sizeof(h), cudaMemcpyDeviceToHost, E.stream));
+  DPB_CUDA(cudaStreamSynchronize(E.stream));
+  double d2;
+  std::memcpy(&d2, &h, sizeof(d2));
+  return std::sqrt(d2);
+}
+
+void launch_thermo(Engine& E, int64_t step, dp_thermo* dst, double* mass_atom, double* ke_scratch) {
+  k_ke_atoms<<<ceil_div(E.n, 256), 256, 0, E.stream>>>(E.n, E.vel3.p, mass_atom, units::MVV_TO_EV,
+                                                       ke_scratch);
+  double* partial = E.red.p + 64;
+  const int nb = static_cast<int>(std::min<int64_t>(RED_BLOCKS, std::max<int64_t>(1, E.n / 64)));
+  k_reduce_cols<<<nb, RED_THREADS, 0, E.stream>>>(E.n, 1, ke_scratch, 1, partial);
+  k_reduce_final<<<1, RED_BLOCKS, 0, E.stream>>>(nb, 1, partial, E.red.p + 10);
+  k_thermo<<<1, 1, 0, E.stream>>>(step, E.n, E.cell.vol, E.red.p, E.red.p + 10, dst);
+  E.launches += 4;
+}
+
+} // namespace dpb

@@ -1,0 +1,330 @@
+// nlist_build: bit-exact GPU neighbour list.
+//
+// Reference: build_neighbor_list neighbor.cpp:162-179, brute scan :63-84 with scan_images
+// :23-48, linked cells :88-158, canonical sort :10-17. Both reference paths accept exactly the
+// images (j, s) with |d|^2 <= cutoff^2 where d is evaluated ONCE per pair from the lower index
+// (cells: q > i half walk; brute: i <= j) and mirrored with -s into the other row. This kernel
+// reproduces that rule: every candidate pair is evaluated from min(i, j) with the reference's
+// image range and un-fused arithmetic, so entries are bitwise identical whatever the binning.
+// Rows are sorted by the packed key (type_j, j, shift) -- the stable type partition of the
+// canonical order, which is the env-mat slot order (env_mat.cpp:25, 36-41).
+#include <cub/cub.cuh>
+
+#include "engine.hpp"
+
+namespace dpb {
+
+namespace {
+
+struct NlParams {
+  DevCell c;
+  double cut2;
+  double margin[3];
+  int nb[3];
+  int full[3]; // 1: visit every bin along the axis (fewer than 3 bins), 0: 3-bin stencil
+  int n;
+};
+
+__device__ __forceinline__ void frac_exact(const DevCell& c, double3 r, double* f) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    f[k] = __dadd_rn(__dadd_rn(__dmul_rn(r.x, c.hinv[k]), __dmul_rn(r.y, c.hinv[3 + k])),
+                     __dmul_rn(r.z, c.hinv[6 + k]));
+}
+
+__global__ void k_frac_bin(NlParams p, const double4* __restrict__ pos, double* __restrict__ frac,
+                           int* __restrict__ bin_of, int* __restrict__ bin_count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p.n) return;
+  double f[3];
+  frac_exact(p.c, ld_pos(pos, i), f);
+  int b[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    frac[3 * i + k] = f[k];
+    if (p.c.per[k] && p.nb[k] > 1) {
+      const double fl = floor(f[k]);
+      int bk = static_cast<int>(__dmul_rn(__dsub_rn(f[k], fl), static_cast<double>(p.nb[k])));
+      b[k] = min(max(bk, 0), p.nb[k] - 1);
+    } else {
+      b[k] = 0;
+    }
+  }
+  const int bin = (b[0] * p.nb[1] + b[1]) * p.nb[2] + b[2];
+  bin_of[i] = bin;
+  atomicAdd(bin_count + bin, 1);
+}
+
+__global__ void k_bin_fill(int n, const int* __restrict__ bin_of, const int* __restrict__ bin_start,
+                           int* __restrict__ bin_fill, int* __restrict__ bin_atoms) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int b = bin_of[i];
+  bin_atoms[bin_start[b] + atomicAdd(bin_fill + b, 1)] = i;
+}
+
+// One thread per centre. WRITE=false counts entries, WRITE=true emits unsorted keys.
+template <bool WRITE>
+__global__ void k_nlist_pass(NlParams p, const double4* __restrict__ pos,
+                             const double* __restrict__ frac, const int32_t* __restrict__ types,
+                             const int* __restrict__ bin_of, const int* __restrict__ bin_start,
+                             const int* __restrict__ bin_atoms, int64_t* __restrict__ row_len,
+                             const int64_t* __restrict__ row_off, uint64_t* __restrict__ keys,
+                             int* err) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p.n) return;
+  const int bi = bin_of[i];
+  const int bc[3] = {bi / (p.nb[1] * p.nb[2]), (bi / p.nb[2]) % p.nb[1], bi % p.nb[2]};
+  int cnt[3], first[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (p.full[k]) {
+      cnt[k] = p.nb[k];
+      first[k] = 0;
+    } else {
+      cnt[k] = 3;
+      first[k] = bc[k] - 1;
+    }
+  }
+  const double3 ri = ld_pos(pos, i);
+  const double fi[3] = {frac[3 * i], frac[3 * i + 1], frac[3 * i + 2]};
+  int64_t count = 0;
+  const int64_t base = WRITE ? row_off[i] : 0;
+  for (int o0 = 0; o0 < cnt[0]; ++o0) {
+    const int q0 = (first[0] + o0 + p.nb[0]) % p.nb[0];
+    for (int o1 = 0; o1 < cnt[1]; ++o1) {
+      const int q1 = (first[1] + o1 + p.nb[1]) % p.nb[1];
+      for (int o2 = 0; o2 < cnt[2]; ++o2) {
+        const int q2 = (first[2] + o2 + p.nb[2]) % p.nb[2];
+        const int q = (q0 * p.nb[1] + q1) * p.nb[2] + q2;
+        const int qe = bin_start[q + 1];
+        for (int idx = bin_start[q]; idx < qe; ++idx) {
+          const int j = bin_atoms[idx];
+          const bool i_low = i <= j;
+          const int a = i_low ? i : j;
+          const int b = i_low ? j : i;
+          const double3 rj = ld_pos(pos, j);
+          const double3 ra = i_low ? ri : rj;
+          const double3 rb = i_low ? rj : ri;
+          int lo[3], hi[3];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            if (p.c.per[k]) {
+              const double fa = i_low ? fi[k] : frac[3 * a + k];
+              const double fb = i_low ? frac[3 * b + k] : fi[k];
+              const double df = __dsub_rn(fb, fa);
+              lo[k] = static_cast<int>(ceil(__dsub_rn(__dsub_rn(-df, p.margin[k]), 1e-12)));
+              hi[k] = static_cast<int>(floor(__dadd_rn(__dadd_rn(-df, p.margin[k]), 1e-12)));
+            } else {
+              lo[k] = hi[k] = 0;
+            }
+          }
+          for (int s0 = lo[0]; s0 <= hi[0]; ++s0)
+            for (int s1 = lo[1]; s1 <= hi[1]; ++s1)
+              for (int s2 = lo[2]; s2 <= hi[2]; ++s2) {
+                if (a == b && s0 == 0 && s1 == 0 && s2 == 0) continue;
+                double d[3];
+                disp_exact(p.c, ra, rb, s0, s1, s2, d);
+                if (norm2_exact(d) <= p.cut2) {
+                  if (WRITE) {
+                    const int e0 = i_low ? s0 : -s0, e1 = i_low ? s1 : -s1,
+                              e2 = i_low ? s2 : -s2;
+                    if (e0 < -511 || e0 > 511 || e1 < -511 || e1 > 511 || e2 < -511 || e2 > 511)
+                      raise_err(err, DEV_SHIFT_RANGE);
+                    keys[base + count] = make_key(types[j], j, e0, e1, e2);
+                  }
+                  ++count;
+                }
+              }
+        }
+      }
+    }
+  }
+  if (!WRITE) row_len[i] = count;
+}
+
+// One block per row: bitonic sort of the row's keys in shared memory.
+__global__ void k_sort_rows(int n, const int64_t* __restrict__ row_off, uint64_t* __restrict__ keys,
+                            int cap, int* err) {
+  extern __shared__ uint64_t sk[];
+  const int i = blockIdx.x;
+  if (i >= n) return;
+  const int64_t off = row_off[i];
+  const int len = static_cast<int>(row_off[i + 1] - off);
+  if (len > cap) {
+    if (threadIdx.x == 0) raise_err(err, DEV_ROW_CAP);
+    return;
+  }
+  if (len < 2) return;
+  int P = 2;
+  while (P < len) P <<= 1;
+  for (int t = threadIdx.x; t < P; t += blockDim.x) sk[t] = t < len ? keys[off + t] : ~0ull;
+  __syncthreads();
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      for (int t = threadIdx.x; t < P; t += blockDim.x) {
+        const int u = t ^ jj;
+        if (u > t) {
+          const uint64_t x = sk[t], y = sk[u];
+          const bool up = (t & k) == 0;
+          if ((x > y) == up) {
+            sk[t] = y;
+            sk[u] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int t = threadIdx.x; t < len; t += blockDim.x) keys[off + t] = sk[t];
+}
+
+// Position of the reverse entry (j -> i, -s) in row j, by binary search in the sorted row.
+__global__ void k_reverse(int n, const int64_t* __restrict__ row_off, const uint64_t* __restrict__ keys,
+                          const int32_t* __restrict__ types, int32_t* __restrict__ rev, int* err) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int ti = types[i];
+  for (int64_t e = row_off[i]; e < row_off[i + 1]; ++e) {
+    const uint64_t k = keys[e];
+    const int j = key_j(k);
+    const uint64_t want = reverse_key(k, ti, i);
+    int64_t lo = row_off[j], hi = row_off[j + 1];
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (keys[mid] < want)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    if (lo >= row_off[j + 1] || keys[lo] != want) {
+      raise_err(err, DEV_ROW_CAP);
+      rev[e] = 0;
+    } else {
+      rev[e] = static_cast<int32_t>(lo - row_off[j]);
+    }
+  }
+}
+
+__global__ void k_max_len(int n, const int64_t* __restrict__ row_len, int* out) {
+  int m = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    m = max(m, static_cast<int>(row_len[i]));
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+double host_spacing(const DevCell& c, int k) {
+  const double* u = c.h + 3 * ((k + 1) % 3);
+  const double* v = c.h + 3 * ((k + 2) % 3);
+  const double cr[3] = {u[1] * v[2] - u[2] * v[1], u[2] * v[0] - u[0] * v[2],
+                        u[0] * v[1] - u[1] * v[0]};
+  return c.vol / std::sqrt(cr[0] * cr[0] + cr[1] * cr[1] + cr[2] * cr[2]);
+}
+
+} // namespace
+
+void Engine::launch_nlist(double cutoff) {
+  if (!(cutoff > 0.0)) throw InputErr("neighbor cutoff must be positive");
+  if (n >= (1ll << 28)) throw InputErr("too many atoms for the packed neighbour key (2^28)");
+  NlParams p;
+  p.c = cell;
+  p.cut2 = cutoff * cutoff;
+  p.n = static_cast<int>(n);
+  int64_t nbins = 1;
+  for (int k = 0; k < 3; ++k) {
+    p.margin[k] = cutoff / host_spacing(cell, k);
+    int nb = 1;
+    if (cell.per[k]) {
+      const double want = std::floor(host_spacing(cell, k) / cutoff);
+      nb = static_cast<int>(std::min(want, 1024.0));
+      if (nb < 1) nb = 1;
+    }
+    p.nb[k] = nb;
+    p.full[k] = nb < 3 ? 1 : 0;
+    nbins *= nb;
+  }
+  const int N = p.n;
+  frac.ensure(3 * n);
+  bin_of.ensure(n);
+  bin_atoms.ensure(n);
+  bin_start.ensure(nbins + 1);
+  bin_fill.ensure(nbins + 1);
+  DevBuf<int64_t>& lens = nl_len;
+  lens.ensure(n + 1);
+  row_off.ensure(n + 1);
+  row_len.ensure(1);
+  DPB_CUDA(cudaMemsetAsync(bin_fill.p, 0, (nbins + 1) * sizeof(int), stream));
+  k_frac_bin<<<ceil_div(N, 256), 256, 0, stream>>>(p, pos4.p, frac.p, bin_of.p, bin_fill.p);
+  ++launches;
+  // exclusive scan of bin counts -> bin_start
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, bin_fill.p, bin_start.p, nbins + 1, stream);
+  DevBuf<unsigned char>& tmp = scan_tmp;
+  tmp.ensure(tmp_bytes + 1);
+  cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, bin_fill.p, bin_start.p, nbins + 1, stream);
+  ++launches;
+  DPB_CUDA(cudaMemsetAsync(bin_fill.p, 0, (nbins + 1) * sizeof(int), stream));
+  k_bin_fill<<<ceil_div(N, 256), 256, 0, stream>>>(N, bin_of.p, bin_start.p, bin_fill.p, bin_atoms.p);
+  ++launches;
+  k_nlist_pass<false><<<ceil_div(N, 128), 128, 0, stream>>>(p, pos4.p, frac.p, types.p, bin_of.p,
+                                                            bin_start.p, bin_atoms.p, lens.p,
+                                                            nullptr, nullptr, err.p);
+  ++launches;
+  DPB_CUDA(cudaMemsetAsync(lens.p + n, 0, sizeof(int64_t), stream));
+  size_t tmp2 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp2, lens.p, row_off.p, n + 1, stream);
+  tmp.ensure(tmp2 + 1);
+  cub::DeviceScan::ExclusiveSum(tmp.p, tmp2, lens.p, row_off.p, n + 1, stream);
+  ++launches;
+  DPB_CUDA(cudaMemsetAsync(row_len.p, 0, sizeof(int), stream));
+  k_max_len<<<std::min(ceil_div(N, 256), 1024), 256, 0, stream>>>(N, lens.p, row_len.p);
+  ++launches;
+  int64_t total = 0;
+  int mx = 0;
+  DPB_CUDA(cudaMemcpyAsync(&total, row_off.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+  DPB_CUDA(cudaMemcpyAsync(&mx, row_len.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  DPB_CUDA(cudaStreamSynchronize(stream));
+  n_entries = total;
+  max_row = mx;
+  keys.ensure(total + 1);
+  rev.ensure(total + 1);
+  k_nlist_pass<true><<<ceil_div(N, 128), 128, 0, stream>>>(p, pos4.p, frac.p, types.p, bin_of.p,
+                                                           bin_start.p, bin_atoms.p, nullptr,
+                                                           row_off.p, keys.p, err.p);
+  ++launches;
+  int cap = 2;
+  while (cap < mx) cap <<= 1;
+  if (cap > 8192) throw NumErr("neighbour row longer than 8192 entries");
+  k_sort_rows<<<N, 256, cap * sizeof(uint64_t), stream>>>(N, row_off.p, keys.p, cap, err.p);
+  ++launches;
+  k_reverse<<<ceil_div(N, 128), 128, 0, stream>>>(N, row_off.p, keys.p, types.p, rev.p, err.p);
+  ++launches;
+  ref_pos.ensure(3 * n);
+  DPB_CUDA(cudaMemcpyAsync(ref_pos.p, pos3.p, 3 * n * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+  list_cutoff = cutoff;
+  list_valid = true;
+}
+
+void Engine::download_list(int64_t* offsets, int32_t* jout, int32_t* shift) {
+  std::vector<int64_t> off(n + 1);
+  std::vector<uint64_t> k(n_entries);
+  DPB_CUDA(cudaMemcpyAsync(off.data(), row_off.p, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+  if (n_entries)
+    DPB_CUDA(cudaMemcpyAsync(k.data(), keys.p, n_entries * sizeof(uint64_t), cudaMemcpyDeviceToHost, stream));
+  DPB_CUDA(cudaStreamSynchronize(stream));
+  // Rows are stored type-sectored; the canonical order drops the type bits (neighbor.cpp:10-17).
+  for (int64_t i = 0; i < n; ++i) {
+    offsets[i] = off[i];
+    std::vector<uint64_t> row(k.begin() + off[i], k.begin() + off[i + 1]);
+    for (auto& x : row) x &= ~(63ull << 58);
+    std::sort(row.begin(), row.end());
+    for (size_t e = 0; e < row.size(); ++e) {
+      jout[off[i] + e] = key_j(row[e]);
+      key_shift(row[e], shift + 3 * (off[i] + e));
+    }
+  }
+  offsets[n] = off[n];
+}
+
+} // namespace dpb
