@@ -1,0 +1,335 @@
+#!/usr/bin/env python
+"""Benchmark: MD atom-steps/s (Cu, FP64) of the B200-native Deep Potential step.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c3|c5]
+
+Workload (BASELINE.json configs[1], "C2"): copper-like DP-SE model gen_model(seed 7) with random
+weights, compression tables h = 0.01, jittered FCC Cu 20x20x20 cells (32,000 atoms, seed 11),
+velocities 330 K (seed 99), velocity-Verlet NVE, dt = 1 fs, list buffer 2 A rebuilt every 50
+steps. A step = half kick + drift + (list rebuild on its cadence) + staleness check + full
+energy/force/virial evaluation + half kick -- the reference's run_md step (md.cpp:204-225).
+
+Arms:
+  ours       value: K device-resident MD steps timed with CUDA events on the library's stream;
+             e2e:   the same steps driven through the reference-facing C-ABI dp_compute with host
+                    (pinned) buffers: positions up, forces/energy/virial/atom energies down every
+                    step, host Verlet update (what a host MD code calling the operator does).
+  reference  the unmodified reference library (oracle/_ref, built from /root/reference) timing
+             compute_energy_forces_virial_tabulated on the same configuration with every host
+             thread, plus its cell-list build amortized over the 50-step rebuild cadence.
+Multi-GPU (torchrun): each rank owns its own C2-sized slab (weak scaling); see DESIGN.md §6.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    "c2": dict(cells=(20, 20, 20), label="C2: Cu FCC 20x20x20 (32,000 atoms) NVE MD step"),
+    "c3": dict(cells=(64, 64, 64), label="C3: Cu FCC 64x64x64 (1,048,576 atoms) NVE MD step"),
+    "c5": dict(cells=(100, 100, 100), label="C5: Cu FCC 100x100x100 (4,000,000 atoms) NVE MD step"),
+}
+MACS_FIT = None  # filled from the model shape
+
+
+def fitting_flops_per_atom(m) -> float:
+    s = m.shape
+    din = s.m_lt * 4 * s.d1
+    w = s.fit_width
+    fwd = din * w + (s.fit_hidden - 1) * w * w + w
+    bwd = (s.fit_hidden - 1) * w * w + din * w
+    return 2.0 * (fwd + bwd)
+
+
+def algorithmic_flops_per_atom(m, n_real: float) -> float:
+    """SURVEY.md §8d accounting: fitting fwd+bwd + 7,060 FLOP per real neighbour."""
+    return fitting_flops_per_atom(m) + 16384 + 32768 + 7060.0 * n_real
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if len(s) > 2 + k and s[2 + k].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", init_method="env://")
+    return world, rank, local, dist
+
+
+def max_over_ranks(x: float, dist) -> float:
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def cpu_reference_sample(cfg, m, t, threads: int, repeats: int = 1):
+    """Reference compute_energy_forces_virial_tabulated on the host (oracle/_ref if built)."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib as O
+    if O.have_ref():
+        r, cnt, secs = O.ref_compute(cfg, m, t, m.r_cut + 2.0, threads, repeats)
+        return {"kind": "reference", "eval_s": float(secs[1]), "list_s": float(secs[0]),
+                "cores": threads}
+    # fall back to the single-threaded restatement (port)
+    t0 = time.perf_counter()
+    O.or_compute(cfg, m, t, m.r_cut + 2.0)
+    return {"kind": "port", "eval_s": time.perf_counter() - t0, "list_s": 0.0, "cores": 1}
+
+
+def run_reference_arm(args, world, rank, dist):
+    import paper_2201_01446_b200 as dp
+    if rank != 0:
+        return
+    spec = CONFIGS[args.config]
+    m = dp.gen_model("copper-like", 7)
+    t = dp.build_tables(m, 0.01)
+    cfg = dp.gen_config("copper-like", *spec["cells"], 0.1, 11)
+    threads = os.cpu_count() or 1
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib as O
+    if not O.have_ref():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libdpref.so not built (build() needs /root/reference)"}))
+        return
+    times = []
+    for k in range(args.warmup + args.steps):
+        s = cpu_reference_sample(cfg, m, t, threads)
+        step = s["eval_s"] + s["list_s"] / 50.0
+        if k >= args.warmup:
+            times.append(step)
+    st = float(np.mean(times))
+    value = cfg.n_atoms / st
+    print(json.dumps({
+        "metric": "MD atom-steps/s (Cu, FP64)", "value": value, "unit": "atom-steps/s",
+        "impl": "reference", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": st * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": spec["label"], "atoms": cfg.n_atoms, "list": "cell list r_c+2 A amortized /50"},
+        "cpu_baseline": {"value": value, "unit": "atom-steps/s", "cores": threads, "kind": "reference",
+                         "sample": f"full {spec['label']} force evaluation per step, {threads} OpenMP threads"},
+        "e2e": {"value": value, "unit": "atom-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "ns_per_day": value / cfg.n_atoms * 0.0864,
+    }))
+
+
+def run_ours(args, world, rank, local, dist):
+    import torch
+    import paper_2201_01446_b200 as dp
+
+    spec = CONFIGS[args.config]
+    m = dp.gen_model("copper-like", 7)
+    t = dp.build_tables(m, 0.01)
+    cells = spec["cells"]
+    cfg = dp.gen_config("copper-like", *cells, 0.1, 11 + rank)
+    vel = dp.init_velocities(cfg, m, 330.0, 99 + rank)
+    n = cfg.n_atoms
+    pot = dp.DeepPot(m, t, device=local)
+    mc = dp.MDConfig(n_steps=args.warmup + args.steps + 10, dt=1.0, buffer=2.0, rebuild_every=50,
+                     thermo_every=10 ** 9)
+    pot.md_begin(cfg, vel, mc)
+    pot.md_step(args.warmup)
+    stream = torch.cuda.ExternalStream(pot.stream, device=torch.device("cuda", local))
+    torch.cuda.synchronize()
+    pot.set_timing(True)
+    pot.phase_times()
+    barrier(dist)
+    torch.cuda.synchronize()
+    l0 = pot.launch_count
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        pot.md_step(args.steps)
+        ev1.record(stream)
+        ev1.synchronize()
+    torch.cuda.synchronize()
+    barrier(dist)
+    launches = pot.launch_count - l0
+    ms = ev0.elapsed_time(ev1)
+    phases = pot.phase_times()
+    pot.set_timing(False)
+    res = pot.md_end()
+    ms_max = max_over_ranks(ms, dist)
+    step_ms = ms_max / args.steps
+    value = world * n * args.steps / (ms_max / 1e3)
+
+    # roofline of the dominant kernel group: the fitting-net FP64 DMMA GEMMs
+    fit_ms, fit_cnt = phases["fitting"]
+    fit_flop_launch = fitting_flops_per_atom(m) * n
+    fit_launch_ms = fit_ms / max(fit_cnt, 1)
+    achieved = fit_flop_launch / (fit_launch_ms / 1e3) / 1e12
+    peak = 37.15
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get("fitting_bytes_per_atom")
+            traffic = traffic * n if traffic else None
+        except Exception:
+            traffic = None
+    n_real = res.counters.rows_forward / max(res.force_evals, 1) / n
+    alg = algorithmic_flops_per_atom(m, n_real) * n
+    total_phase_ms = sum(v[0] for v in phases.values())
+
+    # e2e through the reference-facing operator with host buffers
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda shape: torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+        c2 = dp.AtomicConfig(cfg.pos, cfg.type, cfg.h)
+        pos = pin((n, 3)); pos[:] = cfg.pos
+        c2.pos = pos
+        v = pin((n, 3)); v[:] = vel
+        acc = (1.0 / (1.0e7 / (6.02214076e23 * 1.602176634e-19))) / m.masses[0]
+        pot.set_skin(2.0)
+        r = pot.compute(c2)
+        f = pin((n, 3)); f[:] = r.forces
+        ke = args.e2e_steps
+        for k in range(args.warmup + ke):
+            if k == args.warmup:
+                barrier(dist)
+                t0 = time.perf_counter()
+            v += 0.5 * f * acc
+            pos += v
+            r = pot.compute(c2, forces_out=f)
+            v += 0.5 * f * acc
+        el = time.perf_counter() - t0
+        el = max_over_ranks(el, dist)
+        e2e = {"value": world * n * ke / el, "unit": "atom-steps/s", "h2d_bytes_per_step": int(n * 24),
+               "d2h_bytes_per_step": int(n * 24 + n * 8 + 80), "steps": ke,
+               "api": "dp_compute (C-ABI) with pinned host buffers + host Verlet"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        s = cpu_reference_sample(dp.gen_config("copper-like", 8, 8, 8, 0.1, 11), m, t,
+                                 os.cpu_count() or 1, repeats=3)
+        v_cpu = 2048 / (s["eval_s"] + s["list_s"] / 50.0)
+        cpu = {"value": v_cpu, "unit": "atom-steps/s", "cores": s["cores"], "kind": s["kind"],
+               "sample": "C1 Cu 8x8x8 (2,048 atoms; per-atom cost is size independent) "
+                         "compute_energy_forces_virial_tabulated x3 + cell list /50"}
+    if rank == 0:
+        out = {
+            "metric": "MD atom-steps/s (Cu, FP64)", "value": value, "unit": "atom-steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": spec["label"], "atoms_per_gpu": n, "atoms_total": n * world,
+                       "model": "copper-like DP-SE, random weights (gen_model seed 7), tables h=0.01",
+                       "dt_fs": 1.0, "list": "r_c + 2 A, rebuilt every 50 steps",
+                       "parallelism": "dp%d independent slabs" % world if world > 1 else "single GPU",
+                       "l2": "working set per step > 1 GB (neighbour rows, descriptors), larger than the 126 MB L2"},
+            "ns_per_day": value / (n * world) * 0.0864,
+            "roofline": {"bound": "tensor", "kernel": "fitting-net FP64 DMMA GEMMs (k_gemm, 6 launches/step)",
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                         "peak_source": "measured DMMA.8x8x4 37.15 TFLOP/s (profiles/r01_fp64_peak_microbench.log); MEASURED_PEAKS.json has no FP64 entry",
+                         "traffic": traffic, "flop_per_launch_group": fit_flop_launch,
+                         "group_ms_per_step": fit_launch_ms},
+            "step_roofline": {"algorithmic_flop_per_atom_step": alg / n,
+                              "achieved_tflops": alg * args.steps / (ms / 1e3) / 1e12,
+                              "frac_of_fp64_peak": alg * args.steps / (ms / 1e3) / 1e12 / peak},
+            "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items()},
+            "phase_sum_ms_per_step": total_phase_ms / args.steps,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        if e2e:
+            out["e2e"] = e2e
+        if cpu:
+            out["cpu_baseline"] = cpu
+        print(json.dumps(out))
+    pot.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--e2e-steps", type=int, default=30)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world, rank, local, dist = dist_setup()
+    if args.impl == "reference":
+        run_reference_arm(args, world, rank, dist)
+    else:
+        run_ours(args, world, rank, local, dist)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

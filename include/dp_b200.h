@@ -152,6 +152,12 @@ int dp_md_end(dp_handle* h, double* pos, double* vel, dp_thermo* thermo, int64_t
 void* dp_stream(dp_handle* h);
 /* Number of kernels this handle has launched since creation. */
 uint64_t dp_launch_count(const dp_handle* h);
+/* Per-phase CUDA-event timing on the handle's stream (off by default). dp_phase_times
+ * synchronizes and returns accumulated milliseconds and interval counts for the phases
+ * 0 neighbour list, 1 env-mat + tabulate forward, 2 fitting net (DMMA GEMMs), 3 tabulate
+ * backward, 4 force gather + reductions, 5 integrator; then resets them. */
+int dp_set_timing(dp_handle* h, int enable);
+int dp_phase_times(dp_handle* h, double* ms /* 8 */, uint64_t* counts /* 8 */);
 
 /* ---- host-side fixture generators (CPU, deterministic, bit-identical to the reference) ---- */
 

@@ -135,6 +135,8 @@ def _lib():
         "dp_md_end": ([P, D, D, C.POINTER(_Thermo), I64, C.POINTER(I64), C.POINTER(_MDResult)], I),
         "dp_stream": ([P], P),
         "dp_launch_count": ([P], U64),
+        "dp_set_timing": ([P, I], I),
+        "dp_phase_times": ([P, D, C.POINTER(U64)], I),
         "dp_preset_get": ([C.c_char_p, C.POINTER(_Preset)], I),
         "dp_model_blob_size": ([C.POINTER(_Preset)], I64),
         "dp_gen_model": ([C.c_char_p, U64, D], I),
@@ -562,6 +564,17 @@ class DeepPot:
     @property
     def launch_count(self) -> int:
         return int(_lib().dp_launch_count(self._h))
+
+    PHASES = ("nlist", "tab_fwd", "fitting", "tab_bwd", "forces", "integrate")
+
+    def set_timing(self, enable: bool) -> None:
+        _check(_lib().dp_set_timing(self._h, int(enable)), self._h)
+
+    def phase_times(self) -> dict:
+        ms = np.zeros(8)
+        cnt = (C.c_uint64 * 8)()
+        _check(_lib().dp_phase_times(self._h, _dp(ms), cnt), self._h)
+        return {name: (float(ms[k]), int(cnt[k])) for k, name in enumerate(self.PHASES)}
 
     def compute(self, cfg: AtomicConfig, energy_out=None, forces_out=None) -> EvalResult:
         n = cfg.n_atoms

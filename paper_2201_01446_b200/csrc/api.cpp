@@ -147,4 +147,19 @@ void* dp_stream(dp_handle* h) { return h ? static_cast<void*>(h->eng.stream) : n
 
 uint64_t dp_launch_count(const dp_handle* h) { return h ? h->eng.launches : 0; }
 
+int dp_set_timing(dp_handle* h, int enable) {
+  if (!h) return DP_INPUT_ERROR;
+  return guard_call(&h->eng.last_error, [&] {
+    double ms[8];
+    uint64_t c[8];
+    if (h->eng.timing) h->eng.phase_collect(ms, c);
+    h->eng.timing = enable != 0;
+  });
+}
+
+int dp_phase_times(dp_handle* h, double* ms, uint64_t* counts) {
+  if (!h || !ms || !counts) return DP_INPUT_ERROR;
+  return guard_call(&h->eng.last_error, [&] { h->eng.phase_collect(ms, counts); });
+}
+
 } // extern "C"

@@ -165,6 +165,16 @@ void Engine::destroy() {
   rel(act_y); dz.release(); dy.release(); dz2.release(); dy2.release(); e_slot.release();
   e_atom.release(); g.release(); fcenter.release(); vpart.release(); forces.release();
   red.release(); counters.release(); err.release(); acc_fac.release();
+  for (auto& p : phase_ev) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  for (auto e : ev_pool) cudaEventDestroy(e);
+  phase_ev.clear();
+  ev_pool.clear();
+  scratch.mass_atom.release();
+  scratch.ke.release();
+  scratch.rec.release();
   if (stream) cudaStreamDestroy(stream);
   stream = nullptr;
 }
@@ -268,17 +278,68 @@ void Engine::upload_positions(const double* pos) {
 }
 
 void Engine::build_list(double cutoff) {
+  phase_begin(0);
   launch_nlist(cutoff);
+  phase_end();
   skeys.ensure(n_entries + 1);
   g.ensure(3 * n_entries + 3);
 }
 
 void Engine::evaluate() {
   if (!list_valid) throw InputErr("no neighbour list");
+  phase_begin(1);
   launch_tab_fwd();
+  phase_begin(2);
   launch_fitting();
+  phase_begin(3);
   launch_tab_bwd();
+  phase_begin(4);
   launch_forces();
+  phase_end();
+}
+
+void Engine::phase_begin(int ph) {
+  if (!timing) return;
+  phase_end();
+  cudaEvent_t a, b;
+  if (ev_pool.size() >= 2) {
+    a = ev_pool.back();
+    ev_pool.pop_back();
+    b = ev_pool.back();
+    ev_pool.pop_back();
+  } else {
+    DPB_CUDA(cudaEventCreate(&a));
+    DPB_CUDA(cudaEventCreate(&b));
+  }
+  DPB_CUDA(cudaEventRecord(a, stream));
+  phase_ev.push_back({ph, a, b});
+  open_phase = static_cast<int>(phase_ev.size()) - 1;
+}
+
+void Engine::phase_end() {
+  if (!timing || open_phase < 0) return;
+  DPB_CUDA(cudaEventRecord(phase_ev[open_phase].b, stream));
+  open_phase = -1;
+}
+
+void Engine::phase_collect(double* ms, uint64_t* counts) {
+  phase_end();
+  DPB_CUDA(cudaStreamSynchronize(stream));
+  for (int k = 0; k < 8; ++k) {
+    ms[k] = 0.0;
+    counts[k] = 0;
+  }
+  for (auto& p : phase_ev) {
+    float t = 0.f;
+    DPB_CUDA(cudaEventElapsedTime(&t, p.a, p.b));
+    if (p.phase >= 0 && p.phase < 8) {
+      ms[p.phase] += t;
+      ++counts[p.phase];
+    }
+    ev_pool.push_back(p.a);
+    ev_pool.push_back(p.b);
+  }
+  phase_ev.clear();
 }
 
 void Engine::check_err() {
@@ -364,14 +425,20 @@ void Engine::md_steps(int64_t k) {
   const double half = 0.5 * md.dt;
   for (int64_t it = 0; it < k; ++it) {
     const int64_t s = ++md_step;
+    phase_begin(5);
     launch_kick_drift(*this, half, md.dt);
+    phase_end();
     if (s % md.rebuild_every == 0) build_list(r_cut + md.buffer);
+    phase_begin(5);
     launch_stale_check(*this, 0.5 * md.buffer);
+    phase_end();
     ++md_res.staleness_checks;
     evaluate();
     ++md_res.force_evals;
+    phase_begin(5);
     launch_kick(*this, half);
     if (s % md.thermo_every == 0) launch_thermo(*this, s, S.rec.p + S.n_rec++, S.mass_atom.p, S.ke.p);
+    phase_end();
   }
 }
 

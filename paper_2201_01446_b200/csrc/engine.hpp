@@ -120,6 +120,19 @@ struct Engine {
 
   cudaStream_t stream = nullptr;
   uint64_t launches = 0;
+  // optional per-phase CUDA-event timing (bench.py roofline): 0 nlist, 1 tab_fwd, 2 fitting,
+  // 3 tab_bwd, 4 forces+reductions, 5 integrator
+  bool timing = false;
+  struct PhaseEv {
+    int phase;
+    cudaEvent_t a, b;
+  };
+  std::vector<PhaseEv> phase_ev;
+  std::vector<cudaEvent_t> ev_pool;
+  int open_phase = -1;
+  void phase_begin(int ph);
+  void phase_end();
+  void phase_collect(double* ms, uint64_t* counts);
   std::string last_error;
   dp_counters host_counters{};
 

@@ -60,7 +60,12 @@ __device__ __forceinline__ long locate(const TabParams& p, double x, bool& ext, 
     ext = false;
     return 0;
   }
-  long th = static_cast<long>(floor(__ddiv_rn(__dsub_rn(x, p.x0), p.h)));
+  const double tf = floor(__ddiv_rn(__dsub_rn(x, p.x0), p.h));
+  if (!(tf < static_cast<double>(p.tn) + 2.0)) {  // far past the end (or inf): clamp directly
+    ext = true;
+    return p.tn - 1;
+  }
+  long th = static_cast<long>(tf);
   while (node_x(p.x0, p.h, th + 1) <= x) ++th;
   while (th > 0 && node_x(p.x0, p.h, th) > x) --th;
   ext = false;
@@ -203,9 +208,10 @@ __global__ void __launch_bounds__(128) k_tab_fwd(TabParams p) {
         double d[3];
         disp_exact(p.c, ri, ld_pos(p.pos, key_j(key)), sh[0], sh[1], sh[2], d);
         const double r2 = norm2_exact(d);
-        if (r2 < p.rc2) {
+        if (r2 < 1e-12) {
+          raise_err(p.err, DEV_OVERLAP);  // env_mat.cpp:33 throws before any table lookup
+        } else if (r2 < p.rc2) {
           real = true;
-          if (r2 < 1e-12) raise_err(p.err, DEV_OVERLAP);
           const double r = sqrt(r2);
           const double s = switch_fn(r, p.rs, p.rc) * (1.0 / r);
           const long th = locate(p, s, ext, p.err);
