@@ -161,9 +161,9 @@ void Engine::destroy() {
   types.release(); slot_of.release(); atom_of.release(); row_off.release(); keys.release();
   rev.release(); bin_of.release(); bin_start.release(); bin_atoms.release(); bin_fill.release();
   frac.release(); ref_pos.release(); row_len.release(); nl_len.release(); scan_tmp.release();
-  skeys.release(); n_real.release(); T.release(); D.release(); dD.release(); rel(act_t);
+  skeys.release(); eown.release(); ebin.release(); egrp.release(); erc.release(); n_grp.release(); goff.release(); Pbuf.release(); n_real.release(); T.release(); D.release(); dD.release(); rel(act_t);
   rel(act_y); dz.release(); dy.release(); dz2.release(); dy2.release(); e_slot.release();
-  e_atom.release(); g.release(); fcenter.release(); vpart.release(); forces.release();
+  e_atom.release(); g.release(); vpart.release(); forces.release();
   red.release(); counters.release(); err.release(); acc_fac.release();
   for (auto& p : phase_ev) {
     cudaEventDestroy(p.a);
@@ -264,10 +264,12 @@ void Engine::ensure_step_buffers() {
   dz.ensure(asz); dy.ensure(asz); dz2.ensure(asz); dy2.ensure(asz);
   e_slot.ensure(n_slots);
   e_atom.ensure(n);
-  fcenter.ensure(3 * n);
+
   vpart.ensure(9 * n);
   forces.ensure(3 * n);
   n_real.ensure(n);
+  n_grp.ensure(n + 1);
+  goff.ensure(n + 1);
   pos4.ensure(n);
   pos3.ensure(3 * n);
 }
@@ -282,6 +284,9 @@ void Engine::build_list(double cutoff) {
   launch_nlist(cutoff);
   phase_end();
   skeys.ensure(n_entries + 1);
+  ebin.ensure(n_entries + 1);
+  egrp.ensure(n_entries + 1);
+  erc.ensure(5 * n_entries + 5);
   g.ensure(3 * n_entries + 3);
 }
 

@@ -103,7 +103,13 @@ struct Engine {
   DevBuf<unsigned char> scan_tmp;
 
   // ---- per-step buffers ----
-  DevBuf<uint64_t> skeys;
+  DevBuf<uint64_t> skeys;      // [E] reals sorted by (type, interval)
+  DevBuf<int32_t> eown;         // [E] centre of each list entry
+  DevBuf<int32_t> ebin, egrp;   // [E] bin of real entries (-1 else), group index
+  DevBuf<double> erc;           // [5][E] per-entry R0..R3, u
+  DevBuf<int32_t> n_grp;        // [n+1]
+  DevBuf<int64_t> goff;         // [n+1]
+  DevBuf<double> Pbuf;          // [groups][24]
   DevBuf<int32_t> n_real;
   DevBuf<double> T;
   DevBuf<double> D, dD;
@@ -111,7 +117,7 @@ struct Engine {
   DevBuf<double> dz, dy, dz2, dy2;
   DevBuf<double> e_slot, e_atom;
   DevBuf<double> g;
-  DevBuf<double> fcenter;
+
   DevBuf<double> vpart;
   DevBuf<double> forces;
   DevBuf<double> red; // reduction scratch: energy, virial[9], drift...

@@ -7,29 +7,102 @@
 // neighbor.cpp:76-79, :147-150), and g is stored per list entry (0 when the env-mat filter
 // dropped it), so each atom can GATHER its force without atomics:
 //   F_i = sum_{e in row i} g[e] - sum_{e in row i} g[rev(e)]
-// in a fixed order. The centre term is summed inside the tabulate backward kernel.
+// in a fixed order.
 #include "engine.hpp"
 
 namespace dpb {
 
 namespace {
 
-__global__ void k_forces(int n, const int64_t* __restrict__ row_off, const uint64_t* __restrict__ keys,
-                         const int32_t* __restrict__ rev, const double* __restrict__ g,
-                         const double* __restrict__ fcenter, double* __restrict__ f) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+// One warp per atom: F_i = sum_{e in row i} g[e] - sum_{e in row i} g[rev(e)], and the
+// per-centre virial sum_e d_e (x) g_e with d_e re-evaluated exactly as the env-mat did.
+// Only real entries (ebin >= 0) contribute; the k-th real term of the row (in list order, which
+// filtering by cutoff preserves) is always summed by lane k mod 32, so the result is bitwise
+// independent of the list cutoff, as the reference's is (SURVEY.md §8.1 pitfall 1).
+__global__ void __launch_bounds__(256) k_forces(int n, DevCell c, const double4* __restrict__ pos,
+                                                const int64_t* __restrict__ row_off,
+                                                const uint64_t* __restrict__ keys,
+                                                const int32_t* __restrict__ rev,
+                                                const int32_t* __restrict__ ebin,
+                                                const double* __restrict__ g,
+                                                double* __restrict__ f, double* __restrict__ vpart) {
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (i >= n) return;
-  double fx = 0.0, fy = 0.0, fz = 0.0;
-  for (int64_t e = row_off[i]; e < row_off[i + 1]; ++e) {
-    const int j = key_j(keys[e]);
-    const int64_t m = row_off[j] + rev[e];
-    fx += g[3 * m];
-    fy += g[3 * m + 1];
-    fz += g[3 * m + 2];
+  const double3 ri = ld_pos(pos, i);
+  double acc[15];
+#pragma unroll
+  for (int k = 0; k < 15; ++k) acc[k] = 0.0;
+  const int64_t e0 = row_off[i], e1 = row_off[i + 1];
+  int co = 0, cr = 0;
+  for (int64_t base = e0; base < e1; base += 32) {
+    const int64_t e = base + lane;
+    const bool valid = e < e1;
+    double go[3] = {0.0, 0.0, 0.0}, gr[3] = {0.0, 0.0, 0.0}, d[3] = {0.0, 0.0, 0.0};
+    bool fo = false, fr = false;
+    if (valid) {
+      const uint64_t key = keys[e];
+      const int j = key_j(key);
+      const int64_t m = row_off[j] + rev[e];
+      fo = ebin[e] >= 0;
+      fr = ebin[m] >= 0;
+      if (fo) {
+        go[0] = g[3 * e];
+        go[1] = g[3 * e + 1];
+        go[2] = g[3 * e + 2];
+        int sh[3];
+        key_shift(key, sh);
+        disp_exact(c, ri, ld_pos(pos, j), sh[0], sh[1], sh[2], d);
+      }
+      if (fr) {
+        gr[0] = g[3 * m];
+        gr[1] = g[3 * m + 1];
+        gr[2] = g[3 * m + 2];
+      }
+    }
+    const unsigned mo = __ballot_sync(0xffffffffu, fo);
+    const unsigned mr = __ballot_sync(0xffffffffu, fr);
+    {
+      const int k = (lane - co) & 31;
+      const bool take = k < __popc(mo);
+      const int src = take ? static_cast<int>(__fns(mo, 0, k + 1)) : lane;
+      double v[6];
+#pragma unroll
+      for (int x = 0; x < 3; ++x) {
+        v[x] = __shfl_sync(0xffffffffu, go[x], src);
+        v[3 + x] = __shfl_sync(0xffffffffu, d[x], src);
+      }
+      if (take) {
+#pragma unroll
+        for (int x = 0; x < 3; ++x) acc[x] += v[x];
+#pragma unroll
+        for (int x = 0; x < 3; ++x)
+#pragma unroll
+          for (int y = 0; y < 3; ++y) acc[6 + 3 * x + y] += v[3 + x] * v[y];
+      }
+    }
+    {
+      const int k = (lane - cr) & 31;
+      const bool take = k < __popc(mr);
+      const int src = take ? static_cast<int>(__fns(mr, 0, k + 1)) : lane;
+      double v[3];
+#pragma unroll
+      for (int x = 0; x < 3; ++x) v[x] = __shfl_sync(0xffffffffu, gr[x], src);
+      if (take)
+#pragma unroll
+        for (int x = 0; x < 3; ++x) acc[3 + x] += v[x];
+    }
+    co += __popc(mo);
+    cr += __popc(mr);
   }
-  f[3 * i] = fcenter[3 * i] - fx;
-  f[3 * i + 1] = fcenter[3 * i + 1] - fy;
-  f[3 * i + 2] = fcenter[3 * i + 2] - fz;
+#pragma unroll
+  for (int k = 0; k < 15; ++k) acc[k] = warp_sum(acc[k]);
+  if (lane == 0) {
+#pragma unroll
+    for (int x = 0; x < 3; ++x) f[3 * i + x] = acc[x] - acc[3 + x];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) vpart[9 * static_cast<int64_t>(i) + k] = acc[6 + k];
+  }
 }
 
 // Deterministic two-level reduction of `width` interleaved columns over n rows.
@@ -163,7 +236,8 @@ __global__ void k_thermo(int64_t step, int64_t n, double vol, const double* __re
 void Engine::launch_forces() {
   const int N = static_cast<int>(n);
   forces.ensure(3 * n);
-  k_forces<<<ceil_div(N, 128), 128, 0, stream>>>(N, row_off.p, keys.p, rev.p, g.p, fcenter.p, forces.p);
+  k_forces<<<ceil_div(N, 8), 256, 0, stream>>>(N, cell, pos4.p, row_off.p, keys.p, rev.p, ebin.p,
+                                                g.p, forces.p, vpart.p);
   ++launches;
   // energy (1 column) then virial (9 columns) with fixed-order tree reductions
   red.ensure(RED_BLOCKS * 10 + 64);

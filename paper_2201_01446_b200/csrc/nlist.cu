@@ -70,7 +70,7 @@ __global__ void k_nlist_pass(NlParams p, const double4* __restrict__ pos,
                              const int* __restrict__ bin_of, const int* __restrict__ bin_start,
                              const int* __restrict__ bin_atoms, int64_t* __restrict__ row_len,
                              const int64_t* __restrict__ row_off, uint64_t* __restrict__ keys,
-                             int* err) {
+                             int32_t* __restrict__ eown, int* err) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= p.n) return;
   const int bi = bin_of[i];
@@ -132,6 +132,7 @@ __global__ void k_nlist_pass(NlParams p, const double4* __restrict__ pos,
                     if (e0 < -511 || e0 > 511 || e1 < -511 || e1 > 511 || e2 < -511 || e2 > 511)
                       raise_err(err, DEV_SHIFT_RANGE);
                     keys[base + count] = make_key(types[j], j, e0, e1, e2);
+                    eown[base + count] = i;
                   }
                   ++count;
                 }
@@ -269,7 +270,7 @@ void Engine::launch_nlist(double cutoff) {
   ++launches;
   k_nlist_pass<false><<<ceil_div(N, 128), 128, 0, stream>>>(p, pos4.p, frac.p, types.p, bin_of.p,
                                                             bin_start.p, bin_atoms.p, lens.p,
-                                                            nullptr, nullptr, err.p);
+                                                            nullptr, nullptr, nullptr, err.p);
   ++launches;
   DPB_CUDA(cudaMemsetAsync(lens.p + n, 0, sizeof(int64_t), stream));
   size_t tmp2 = 0;
@@ -289,9 +290,10 @@ void Engine::launch_nlist(double cutoff) {
   max_row = mx;
   keys.ensure(total + 1);
   rev.ensure(total + 1);
+  eown.ensure(total + 1);
   k_nlist_pass<true><<<ceil_div(N, 128), 128, 0, stream>>>(p, pos4.p, frac.p, types.p, bin_of.p,
                                                            bin_start.p, bin_atoms.p, nullptr,
-                                                           row_off.p, keys.p, err.p);
+                                                           row_off.p, keys.p, eown.p, err.p);
   ++launches;
   int cap = 2;
   while (cap < mx) cap <<= 1;

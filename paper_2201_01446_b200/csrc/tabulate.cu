@@ -16,7 +16,16 @@
 //             drow[a] = sum_m u^m P[a][m],  H'[a] = sum_m m u^(m-1) P[a][m],  ds = sum_a R[a] H'[a]
 // so the embedding matrix G is never formed (not even one row at a time), and each touched
 // coefficient block (6 x M doubles) is read once per centre instead of once per neighbour.
-// One warp per centre; lanes own features in the contraction and neighbours in the env-mat.
+//
+// Kernels (per evaluation):
+//   k_env_fwd    one thread per list entry: env-mat, real filter, interval, (R, u)   [parallel]
+//   k_tab_fwd    one warp per centre: stable counting sort of reals by (type, interval),
+//                group moments, T = W . C, D = T<^T T
+//   k_tab_bwd_P  one warp per centre: dT from dD, interval projections P per group
+//   k_tab_bwd_g  one thread per list entry: dE_i/dd_ij from P, written at the entry   [parallel]
+// All reductions have a fixed order, so results are bitwise reproducible run to run.
+#include <cub/cub.cuh>
+
 #include "engine.hpp"
 
 namespace dpb {
@@ -27,34 +36,40 @@ struct TabParams {
   const double4* pos;
   const int64_t* row_off;
   const uint64_t* keys;
-  uint64_t* skeys;
-  int32_t* n_real;
-  const double* tab; // [type][interval][6][Mp]
+  const int32_t* eown;  // [E] centre of each list entry
+  int32_t* ebin;        // [E] global bin t*tn + interval of a real entry, -1 otherwise
+  double* erc;          // [5][E] SoA: R0..R3, u of real entries
+  int32_t* egrp;        // [E] group index of a real entry inside its centre
+  uint64_t* skeys;      // [E] per row: reals sorted by bin, (bin << 32 | entry)
+  int32_t* n_real;      // [n]
+  int32_t* n_grp;       // [n+1] groups per centre -> (scanned) offsets into Pbuf
+  const int64_t* goff;  // [n+1] exclusive scan of n_grp
+  double* Pbuf;         // [sum groups][24]
+  const double* tab;    // [type][interval][6][Mp]
   const int* max_nbr;
   DevCell c;
   double rc2, rs, rc;
   double x0, h, x_end;
-  long tn;
+  int tn;
   int n, n_types, M, Mp, mlt, K0p;
+  int64_t E;
   const int32_t* slot_of;
-  double* T;  // [n][4][Mp]
-  double* D;  // [slots][K0p]
+  double* T;            // [n][4][Mp]
+  double* D;            // [slots][K0p]
   const double* dD;
-  double* g;        // [E][3]
-  double* fcenter;  // [n][3]
-  double* vpart;    // [n][9]
+  double* g;            // [E][3]
   unsigned long long* counters;
   int* err;
   int scap;
 };
 
-__device__ __forceinline__ double node_x(double x0, double h, long th) {
+__device__ __forceinline__ double node_x(double x0, double h, int th) {
   return __dadd_rn(x0, __dmul_rn(static_cast<double>(th), h));
 }
 
 // locate (table.cpp:20-32): floor, then nudge so node(th) <= x < node(th+1) in the exact
 // arithmetic of the nodes; clamp past the end and flag extrapolation.
-__device__ __forceinline__ long locate(const TabParams& p, double x, bool& ext, int* err) {
+__device__ __forceinline__ int locate(const TabParams& p, double x, bool& ext, int* err) {
   if (!(x >= p.x0)) {
     raise_err(err, DEV_TABLE_LOW);
     ext = false;
@@ -65,7 +80,7 @@ __device__ __forceinline__ long locate(const TabParams& p, double x, bool& ext, 
     ext = true;
     return p.tn - 1;
   }
-  long th = static_cast<long>(tf);
+  int th = static_cast<int>(tf);
   while (node_x(p.x0, p.h, th + 1) <= x) ++th;
   while (th > 0 && node_x(p.x0, p.h, th) > x) --th;
   ext = false;
@@ -109,127 +124,6 @@ __device__ __forceinline__ void env_of(const TabParams& p, double3 ri, uint64_t 
   e.sd = switch_deriv(e.r, p.rs, p.rc) * e.ir - w * e.ir * e.ir;
 #pragma unroll
   for (int x = 0; x < 3; ++x) e.u[x] = e.d[x] * e.ir;
-}
-
-// ---------------------------------------------------------------- per-warp shared memory
-// Forward: reals in list order (bin, entry, stable rank), sorted order, bin histogram, groups,
-// a cache of (R[4], u) for the first NC reals, one batch of group moments, and T for D.
-// Backward: sorted (bin, entry) keys, groups, one batch of interval projections P, T.
-constexpr int NC = 256;   // cached reals per centre (the rest are recomputed)
-constexpr int HCAP = 512; // counting-sort bins; wider ranges fall back to a bitonic sort
-constexpr int GB = 8;     // groups per batch
-
-struct FwdSmem {
-  uint32_t* rk;  // [scap] global bin t*tn + interval of real k
-  uint16_t* ex;  // [scap] list entry of real k
-  uint16_t* rn;  // [scap] stable rank of real k inside its bin
-  uint16_t* od;  // [scap] sorted position -> k
-  int* hs;       // [HCAP + 1] bin counts -> bin starts
-  int* gs;       // [gcap + 1] group start (sorted positions)
-  int* gb;       // [gcap] group bin
-  int* tc;       // [64] per-type real counts
-  double* W;     // [GB][24] moments of one batch
-  double* cache; // [5][NC] R0..R3, u  (aliased: bitonic scratch, then T copy)
-};
-
-__host__ __device__ __forceinline__ size_t align16(size_t b) { return (b + 15) & ~size_t(15); }
-
-__host__ __device__ __forceinline__ size_t fwd_cache_bytes(int scap, int Mp) {
-  size_t c = static_cast<size_t>(5) * NC * 8;
-  if (static_cast<size_t>(scap) * 8 > c) c = static_cast<size_t>(scap) * 8;
-  if (static_cast<size_t>(4) * Mp * 8 > c) c = static_cast<size_t>(4) * Mp * 8;
-  return c;
-}
-
-__host__ __device__ __forceinline__ int gcap_of(int scap) { return scap > HCAP ? scap : HCAP; }
-
-__host__ __device__ __forceinline__ size_t fwd_smem_bytes(int scap, int Mp) {
-  const int gcap = gcap_of(scap);
-  size_t b = fwd_cache_bytes(scap, Mp) + GB * 24 * 8;
-  b += static_cast<size_t>(scap) * (4 + 2 + 2 + 2);
-  b += static_cast<size_t>(HCAP + 1) * 4 + static_cast<size_t>(2 * gcap + 1) * 4 + 64 * 4;
-  return align16(b);
-}
-
-__device__ __forceinline__ FwdSmem carve_fwd(unsigned char* base, int scap, int Mp) {
-  FwdSmem w;
-  w.cache = reinterpret_cast<double*>(base);
-  unsigned char* p = base + fwd_cache_bytes(scap, Mp);
-  w.W = reinterpret_cast<double*>(p);
-  p += GB * 24 * 8;
-  w.rk = reinterpret_cast<uint32_t*>(p);
-  p += static_cast<size_t>(scap) * 4;
-  w.hs = reinterpret_cast<int*>(p);
-  p += (HCAP + 1) * 4;
-  const int gcap = gcap_of(scap);
-  w.gs = reinterpret_cast<int*>(p);
-  p += (gcap + 1) * 4;
-  w.gb = reinterpret_cast<int*>(p);
-  p += gcap * 4;
-  w.tc = reinterpret_cast<int*>(p);
-  p += 64 * 4;
-  w.ex = reinterpret_cast<uint16_t*>(p);
-  p += static_cast<size_t>(scap) * 2;
-  w.rn = reinterpret_cast<uint16_t*>(p);
-  p += static_cast<size_t>(scap) * 2;
-  w.od = reinterpret_cast<uint16_t*>(p);
-  return w;
-}
-
-struct BwdSmem {
-  uint64_t* sk; // [scap] sorted (bin << 32 | entry)
-  int* gs;      // [gcap + 1]
-  int* gb;      // [gcap]
-  double* P;    // [GB][24]
-  double* S;    // [m_lt <= 256][4] second term of dT
-  double* ts;   // [4][Mp]
-};
-
-__host__ __device__ __forceinline__ size_t bwd_smem_bytes(int scap, int Mp) {
-  const int gcap = gcap_of(scap);
-  size_t b = static_cast<size_t>(scap) * 8 + GB * 24 * 8 + 256 * 4 * 8 + static_cast<size_t>(4) * Mp * 8;
-  b += static_cast<size_t>(2 * gcap + 1) * 4;
-  return align16(b);
-}
-
-__device__ __forceinline__ BwdSmem carve_bwd(unsigned char* base, int scap, int Mp) {
-  BwdSmem w;
-  w.sk = reinterpret_cast<uint64_t*>(base);
-  unsigned char* p = base + static_cast<size_t>(scap) * 8;
-  w.P = reinterpret_cast<double*>(p);
-  p += GB * 24 * 8;
-  w.S = reinterpret_cast<double*>(p);
-  p += 256 * 4 * 8;
-  w.ts = reinterpret_cast<double*>(p);
-  p += static_cast<size_t>(4) * Mp * 8;
-  const int gcap = gcap_of(scap);
-  w.gs = reinterpret_cast<int*>(p);
-  p += (gcap + 1) * 4;
-  w.gb = reinterpret_cast<int*>(p);
-  return w;
-}
-
-// Warp bitonic sort of sk[0..n) ascending (pads to a power of two with ~0). Fallback only.
-__device__ void warp_sort(uint64_t* sk, int n, int lane) {
-  int P = 1;
-  while (P < n) P <<= 1;
-  for (int t = n + lane; t < P; t += 32) sk[t] = ~0ull;
-  __syncwarp();
-  for (int k = 2; k <= P; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int t = lane; t < P; t += 32) {
-        const int u = t ^ j;
-        if (u > t) {
-          const uint64_t x = sk[t], y = sk[u];
-          if ((x > y) == ((t & k) == 0)) {
-            sk[t] = y;
-            sk[u] = x;
-          }
-        }
-      }
-      __syncwarp();
-    }
-  }
 }
 
 __device__ __forceinline__ int warp_min(int v) {
@@ -308,11 +202,130 @@ __device__ __forceinline__ double rs32(double* v, int lane) {
   return v[0];
 }
 
-// Sort the nreal reals by bin (stable: list order inside a bin) and build the groups.
-// Returns the group count. Counting sort over [kmin, kmax] when it fits HCAP bins, otherwise
-// a bitonic sort of (bin, k) keys in the cache region (the cache is then unusable: *cache_ok=0).
-__device__ int sort_and_group(const FwdSmem& w, int nreal, int kmin, int kmax, int lane,
-                              bool* cache_ok) {
+
+// ---------------------------------------------------------------- k_env_fwd (thread per entry)
+__global__ void __launch_bounds__(256) k_env_fwd(TabParams p) {
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  bool ext = false;
+  if (e < p.E) {
+    const int i = p.eown[e];
+    const uint64_t key = p.keys[e];
+    int sh[3];
+    key_shift(key, sh);
+    double d[3];
+    disp_exact(p.c, ld_pos(p.pos, i), ld_pos(p.pos, key_j(key)), sh[0], sh[1], sh[2], d);
+    const double r2 = norm2_exact(d);
+    int bin = -1;
+    if (r2 < 1e-12) {
+      raise_err(p.err, DEV_OVERLAP); // env_mat.cpp:33 throws before any table lookup
+    } else if (r2 < p.rc2) {
+      const double r = sqrt(r2);
+      const double ir = 1.0 / r;
+      const double s = switch_fn(r, p.rs, p.rc) * ir;
+      const int th = locate(p, s, ext, p.err);
+      bin = key_type(key) * p.tn + th;
+      p.erc[e] = s;
+      p.erc[p.E + e] = s * (d[0] * ir);
+      p.erc[2 * p.E + e] = s * (d[1] * ir);
+      p.erc[3 * p.E + e] = s * (d[2] * ir);
+      p.erc[4 * p.E + e] = s - node_x(p.x0, p.h, th);
+    }
+    p.ebin[e] = bin;
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, ext);
+  if ((threadIdx.x & 31) == 0 && m) atomicAdd(p.counters + 2, static_cast<unsigned long long>(__popc(m)));
+}
+
+// ---------------------------------------------------------------- per-warp shared memory
+constexpr int HCAP = 256; // counting-sort bins; wider (type, interval) ranges use a bitonic sort
+constexpr int GB = 8;     // groups per batch
+
+struct FwdSmem {
+  uint32_t* rk; // [scap] bin of real k (list order)
+  uint16_t* ex; // [scap] entry of real k
+  uint16_t* rn; // [scap] stable rank of real k inside its bin
+  uint16_t* od; // [scap] sorted position -> k
+  int* hs;      // [HCAP + 1] bin counts -> bin starts
+  int* gs;      // [gcap + 1] group start (sorted position)
+  int* gb;      // [gcap] group bin
+  int* tc;      // [64] per-type real counts
+  double* W;    // [GB][24] moments of one batch
+  double* ts;   // [4][Mp] copy of T (aliases rk/rn/hs after the sort)
+};
+
+__host__ __device__ __forceinline__ size_t align16(size_t b) { return (b + 15) & ~size_t(15); }
+__host__ __device__ __forceinline__ int gcap_of(int scap) { return scap > HCAP ? scap : HCAP; }
+
+__host__ __device__ __forceinline__ size_t fwd_front_bytes(int scap, int Mp) {
+  const size_t front = static_cast<size_t>(scap) * (4 + 2) + (HCAP + 1) * 4;
+  const size_t tsb = static_cast<size_t>(4) * Mp * 8;
+  return align16(front > tsb ? front : tsb);
+}
+
+__host__ __device__ __forceinline__ size_t fwd_smem_bytes(int scap, int Mp) {
+  return align16(fwd_front_bytes(scap, Mp) + GB * 24 * 8 + static_cast<size_t>(scap) * 4 +
+                 static_cast<size_t>(2 * gcap_of(scap) + 1) * 4 + 64 * 4);
+}
+
+__device__ __forceinline__ FwdSmem carve_fwd(unsigned char* base, int scap, int Mp) {
+  FwdSmem w;
+  w.ts = reinterpret_cast<double*>(base);
+  w.rk = reinterpret_cast<uint32_t*>(base);
+  w.hs = reinterpret_cast<int*>(base + static_cast<size_t>(scap) * 4);
+  w.rn = reinterpret_cast<uint16_t*>(base + static_cast<size_t>(scap) * 4 + (HCAP + 1) * 4);
+  unsigned char* q = base + fwd_front_bytes(scap, Mp);
+  w.W = reinterpret_cast<double*>(q);
+  q += GB * 24 * 8;
+  w.gs = reinterpret_cast<int*>(q);
+  q += (gcap_of(scap) + 1) * 4;
+  w.gb = reinterpret_cast<int*>(q);
+  q += gcap_of(scap) * 4;
+  w.tc = reinterpret_cast<int*>(q);
+  q += 64 * 4;
+  w.od = reinterpret_cast<uint16_t*>(q);
+  q += static_cast<size_t>(scap) * 2;
+  w.ex = reinterpret_cast<uint16_t*>(q);
+  return w;
+}
+
+// Global-memory warp sort of a[0..n) ascending (fallback for wide bin ranges; rare). Bitonic
+// network in its all-ascending form (mirror stage + half cleaners), so the implicit +inf padding
+// up to the next power of two never moves and its comparisons can simply be skipped.
+__device__ void warp_sort_global(uint64_t* a, int n, int lane) {
+  int P = 1;
+  while (P < n) P <<= 1;
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int t = lane; t < P; t += 32) {
+      const int u = t ^ (k - 1);
+      if (u > t && u < n) {
+        const uint64_t x = a[t], y = a[u];
+        if (x > y) {
+          a[t] = y;
+          a[u] = x;
+        }
+      }
+    }
+    __syncwarp();
+    for (int j = k >> 2; j > 0; j >>= 1) {
+      for (int t = lane; t < P; t += 32) {
+        const int u = t ^ j;
+        if (u > t && u < n) {
+          const uint64_t x = a[t], y = a[u];
+          if (x > y) {
+            a[t] = y;
+            a[u] = x;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// Stable sort of the reals by bin: od[j] = real index at sorted position j, plus the group
+// table (gs, gb). Counting sort over [kmin, kmax] when it fits HCAP bins, else bitonic.
+__device__ int sort_and_group(const FwdSmem& w, uint64_t* scratch, int nreal, int kmin, int kmax,
+                              int lane) {
   if (nreal == 0) return 0;
   const int range = kmax - kmin + 1;
   int G = 0;
@@ -333,7 +346,6 @@ __device__ int sort_and_group(const FwdSmem& w, int nreal, int kmin, int kmax, i
       }
       __syncwarp();
     }
-    // exclusive scan of counts, segment per lane; groups = non-empty bins
     const int seg = (range + 31) / 32;
     const int b0 = min(lane * seg, range), b1 = min(b0 + seg, range);
     int sum = 0, ne = 0;
@@ -359,118 +371,85 @@ __device__ int sort_and_group(const FwdSmem& w, int nreal, int kmin, int kmax, i
     if (lane == 0) w.gs[G] = nreal;
     __syncwarp();
     for (int k = lane; k < nreal; k += 32) w.od[w.hs[w.rk[k] - kmin] + w.rn[k]] = static_cast<uint16_t>(k);
-    __syncwarp();
   } else {
-    *cache_ok = false;
-    uint64_t* sk = reinterpret_cast<uint64_t*>(w.cache);
-    for (int k = lane; k < nreal; k += 32) sk[k] = (static_cast<uint64_t>(w.rk[k]) << 16) | k;
-    warp_sort(sk, nreal, lane);
+    for (int k = lane; k < nreal; k += 32) scratch[k] = (static_cast<uint64_t>(w.rk[k]) << 32) | k;
+    __syncwarp();
+    warp_sort_global(scratch, nreal, lane);
     for (int base = 0; base < nreal; base += 32) {
-      const int k = base + lane;
+      const int j = base + lane;
       bool head = false;
-      if (k < nreal) {
-        w.od[k] = static_cast<uint16_t>(sk[k] & 0xffff);
-        head = (k == 0) || ((sk[k] >> 16) != (sk[k - 1] >> 16));
+      uint64_t v = 0;
+      if (j < nreal) {
+        v = scratch[j];
+        head = (j == 0) || ((v >> 32) != (scratch[j - 1] >> 32));
       }
       const unsigned m = __ballot_sync(0xffffffffu, head);
       if (head) {
         const int at = G + __popc(m & ((1u << lane) - 1u));
-        w.gs[at] = k;
-        w.gb[at] = static_cast<int>(sk[k] >> 16);
+        w.gs[at] = j;
+        w.gb[at] = static_cast<int>(v >> 32);
       }
       G += __popc(m);
+      if (j < nreal) w.od[j] = static_cast<uint16_t>(v & 0xffffffffu);
     }
     if (lane == 0) w.gs[G] = nreal;
-    __syncwarp();
   }
+  __syncwarp();
   return G;
 }
 
+// ---------------------------------------------------------------- k_tab_fwd (warp per centre)
+// Features are owned in contiguous runs: lane l holds f = F*l .. F*l + F-1.
 template <int F>
-__global__ void __launch_bounds__(64) k_tab_fwd(TabParams p) {
+__global__ void __launch_bounds__(64, 8) k_tab_fwd(TabParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
   const int wpb = blockDim.x >> 5;
   const FwdSmem w = carve_fwd(smem + wid * fwd_smem_bytes(p.scap, p.Mp), p.scap, p.Mp);
   const size_t istride = static_cast<size_t>(6) * p.Mp;
-  const int nc = NC < p.scap ? NC : p.scap;
-  double* cR = w.cache;  // [4][NC]
-  double* cU = w.cache + 4 * NC;
+  const int f0 = F * lane;
   for (int i = blockIdx.x * wpb + wid; i < p.n; i += gridDim.x * wpb) {
     const int64_t off = p.row_off[i];
     const int len = static_cast<int>(p.row_off[i + 1] - off);
-    const double3 ri = ld_pos(p.pos, i);
     for (int t = lane; t < 64; t += 32) w.tc[t] = 0;
     __syncwarp();
-    // --- pass 1: env-mat of every list entry, compaction of the reals ---
-    int nreal = 0, next = 0, kmin = 0x7fffffff, kmax = -1;
+    // --- compaction of the reals (list order), per-type counts ---
+    int nreal = 0, kmin = 0x7fffffff, kmax = -1;
     for (int base = 0; base < len; base += 32) {
       const int e = base + lane;
-      bool real = false, ext = false;
-      int bin = 0, t = 0;
-      double R0 = 0, R1 = 0, R2 = 0, R3 = 0, ul = 0;
-      if (e < len) {
-        const uint64_t key = p.keys[off + e];
-        int sh[3];
-        key_shift(key, sh);
-        double d[3];
-        disp_exact(p.c, ri, ld_pos(p.pos, key_j(key)), sh[0], sh[1], sh[2], d);
-        const double r2 = norm2_exact(d);
-        if (r2 < 1e-12) {
-          raise_err(p.err, DEV_OVERLAP); // env_mat.cpp:33 throws before any table lookup
-        } else if (r2 < p.rc2) {
-          real = true;
-          const double r = sqrt(r2);
-          const double ir = 1.0 / r;
-          const double s = switch_fn(r, p.rs, p.rc) * ir;
-          const long th = locate(p, s, ext, p.err);
-          t = key_type(key);
-          bin = static_cast<int>(t * p.tn + th);
-          R0 = s;
-          R1 = s * (d[0] * ir);
-          R2 = s * (d[1] * ir);
-          R3 = s * (d[2] * ir);
-          ul = s - node_x(p.x0, p.h, th);
-        }
-      }
+      const int bin = e < len ? p.ebin[off + e] : -1;
+      const bool real = bin >= 0;
       const unsigned m = __ballot_sync(0xffffffffu, real);
-      const int at = nreal + __popc(m & ((1u << lane) - 1u));
+      const int t = real ? bin / p.tn : -1;
       if (real) {
+        const int at = nreal + __popc(m & ((1u << lane) - 1u));
         w.rk[at] = static_cast<uint32_t>(bin);
         w.ex[at] = static_cast<uint16_t>(e);
-        if (at < nc) {
-          cR[at] = R0;
-          cR[NC + at] = R1;
-          cR[2 * NC + at] = R2;
-          cR[3 * NC + at] = R3;
-          cU[at] = ul;
-        }
         kmin = min(kmin, bin);
         kmax = max(kmax, bin);
       }
-      const unsigned tm = __match_any_sync(0xffffffffu, real ? t : -1);
+      const unsigned tm = __match_any_sync(0xffffffffu, t);
       if (real && (tm & ((1u << lane) - 1u)) == 0) w.tc[t] += __popc(tm);
       nreal += __popc(m);
-      next += __popc(__ballot_sync(0xffffffffu, ext));
       __syncwarp();
     }
     kmin = warp_min(kmin);
     kmax = warp_max(kmax);
-    __syncwarp();
     for (int t = lane; t < p.n_types; t += 32)
       if (w.tc[t] > p.max_nbr[t]) raise_err(p.err, DEV_OVERFLOW);
+    const int G = sort_and_group(w, p.skeys + off, nreal, kmin, kmax, lane);
     if (lane == 0) {
       atomicAdd(p.counters + 0, static_cast<unsigned long long>(nreal));
-      if (next) atomicAdd(p.counters + 2, static_cast<unsigned long long>(next));
       p.n_real[i] = nreal;
+      p.n_grp[i] = G;
     }
-    bool cache_ok = true;
-    const int G = sort_and_group(w, nreal, kmin, kmax, lane, &cache_ok);
     for (int j = lane; j < nreal; j += 32) {
       const int k = w.od[j];
       p.skeys[off + j] = (static_cast<uint64_t>(w.rk[k]) << 32) | w.ex[k];
     }
+    for (int g = lane; g < G; g += 32)
+      for (int j = w.gs[g]; j < w.gs[g + 1]; ++j) p.egrp[off + w.ex[w.od[j]]] = g;
     // --- moments of each (type, interval) group, then T += W . C[interval] ---
     double tacc[4][F];
 #pragma unroll
@@ -479,105 +458,138 @@ __global__ void __launch_bounds__(64) k_tab_fwd(TabParams p) {
       for (int q = 0; q < F; ++q) tacc[a][q] = 0.0;
     for (int g0 = 0; g0 < G; g0 += GB) {
       {
-        const int g = g0 + (lane >> 2), a = lane & 3;
+        // 4 lanes per group split its members; reduce-scatter leaves lane r with W[a = r][0..5]
+        const int gl = lane >> 2, r = lane & 3;
+        const int g = g0 + gl;
+        double Wv[24];
+#pragma unroll
+        for (int k = 0; k < 24; ++k) Wv[k] = 0.0;
         if (g < G) {
-          double Wm[6] = {0, 0, 0, 0, 0, 0};
           const int j1 = w.gs[g + 1];
-          const int th = w.gb[g] % static_cast<int>(p.tn);
-          for (int j = w.gs[g]; j < j1; ++j) {
-            const int k = w.od[j];
-            double Ra, uu;
-            if (cache_ok && k < nc) {
-              Ra = cR[a * NC + k];
-              uu = cU[k];
-            } else {
-              Env ev;
-              env_of(p, ri, p.keys[off + w.ex[k]], ev);
-              Ra = a == 0 ? ev.s : ev.s * ev.u[a - 1];
-              uu = ev.s - node_x(p.x0, p.h, th);
-            }
-            double um = Ra;
+          for (int j = w.gs[g] + r; j < j1; j += 4) {
+            const int64_t e = off + w.ex[w.od[j]];
+            const double R[4] = {p.erc[e], p.erc[p.E + e], p.erc[2 * p.E + e], p.erc[3 * p.E + e]};
+            const double uu = p.erc[4 * p.E + e];
+            double um = 1.0;
 #pragma unroll
             for (int mm = 0; mm < 6; ++mm) {
-              Wm[mm] += um;
+#pragma unroll
+              for (int a = 0; a < 4; ++a) Wv[a * 6 + mm] += R[a] * um;
               um *= uu;
             }
           }
-#pragma unroll
-          for (int mm = 0; mm < 6; ++mm) w.W[(lane >> 2) * 24 + a * 6 + mm] = Wm[mm];
         }
+        {
+          const bool hi = lane & 2;
+#pragma unroll
+          for (int k = 0; k < 12; ++k) {
+            const double send = hi ? Wv[k] : Wv[k + 12];
+            const double keep = hi ? Wv[k + 12] : Wv[k];
+            Wv[k] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+          }
+        }
+        {
+          const bool hi = lane & 1;
+#pragma unroll
+          for (int k = 0; k < 6; ++k) {
+            const double send = hi ? Wv[k] : Wv[k + 6];
+            const double keep = hi ? Wv[k + 6] : Wv[k];
+            Wv[k] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+          }
+        }
+        if (g < G)
+#pragma unroll
+          for (int mm = 0; mm < 6; ++mm) w.W[gl * 24 + r * 6 + mm] = Wv[mm];
       }
       __syncwarp();
       const int gn = min(GB, G - g0);
       for (int gg = 0; gg < gn; ++gg) {
-        const double* C = p.tab + static_cast<size_t>(w.gb[g0 + gg]) * istride;
+        const double* C = p.tab + static_cast<size_t>(w.gb[g0 + gg]) * istride + f0;
         const double* Wg = w.W + gg * 24;
-        double c[F][6];
+        double c[6][F];
 #pragma unroll
-        for (int q = 0; q < F; ++q)
+        for (int mm = 0; mm < 6; ++mm) {
+          if constexpr (F % 2 == 0) {
 #pragma unroll
-          for (int mm = 0; mm < 6; ++mm) c[q][mm] = __ldg(C + mm * p.Mp + lane + 32 * q);
+            for (int q = 0; q < F; q += 2) {
+              const double2 v = __ldg(reinterpret_cast<const double2*>(C + mm * p.Mp + q));
+              c[mm][q] = v.x;
+              c[mm][q + 1] = v.y;
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < F; ++q) c[mm][q] = __ldg(C + mm * p.Mp + q);
+          }
+        }
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
-          double wa[6];
 #pragma unroll
-          for (int mm = 0; mm < 6; ++mm) wa[mm] = Wg[a * 6 + mm];
+          for (int mm = 0; mm < 6; ++mm) {
+            const double wa = Wg[a * 6 + mm];
 #pragma unroll
-          for (int q = 0; q < F; ++q) {
-            double acc = tacc[a][q];
-#pragma unroll
-            for (int mm = 0; mm < 6; ++mm) acc += wa[mm] * c[q][mm];
-            tacc[a][q] = acc;
+            for (int q = 0; q < F; ++q) tacc[a][q] += wa * c[mm][q];
           }
         }
       }
       __syncwarp();
     }
     // --- T out, D = T<^T T (contract.hpp:9-17) ---
-    double* ts = w.cache;
+    double* ts = w.ts;
     double* Ti = p.T + static_cast<size_t>(i) * 4 * p.Mp;
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int q = 0; q < F; ++q) {
-        Ti[a * p.Mp + lane + 32 * q] = tacc[a][q];
-        ts[a * p.Mp + lane + 32 * q] = tacc[a][q];
+        Ti[a * p.Mp + f0 + q] = tacc[a][q];
+        ts[a * p.Mp + f0 + q] = tacc[a][q];
       }
     __syncwarp();
     double* Drow = p.D + static_cast<size_t>(p.slot_of[i]) * p.K0p;
-    for (int qq = 0; qq < p.mlt; ++qq) {
-      const double t0 = ts[qq], t1 = ts[p.Mp + qq], t2 = ts[2 * p.Mp + qq], t3 = ts[3 * p.Mp + qq];
+    if (f0 < p.M) {
+      for (int qq = 0; qq < p.mlt; ++qq) {
+        const double t0 = ts[qq], t1 = ts[p.Mp + qq], t2 = ts[2 * p.Mp + qq], t3 = ts[3 * p.Mp + qq];
+        double dv[F];
 #pragma unroll
-      for (int q = 0; q < F; ++q) {
-        const int f = lane + 32 * q;
-        if (f < p.M) {
+        for (int q = 0; q < F; ++q) {
           double acc = t0 * tacc[0][q];
           acc += t1 * tacc[1][q];
           acc += t2 * tacc[2][q];
           acc += t3 * tacc[3][q];
-          Drow[qq * p.M + f] = acc;
+          dv[q] = acc;
         }
+        double* dst = Drow + qq * p.M + f0;
+        if constexpr (F % 2 == 0) {
+          if ((p.M & 1) == 0) {
+#pragma unroll
+            for (int q = 0; q < F; q += 2) *reinterpret_cast<double2*>(dst + q) = make_double2(dv[q], dv[q + 1]);
+            continue;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < F; ++q) dst[q] = dv[q];
       }
     }
     __syncwarp();
   }
 }
 
+// ---------------------------------------------------------------- k_tab_bwd_P (warp per centre)
 template <int F>
-__global__ void __launch_bounds__(64) k_tab_bwd(TabParams p) {
+__global__ void __launch_bounds__(64, 6) k_tab_bwd_P(TabParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
   const int wpb = blockDim.x >> 5;
-  const BwdSmem w = carve_bwd(smem + wid * bwd_smem_bytes(p.scap, p.Mp), p.scap, p.Mp);
+  double* ts = reinterpret_cast<double*>(smem) + wid * (4 * p.Mp + 4 * p.mlt);
+  double* S = ts + 4 * p.Mp;
   const size_t istride = static_cast<size_t>(6) * p.Mp;
+  const int f0 = F * lane;
   for (int i = blockIdx.x * wpb + wid; i < p.n; i += gridDim.x * wpb) {
     const int64_t off = p.row_off[i];
-    const int len = static_cast<int>(p.row_off[i + 1] - off);
-    const double3 ri = ld_pos(p.pos, i);
-    for (int e = lane; e < 3 * len; e += 32) p.g[3 * off + e] = 0.0;
     const int nreal = p.n_real[i];
-    for (int k = lane; k < nreal; k += 32) w.sk[k] = p.skeys[off + k];
+    const int G = p.n_grp[i];
+    const uint64_t* sk = p.skeys + off;
+    double* Pout = p.Pbuf + p.goff[i] * 24;
     // --- dT = adjoint of D = T<^T T (contract.hpp:21-38) ---
     const double* Ti = p.T + static_cast<size_t>(i) * 4 * p.Mp;
     double tv[4][F], dT[4][F];
@@ -585,12 +597,13 @@ __global__ void __launch_bounds__(64) k_tab_bwd(TabParams p) {
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int q = 0; q < F; ++q) {
-        tv[a][q] = Ti[a * p.Mp + lane + 32 * q];
-        w.ts[a * p.Mp + lane + 32 * q] = tv[a][q];
+        tv[a][q] = Ti[a * p.Mp + f0 + q];
+        ts[a * p.Mp + f0 + q] = tv[a][q];
         dT[a][q] = 0.0;
       }
     __syncwarp();
     const double* dDrow = p.dD + static_cast<size_t>(p.slot_of[i]) * p.K0p;
+    const bool fon = f0 < p.M;
     for (int q0 = 0; q0 < p.mlt; q0 += 8) {
       double part[32];
 #pragma unroll
@@ -601,13 +614,10 @@ __global__ void __launch_bounds__(64) k_tab_bwd(TabParams p) {
         if (qq < p.mlt) {
           double dq[F];
 #pragma unroll
-          for (int q = 0; q < F; ++q) {
-            const int f = lane + 32 * q;
-            dq[q] = f < p.M ? dDrow[qq * p.M + f] : 0.0;
-          }
+          for (int q = 0; q < F; ++q) dq[q] = fon ? dDrow[qq * p.M + f0 + q] : 0.0;
 #pragma unroll
           for (int a = 0; a < 4; ++a) {
-            const double ta = w.ts[a * p.Mp + qq];
+            const double ta = ts[a * p.Mp + qq];
 #pragma unroll
             for (int q = 0; q < F; ++q) {
               dT[a][q] += dq[q] * ta;
@@ -617,151 +627,134 @@ __global__ void __launch_bounds__(64) k_tab_bwd(TabParams p) {
         }
       }
       const double s = rs32(part, lane);
-      if (q0 + (lane >> 2) < p.mlt) w.S[(q0 + (lane >> 2)) * 4 + (lane & 3)] = s;
+      if (q0 + (lane >> 2) < p.mlt) S[(q0 + (lane >> 2)) * 4 + (lane & 3)] = s;
     }
     __syncwarp();
 #pragma unroll
     for (int q = 0; q < F; ++q) {
-      const int f = lane + 32 * q;
+      const int f = f0 + q;
       if (f < p.mlt)
 #pragma unroll
-        for (int a = 0; a < 4; ++a) dT[a][q] += w.S[f * 4 + a];
+        for (int a = 0; a < 4; ++a) dT[a][q] += S[f * 4 + a];
     }
-    // --- groups of the sorted reals (written by the forward pass) ---
-    int G = 0;
-    for (int base = 0; base < nreal; base += 32) {
+    __syncwarp();
+    if (lane == 0) atomicAdd(p.counters + 1, static_cast<unsigned long long>(nreal));
+    // --- P[a][m] = sum_p dT[a][p] C[m][p] per group (reduce-scatter over the feature lanes) ---
+    int g = 0;
+    for (int base = 0; base < nreal && g < G; base += 32) {
       const int k = base + lane;
       bool head = false;
-      if (k < nreal) head = (k == 0) || ((w.sk[k] >> 32) != (w.sk[k - 1] >> 32));
-      const unsigned m = __ballot_sync(0xffffffffu, head);
-      if (head) {
-        const int at = G + __popc(m & ((1u << lane) - 1u));
-        w.gs[at] = k;
-        w.gb[at] = static_cast<int>(w.sk[k] >> 32);
+      uint64_t v = 0;
+      if (k < nreal) {
+        v = sk[k];
+        head = (k == 0) || ((v >> 32) != (sk[k - 1] >> 32));
       }
-      G += __popc(m);
-    }
-    if (lane == 0) {
-      w.gs[G] = nreal;
-      atomicAdd(p.counters + 1, static_cast<unsigned long long>(nreal));
-    }
-    __syncwarp();
-    double fc[3] = {0.0, 0.0, 0.0};
-    double vir[9];
+      unsigned m = __ballot_sync(0xffffffffu, head);
+      while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        const int bin = static_cast<int>(__shfl_sync(0xffffffffu, v, src) >> 32);
+        const double* C = p.tab + static_cast<size_t>(bin) * istride + f0;
+        double c[6][F];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) vir[k] = 0.0;
-    for (int g0 = 0; g0 < G; g0 += GB) {
-      const int gn = min(GB, G - g0);
-      // P[a][m] = sum_p dT[a][p] C[m][p] per group (reduce-scatter over the feature lanes)
-      for (int gg = 0; gg < gn; ++gg) {
-        const double* C = p.tab + static_cast<size_t>(w.gb[g0 + gg]) * istride;
+        for (int mm = 0; mm < 6; ++mm) {
+          if constexpr (F % 2 == 0) {
+#pragma unroll
+            for (int q = 0; q < F; q += 2) {
+              const double2 cv = __ldg(reinterpret_cast<const double2*>(C + mm * p.Mp + q));
+              c[mm][q] = cv.x;
+              c[mm][q + 1] = cv.y;
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < F; ++q) c[mm][q] = __ldg(C + mm * p.Mp + q);
+          }
+        }
         double part[24];
 #pragma unroll
-        for (int k = 0; k < 24; ++k) part[k] = 0.0;
-#pragma unroll
-        for (int q = 0; q < F; ++q) {
+        for (int a = 0; a < 4; ++a)
 #pragma unroll
           for (int mm = 0; mm < 6; ++mm) {
-            const double c = __ldg(C + mm * p.Mp + lane + 32 * q);
+            double acc = 0.0;
 #pragma unroll
-            for (int a = 0; a < 4; ++a) part[a * 6 + mm] += dT[a][q] * c;
+            for (int q = 0; q < F; ++q) acc += dT[a][q] * c[mm][q];
+            part[a * 6 + mm] = acc;
           }
-        }
         const int b = rs24(part, lane);
         if ((lane & 3) == 0) {
-          w.P[gg * 24 + b] = part[0];
-          w.P[gg * 24 + b + 1] = part[1];
-          w.P[gg * 24 + b + 2] = part[2];
+          Pout[g * 24 + b] = part[0];
+          Pout[g * 24 + b + 1] = part[1];
+          Pout[g * 24 + b + 2] = part[2];
         }
+        ++g;
       }
-      __syncwarp();
-      // members of the batch: one lane per real neighbour
-      const int j0 = w.gs[g0], j1 = w.gs[g0 + gn];
-      for (int j = j0 + lane; j < j1; j += 32) {
-        const uint64_t sk = w.sk[j];
-        const int e = static_cast<int>(sk & 0xffffffffu);
-        const int bin = static_cast<int>(sk >> 32);
-        const long th = bin % p.tn;
-        int gg = 0;
-        while (gg + 1 < gn && w.gs[g0 + gg + 1] <= j) ++gg;
-        const double* P = w.P + gg * 24;
-        Env ev;
-        env_of(p, ri, p.keys[off + e], ev);
-        const double R[4] = {ev.s, ev.s * ev.u[0], ev.s * ev.u[1], ev.s * ev.u[2]};
-        const double uu = ev.s - node_x(p.x0, p.h, th);
-        double drow[4], dsum = 0.0;
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          const double* Pa = P + a * 6;
-          drow[a] = ((((Pa[5] * uu + Pa[4]) * uu + Pa[3]) * uu + Pa[2]) * uu + Pa[1]) * uu + Pa[0];
-          const double h1 =
-              (((5.0 * Pa[5] * uu + 4.0 * Pa[4]) * uu + 3.0 * Pa[3]) * uu + 2.0 * Pa[2]) * uu + Pa[1];
-          dsum += R[a] * h1;
-        }
-        drow[0] += dsum;
-        double dd[12];
-#pragma unroll
-        for (int x = 0; x < 3; ++x) dd[x] = ev.sd * ev.u[x];
-#pragma unroll
-        for (int y = 0; y < 3; ++y)
-#pragma unroll
-          for (int x = 0; x < 3; ++x) {
-            double v = ev.sd * ev.u[x] * ev.u[y] - ev.s * ev.ir * ev.u[x] * ev.u[y];
-            if (x == y) v += ev.s * ev.ir;
-            dd[3 * (1 + y) + x] = v;
-          }
-        double gx[3];
-#pragma unroll
-        for (int x = 0; x < 3; ++x) {
-          double acc = 0.0;
-#pragma unroll
-          for (int a = 0; a < 4; ++a) acc += drow[a] * dd[3 * a + x];
-          gx[x] = acc;
-          p.g[3 * (off + e) + x] = acc;
-          fc[x] += acc;
-        }
-#pragma unroll
-        for (int x = 0; x < 3; ++x)
-#pragma unroll
-          for (int y = 0; y < 3; ++y) vir[3 * x + y] += ev.d[x] * gx[y];
-      }
-      __syncwarp();
     }
-#pragma unroll
-    for (int x = 0; x < 3; ++x) fc[x] = warp_sum(fc[x]);
-#pragma unroll
-    for (int k = 0; k < 9; ++k) vir[k] = warp_sum(vir[k]);
-    if (lane == 0) {
-#pragma unroll
-      for (int x = 0; x < 3; ++x) p.fcenter[3 * i + x] = fc[x];
-#pragma unroll
-      for (int k = 0; k < 9; ++k) p.vpart[9 * static_cast<size_t>(i) + k] = vir[k];
-    }
-    __syncwarp();
   }
 }
 
-template <int F>
-void launch_tab(bool fwd, const TabParams& p, int n, cudaStream_t st, int sms) {
-  const size_t per = fwd ? fwd_smem_bytes(p.scap, p.Mp) : bwd_smem_bytes(p.scap, p.Mp);
-  const int wpb = 2;
-  const size_t bytes = per * wpb;
-  if (bytes > 227 * 1024) throw NumErr("neighbour rows too long for the tabulate kernel");
-  auto kern = fwd ? k_tab_fwd<F> : k_tab_bwd<F>;
-  DPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(bytes)));
-  const int blocks = std::max(1, std::min(ceil_div(n, wpb), sms * 32));
-  kern<<<blocks, wpb * 32, bytes, st>>>(p);
-  DPB_CUDA(cudaGetLastError());
+// ---------------------------------------------------------------- k_tab_bwd_g (thread per entry)
+__global__ void __launch_bounds__(256) k_tab_bwd_g(TabParams p) {
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (e >= p.E) return;
+  const int bin = p.ebin[e];
+  double* ge = p.g + 3 * e;
+  if (bin < 0) {
+    ge[0] = 0.0;
+    ge[1] = 0.0;
+    ge[2] = 0.0;
+    return;
+  }
+  const int i = p.eown[e];
+  Env ev;
+  env_of(p, ld_pos(p.pos, i), p.keys[e], ev);
+  const int th = bin % p.tn;
+  const double* P = p.Pbuf + (p.goff[i] + p.egrp[e]) * 24;
+  const double R[4] = {ev.s, ev.s * ev.u[0], ev.s * ev.u[1], ev.s * ev.u[2]};
+  const double uu = ev.s - node_x(p.x0, p.h, th);
+  double drow[4], dsum = 0.0;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const double* Pa = P + a * 6;
+    drow[a] = ((((Pa[5] * uu + Pa[4]) * uu + Pa[3]) * uu + Pa[2]) * uu + Pa[1]) * uu + Pa[0];
+    const double h1 = (((5.0 * Pa[5] * uu + 4.0 * Pa[4]) * uu + 3.0 * Pa[3]) * uu + 2.0 * Pa[2]) * uu + Pa[1];
+    dsum += R[a] * h1;
+  }
+  drow[0] += dsum;
+  double dd[12];
+#pragma unroll
+  for (int x = 0; x < 3; ++x) dd[x] = ev.sd * ev.u[x];
+#pragma unroll
+  for (int y = 0; y < 3; ++y)
+#pragma unroll
+    for (int x = 0; x < 3; ++x) {
+      double v = ev.sd * ev.u[x] * ev.u[y] - ev.s * ev.ir * ev.u[x] * ev.u[y];
+      if (x == y) v += ev.s * ev.ir;
+      dd[3 * (1 + y) + x] = v;
+    }
+#pragma unroll
+  for (int x = 0; x < 3; ++x) {
+    double acc = 0.0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) acc += drow[a] * dd[3 * a + x];
+    ge[x] = acc;
+  }
 }
 
+// ---------------------------------------------------------------- host side
 TabParams make_params(Engine& E) {
   TabParams p{};
   p.pos = E.pos4.p;
   p.row_off = E.row_off.p;
   p.keys = E.keys.p;
+  p.eown = E.eown.p;
+  p.ebin = E.ebin.p;
+  p.erc = E.erc.p;
+  p.egrp = E.egrp.p;
   p.skeys = E.skeys.p;
   p.n_real = E.n_real.p;
+  p.n_grp = E.n_grp.p;
+  p.goff = E.goff.p;
+  p.Pbuf = E.Pbuf.p;
   p.tab = E.tab.p;
   p.max_nbr = E.d_max_nbr.p;
   p.c = E.cell;
@@ -771,20 +764,19 @@ TabParams make_params(Engine& E) {
   p.x0 = E.tab_x0;
   p.h = E.tab_h;
   p.x_end = E.tab_x0 + E.tab_h * static_cast<double>(E.tab_n);
-  p.tn = static_cast<long>(E.tab_n);
+  p.tn = static_cast<int>(E.tab_n);
   p.n = static_cast<int>(E.n);
   p.n_types = E.n_types;
   p.M = E.M;
   p.Mp = E.Mp;
   p.mlt = E.mlt;
   p.K0p = E.K0p;
+  p.E = E.n_entries;
   p.slot_of = E.slot_of.p;
   p.T = E.T.p;
   p.D = E.D.p;
   p.dD = E.dD.p;
   p.g = E.g.p;
-  p.fcenter = E.fcenter.p;
-  p.vpart = E.vpart.p;
   p.counters = E.counters.p;
   p.err = E.err.p;
   int scap = 32;
@@ -799,26 +791,80 @@ int sm_count(int dev) {
   return s > 0 ? s : 148;
 }
 
-void dispatch(Engine& E, bool fwd) {
-  TabParams p = make_params(E);
-  const int sms = sm_count(E.device);
-  switch (E.Mp / 32) {
-    case 1: launch_tab<1>(fwd, p, p.n, E.stream, sms); break;
-    case 2: launch_tab<2>(fwd, p, p.n, E.stream, sms); break;
-    case 3: launch_tab<3>(fwd, p, p.n, E.stream, sms); break;
-    case 4: launch_tab<4>(fwd, p, p.n, E.stream, sms); break;
-    case 5: launch_tab<5>(fwd, p, p.n, E.stream, sms); break;
-    case 6: launch_tab<6>(fwd, p, p.n, E.stream, sms); break;
-    case 7: launch_tab<7>(fwd, p, p.n, E.stream, sms); break;
-    case 8: launch_tab<8>(fwd, p, p.n, E.stream, sms); break;
-    default: throw InputErr("feature width 4*d1 must be at most 256");
-  }
-  ++E.launches;
+template <int F>
+void launch_fwd_warp(const TabParams& p, cudaStream_t st, int sms) {
+  const size_t bytes = 2 * fwd_smem_bytes(p.scap, p.Mp);
+  if (bytes > 227 * 1024) throw NumErr("neighbour rows too long for the tabulate kernel");
+  DPB_CUDA(cudaFuncSetAttribute(k_tab_fwd<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(bytes)));
+  const int blocks = std::max(1, std::min(ceil_div(p.n, 2), sms * 32));
+  k_tab_fwd<F><<<blocks, 64, bytes, st>>>(p);
+  DPB_CUDA(cudaGetLastError());
+}
+
+template <int F>
+void launch_bwd_warp(const TabParams& p, cudaStream_t st, int sms) {
+  const size_t bytes = 2 * (4 * static_cast<size_t>(p.Mp) + 4 * p.mlt) * sizeof(double);
+  DPB_CUDA(cudaFuncSetAttribute(k_tab_bwd_P<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(bytes)));
+  const int blocks = std::max(1, std::min(ceil_div(p.n, 2), sms * 32));
+  k_tab_bwd_P<F><<<blocks, 64, bytes, st>>>(p);
+  DPB_CUDA(cudaGetLastError());
 }
 
 } // namespace
 
-void Engine::launch_tab_fwd() { dispatch(*this, true); }
-void Engine::launch_tab_bwd() { dispatch(*this, false); }
+void Engine::launch_tab_fwd() {
+  TabParams p = make_params(*this);
+  const int sms = sm_count(device);
+  if (p.E > 0) {
+    k_env_fwd<<<ceil_div(p.E, 256), 256, 0, stream>>>(p);
+    ++launches;
+  }
+  switch (Mp / 32) {
+    case 1: launch_fwd_warp<1>(p, stream, sms); break;
+    case 2: launch_fwd_warp<2>(p, stream, sms); break;
+    case 3: launch_fwd_warp<3>(p, stream, sms); break;
+    case 4: launch_fwd_warp<4>(p, stream, sms); break;
+    case 5: launch_fwd_warp<5>(p, stream, sms); break;
+    case 6: launch_fwd_warp<6>(p, stream, sms); break;
+    case 7: launch_fwd_warp<7>(p, stream, sms); break;
+    case 8: launch_fwd_warp<8>(p, stream, sms); break;
+    default: throw InputErr("feature width 4*d1 must be at most 256");
+  }
+  ++launches;
+  // group offsets for the backward projections; the total sizes Pbuf (one small sync per step)
+  DPB_CUDA(cudaMemsetAsync(n_grp.p + n, 0, sizeof(int32_t), stream));
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, n_grp.p, goff.p, n + 1, stream);
+  scan_tmp.ensure(tb + 1);
+  cub::DeviceScan::ExclusiveSum(scan_tmp.p, tb, n_grp.p, goff.p, n + 1, stream);
+  ++launches;
+  int64_t total = 0;
+  DPB_CUDA(cudaMemcpyAsync(&total, goff.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+  DPB_CUDA(cudaStreamSynchronize(stream));
+  Pbuf.ensure(static_cast<size_t>(total) * 24 + 24);
+}
+
+void Engine::launch_tab_bwd() {
+  TabParams p = make_params(*this);
+  const int sms = sm_count(device);
+  switch (Mp / 32) {
+    case 1: launch_bwd_warp<1>(p, stream, sms); break;
+    case 2: launch_bwd_warp<2>(p, stream, sms); break;
+    case 3: launch_bwd_warp<3>(p, stream, sms); break;
+    case 4: launch_bwd_warp<4>(p, stream, sms); break;
+    case 5: launch_bwd_warp<5>(p, stream, sms); break;
+    case 6: launch_bwd_warp<6>(p, stream, sms); break;
+    case 7: launch_bwd_warp<7>(p, stream, sms); break;
+    case 8: launch_bwd_warp<8>(p, stream, sms); break;
+    default: throw InputErr("feature width 4*d1 must be at most 256");
+  }
+  ++launches;
+  if (p.E > 0) {
+    k_tab_bwd_g<<<ceil_div(p.E, 256), 256, 0, stream>>>(p);
+    ++launches;
+  }
+}
 
 } // namespace dpb
