@@ -148,6 +148,24 @@ int dp_md_step(dp_handle* h, int64_t k);
 int dp_md_end(dp_handle* h, double* pos, double* vel, dp_thermo* thermo, int64_t thermo_cap,
               int64_t* n_thermo, dp_md_result* result);
 
+/* ---- multi-GPU: one process (one handle) per GPU, spatial domain decomposition ----------------
+ * Slab partition with partition_domain semantics (domain.cpp:21-82); ghost positions go to
+ * neighbours and ghost force partials come back through NCCL send/recv every step. Rank 0 creates
+ * the NCCL id with dp_nccl_unique_id (128 bytes) and shares it (e.g. torch.distributed); every rank
+ * then calls dp_dist_init on its handle. After that dp_md_begin takes the GLOBAL initial state on
+ * every rank and dp_md_end returns the global final state on every rank; thermo records hold
+ * global sums. */
+int dp_nccl_unique_id(void* out, int len);
+/* partition_domain (domain.cpp:21-82) on the host: owner[n], ghost_mask[n_workers * n]. */
+int dp_partition_domain(int64_t n, const double* pos, const double* box, const uint8_t* pbc,
+                        int n_workers, double margin, int32_t* owner, uint8_t* ghost_mask);
+/* Host plan of one rank: local atoms (ascending global id), centre mask, per-peer send/recv
+ * global ids (offsets n_workers+1). All arrays sized n. For tests without GPUs. */
+int dp_dist_plan(int64_t n, const double* pos, const double* box, const uint8_t* pbc, int n_workers,
+                 int rank, double margin, int64_t* n_local, int64_t* lgid, uint8_t* center,
+                 int64_t* send_off, int64_t* send_gid, int64_t* recv_off, int64_t* recv_gid);
+int dp_dist_init(dp_handle* h, int rank, int world, const void* nccl_id);
+
 /* cudaStream_t of the handle (for CUDA-event timing on the launching stream). */
 void* dp_stream(dp_handle* h);
 /* Number of kernels this handle has launched since creation. */
@@ -155,7 +173,7 @@ uint64_t dp_launch_count(const dp_handle* h);
 /* Per-phase CUDA-event timing on the handle's stream (off by default). dp_phase_times
  * synchronizes and returns accumulated milliseconds and interval counts for the phases
  * 0 neighbour list, 1 env-mat + tabulate forward, 2 fitting net (DMMA GEMMs), 3 tabulate
- * backward, 4 force gather + reductions, 5 integrator; then resets them. */
+ * backward, 4 force gather + reductions, 5 integrator, 6 halo exchange; then resets them. */
 int dp_set_timing(dp_handle* h, int enable);
 int dp_phase_times(dp_handle* h, double* ms /* 8 */, uint64_t* counts /* 8 */);
 

@@ -34,7 +34,7 @@ __all__ = [
     "write_tables", "AtomicConfig", "gen_config", "make_random_config", "init_velocities",
     "mix_seed", "EvalResult", "FusedCounters", "NeighborList", "MDConfig", "ThermoRecord",
     "MDResult", "DeepPot", "build_neighbor_list", "compute_energy_forces_virial_tabulated",
-    "run_md", "library_path", "tanh_table",
+    "run_md", "library_path", "tanh_table", "partition_domain",
 ]
 
 _PKG = Path(__file__).resolve().parent
@@ -136,6 +136,11 @@ def _lib():
         "dp_stream": ([P], P),
         "dp_launch_count": ([P], U64),
         "dp_set_timing": ([P, I], I),
+        "dp_nccl_unique_id": ([C.c_void_p, I], I),
+        "dp_partition_domain": ([I64, D, D, U8P, I, C.c_double, I32P, U8P], I),
+        "dp_dist_plan": ([I64, D, D, U8P, I, I, C.c_double, C.POINTER(I64), C.POINTER(I64), U8P,
+                          C.POINTER(I64), C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)], I),
+        "dp_dist_init": ([P, I, I, C.c_char_p], I),
         "dp_phase_times": ([P, D, C.POINTER(U64)], I),
         "dp_preset_get": ([C.c_char_p, C.POINTER(_Preset)], I),
         "dp_model_blob_size": ([C.POINTER(_Preset)], I64),
@@ -565,7 +570,18 @@ class DeepPot:
     def launch_count(self) -> int:
         return int(_lib().dp_launch_count(self._h))
 
-    PHASES = ("nlist", "tab_fwd", "fitting", "tab_bwd", "forces", "integrate")
+    PHASES = ("nlist", "tab_fwd", "fitting", "tab_bwd", "forces", "integrate", "halo")
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(_lib().dp_nccl_unique_id(buf, 128))
+        return buf.raw
+
+    def dist_init(self, rank: int, world: int, nccl_id: bytes) -> None:
+        """Join a domain-decomposed run (one handle per GPU process)."""
+        _check(_lib().dp_dist_init(self._h, rank, world, nccl_id), self._h)
+        self._dist = True
 
     def set_timing(self, enable: bool) -> None:
         _check(_lib().dp_set_timing(self._h, int(enable)), self._h)
@@ -634,6 +650,10 @@ class DeepPot:
         _check(_lib().dp_md_step(self._h, k), self._h)
 
     def md_end(self, pos_out: Optional[np.ndarray] = None, vel_out: Optional[np.ndarray] = None) -> MDResult:
+        if pos_out is not None:
+            assert pos_out.flags.c_contiguous and pos_out.dtype == np.float64
+        if vel_out is not None:
+            assert vel_out.flags.c_contiguous and vel_out.dtype == np.float64
         cap = self._md_cap
         th = (_Thermo * cap)()
         nth = C.c_int64()
@@ -652,6 +672,36 @@ def _md_result(th, n, res: _MDResult) -> MDResult:
     return MDResult(recs, int(res.force_evals), int(res.staleness_checks), res.max_drift_seen,
                     FusedCounters(c.rows_forward, c.rows_backward, c.extrapolations),
                     res.final_ke, res.final_pe, res.final_total)
+
+
+def partition_domain(cfg: AtomicConfig, n_workers: int, margin: float):
+    """partition_domain (domain.hpp:29): (owner[n], ghost_mask[n_workers, n]) on the host."""
+    n = cfg.n_atoms
+    owner = np.empty(n, dtype=np.int32)
+    gm = np.empty((n_workers, n), dtype=np.uint8)
+    _check(_lib().dp_partition_domain(n, _dp(cfg.pos), _dp(cfg.h), _u8(cfg.periodic), n_workers,
+                                      margin, _ip(owner), _u8(gm)))
+    return owner, gm.astype(bool)
+
+
+def dist_plan(cfg: AtomicConfig, n_workers: int, rank: int, margin: float) -> dict:
+    """Host plan of one rank of the decomposed run (local ids, centre mask, per-peer exchange)."""
+    n = cfg.n_atoms
+    I64P = C.POINTER(C.c_int64)
+    nl = C.c_int64()
+    lgid = np.empty(n, dtype=np.int64)
+    cen = np.empty(n, dtype=np.uint8)
+    so = np.empty(n_workers + 1, dtype=np.int64)
+    ro = np.empty(n_workers + 1, dtype=np.int64)
+    sg = np.empty(n, dtype=np.int64)
+    rg = np.empty(n, dtype=np.int64)
+    _check(_lib().dp_dist_plan(n, _dp(cfg.pos), _dp(cfg.h), _u8(cfg.periodic), n_workers, rank, margin,
+                               C.byref(nl), lgid.ctypes.data_as(I64P), _u8(cen), so.ctypes.data_as(I64P),
+                               sg.ctypes.data_as(I64P), ro.ctypes.data_as(I64P), rg.ctypes.data_as(I64P)))
+    k = nl.value
+    return {"lgid": lgid[:k], "center": cen[:k].astype(bool),
+            "send": {p: sg[so[p]:so[p + 1]] for p in range(n_workers)},
+            "recv": {p: rg[ro[p]:ro[p + 1]] for p in range(n_workers)}}
 
 
 # ---------------------------------------------------------------- reference-named functions

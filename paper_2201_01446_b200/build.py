@@ -82,7 +82,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     if failed:
         raise RuntimeError("libdpb200 build failed")
     tmp = LIB.with_suffix(".so.tmp")
-    _run([nvcc, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lgomp"], verbose)
+    _run([nvcc, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lgomp", "-lnccl"], verbose)
     os.replace(tmp, LIB)
     return LIB
 

@@ -106,7 +106,10 @@ int dp_md_begin(dp_handle* h, int64_t n, const double* pos, const double* vel,
   return guard_call(&h->eng.last_error, [&] {
     dpb::Engine& E = h->eng;
     if (n < 1) throw InputErr("configuration has no atoms");
-    E.set_config(n, pos, types, box, pbc);
+    if (E.dist)
+      dpb::dist_md_begin(E, n, pos, vel, types, box, pbc, cfg);
+    else
+      E.set_config(n, pos, types, box, pbc);
     E.md_begin(pos, vel, cfg);
   });
 }
@@ -146,6 +149,11 @@ int dp_md_run(dp_handle* h, int64_t n, double* pos, double* vel, const int32_t* 
 void* dp_stream(dp_handle* h) { return h ? static_cast<void*>(h->eng.stream) : nullptr; }
 
 uint64_t dp_launch_count(const dp_handle* h) { return h ? h->eng.launches : 0; }
+
+int dp_dist_init(dp_handle* h, int rank, int world, const void* nccl_id) {
+  if (!h || !nccl_id) return DP_INPUT_ERROR;
+  return guard_call(&h->eng.last_error, [&] { dpb::dist_init(h->eng, rank, world, nccl_id); });
+}
 
 int dp_set_timing(dp_handle* h, int enable) {
   if (!h) return DP_INPUT_ERROR;

@@ -158,7 +158,7 @@ void Engine::destroy() {
   };
   tab.release(); tab32.release(); rel(fit_wt); rel(fit_w); rel(fit_b); rel(fit_wout);
   d_max_nbr.release(); tanh_tab.release(); pos4.release(); pos3.release(); vel3.release();
-  types.release(); slot_of.release(); atom_of.release(); row_off.release(); keys.release();
+  types.release(); center.release(); slot_of.release(); atom_of.release(); row_off.release(); keys.release();
   rev.release(); bin_of.release(); bin_start.release(); bin_atoms.release(); bin_fill.release();
   frac.release(); ref_pos.release(); row_len.release(); nl_len.release(); scan_tmp.release();
   skeys.release(); eown.release(); ebin.release(); egrp.release(); erc.release(); n_grp.release(); goff.release(); Pbuf.release(); n_real.release(); T.release(); D.release(); dD.release(); rel(act_t);
@@ -175,12 +175,13 @@ void Engine::destroy() {
   scratch.mass_atom.release();
   scratch.ke.release();
   scratch.rec.release();
+  if (dist) dist_destroy(*this);
   if (stream) cudaStreamDestroy(stream);
   stream = nullptr;
 }
 
 void Engine::set_config(int64_t nn, const double* pos, const int32_t* ty, const double* box,
-                        const uint8_t* pbc) {
+                        const uint8_t* pbc, const uint8_t* cmask) {
   // validate_config (geom.cpp:40-56) and Cell::refresh (geom.cpp:7-29)
   if (nn <= 0) throw InputErr("configuration has no atoms");
   if (!pos || !ty || !box || !pbc) throw InputErr("null configuration array");
@@ -208,7 +209,10 @@ void Engine::set_config(int64_t nn, const double* pos, const int32_t* ty, const 
   bool same = nn == n && std::memcmp(c.h, cell.h, sizeof(c.h)) == 0 &&
               std::memcmp(c.per, cell.per, sizeof(c.per)) == 0 &&
               static_cast<int64_t>(h_types.size()) == nn &&
-              std::memcmp(h_types.data(), ty, nn * sizeof(int32_t)) == 0;
+              std::memcmp(h_types.data(), ty, nn * sizeof(int32_t)) == 0 &&
+              static_cast<int64_t>(h_center.size()) == nn &&
+              (cmask ? std::memcmp(h_center.data(), cmask, nn) == 0
+                     : std::all_of(h_center.begin(), h_center.end(), [](uint8_t v) { return v != 0; }));
   cell = c;
   if (!same) {
     n = nn;
@@ -216,9 +220,18 @@ void Engine::set_config(int64_t nn, const double* pos, const int32_t* ty, const 
     h_types.assign(ty, ty + nn);
     types.ensure(n);
     DPB_CUDA(cudaMemcpyAsync(types.p, ty, n * sizeof(int32_t), cudaMemcpyHostToDevice, stream));
+    if (cmask)
+      h_center.assign(cmask, cmask + nn);
+    else
+      h_center.assign(nn, 1);
+    n_centers = 0;
+    for (int64_t i = 0; i < n; ++i) n_centers += h_center[i] != 0;
+    center.ensure(n);
+    DPB_CUDA(cudaMemcpyAsync(center.p, h_center.data(), n, cudaMemcpyHostToDevice, stream));
     // slots: atoms grouped by centre type, each segment padded to the GEMM tile (64 rows)
     seg_count.assign(n_types, 0);
-    for (int64_t i = 0; i < n; ++i) ++seg_count[ty[i]];
+    for (int64_t i = 0; i < n; ++i)
+      if (h_center[i]) ++seg_count[ty[i]];
     seg_start.assign(n_types, 0);
     seg_rows.assign(n_types, 0);
     int64_t at = 0;
@@ -231,6 +244,10 @@ void Engine::set_config(int64_t nn, const double* pos, const int32_t* ty, const 
     std::vector<int32_t> so(n), ao(n_slots, -1);
     std::vector<int> fill(n_types, 0);
     for (int64_t i = 0; i < n; ++i) {
+      if (!h_center[i]) {
+        so[i] = -1;
+        continue;
+      }
       const int t = ty[i];
       const int s = seg_start[t] + fill[t]++;
       so[i] = s;
@@ -388,14 +405,7 @@ double Engine::max_drift() { return host_max_drift(*this); }
 
 // ---------------------------------------------------------------- MD (md.cpp:151-231)
 
-void Engine::md_begin(const double* pos, const double* vel, const dp_md_config* cfg) {
-  (void)pos;
-  if (!(cfg->dt > 0.0)) throw InputErr("time step must be positive");
-  if (cfg->n_steps < 0) throw InputErr("step count must be non-negative");
-  if (cfg->rebuild_every < 1 || cfg->thermo_every < 1)
-    throw InputErr("rebuild and thermo intervals must be at least 1");
-  if (!(cfg->buffer >= 0.0)) throw InputErr("buffer must be non-negative");
-  md = *cfg;
+void Engine::md_upload_atoms(const double* vel_local) {
   MdScratch& S = scratch;
   std::vector<double> m(n), af(n);
   for (int64_t i = 0; i < n; ++i) {
@@ -408,15 +418,31 @@ void Engine::md_begin(const double* pos, const double* vel, const dp_md_config* 
   vel3.ensure(3 * n);
   DPB_CUDA(cudaMemcpyAsync(S.mass_atom.p, m.data(), n * 8, cudaMemcpyHostToDevice, stream));
   DPB_CUDA(cudaMemcpyAsync(acc_fac.p, af.data(), n * 8, cudaMemcpyHostToDevice, stream));
-  DPB_CUDA(cudaMemcpyAsync(vel3.p, vel, 3 * n * 8, cudaMemcpyHostToDevice, stream));
+  DPB_CUDA(cudaMemcpyAsync(vel3.p, vel_local, 3 * n * 8, cudaMemcpyHostToDevice, stream));
+  DPB_CUDA(cudaStreamSynchronize(stream));
+}
+
+void Engine::md_begin(const double* pos, const double* vel, const dp_md_config* cfg) {
+  (void)pos;
+  if (!(cfg->dt > 0.0)) throw InputErr("time step must be positive");
+  if (cfg->n_steps < 0) throw InputErr("step count must be non-negative");
+  if (cfg->rebuild_every < 1 || cfg->thermo_every < 1)
+    throw InputErr("rebuild and thermo intervals must be at least 1");
+  if (!(cfg->buffer >= 0.0)) throw InputErr("buffer must be non-negative");
+  md = *cfg;
+  MdScratch& S = scratch;
+  if (!dist) {
+    md_upload_atoms(vel);
+    build_list(r_cut + md.buffer);
+  }
   const int64_t n_rec = cfg->n_steps / cfg->thermo_every + 1;
   S.rec.ensure(n_rec + 1);
   S.n_rec = 0;
   md_res = dp_md_result{};
   DPB_CUDA(cudaMemsetAsync(red.p + 11, 0, sizeof(double), stream)); // max drift seen
   reset_counters();
-  build_list(r_cut + md.buffer);
   evaluate();
+  if (dist) dist_halo_reverse(*this);
   md_res.force_evals = 1;
   launch_thermo(*this, 0, S.rec.p + S.n_rec++, S.mass_atom.p, S.ke.p);
   md_step = 0;
@@ -433,12 +459,26 @@ void Engine::md_steps(int64_t k) {
     phase_begin(5);
     launch_kick_drift(*this, half, md.dt);
     phase_end();
-    if (s % md.rebuild_every == 0) build_list(r_cut + md.buffer);
+    if (s % md.rebuild_every == 0) {
+      if (dist)
+        dist_rebuild(*this);
+      else
+        build_list(r_cut + md.buffer);
+    } else if (dist) {
+      phase_begin(6);
+      dist_halo_forward(*this);
+      phase_end();
+    }
     phase_begin(5);
     launch_stale_check(*this, 0.5 * md.buffer);
     phase_end();
     ++md_res.staleness_checks;
     evaluate();
+    if (dist) {
+      phase_begin(6);
+      dist_halo_reverse(*this);
+      phase_end();
+    }
     ++md_res.force_evals;
     phase_begin(5);
     launch_kick(*this, half);
@@ -456,15 +496,19 @@ void Engine::md_end(double* pos, double* vel) {
   thermo.resize(S.n_rec);
   if (S.n_rec)
     DPB_CUDA(cudaMemcpyAsync(thermo.data(), S.rec.p, S.n_rec * sizeof(dp_thermo), cudaMemcpyDeviceToHost, stream));
-  if (pos) DPB_CUDA(cudaMemcpyAsync(pos, pos3.p, 3 * n * 8, cudaMemcpyDeviceToHost, stream));
-  if (vel) DPB_CUDA(cudaMemcpyAsync(vel, vel3.p, 3 * n * 8, cudaMemcpyDeviceToHost, stream));
+  if (dist) {
+    dist_md_end(*this, pos, vel);
+  } else {
+    if (pos) DPB_CUDA(cudaMemcpyAsync(pos, pos3.p, 3 * n * 8, cudaMemcpyDeviceToHost, stream));
+    if (vel) DPB_CUDA(cudaMemcpyAsync(vel, vel3.p, 3 * n * 8, cudaMemcpyDeviceToHost, stream));
+  }
   // final KE/PE (md.cpp:227-229)
   DevBuf<dp_thermo> fin;
   fin.ensure(1);
   launch_thermo(*this, md_step, fin.p, S.mass_atom.p, S.ke.p);
   dp_thermo ft;
-  double seen = 0.0;
   DPB_CUDA(cudaMemcpyAsync(&ft, fin.p, sizeof(ft), cudaMemcpyDeviceToHost, stream));
+  double seen = 0.0;
   DPB_CUDA(cudaMemcpyAsync(&seen, red.p + 11, sizeof(double), cudaMemcpyDeviceToHost, stream));
   DPB_CUDA(cudaStreamSynchronize(stream));
   fin.release();

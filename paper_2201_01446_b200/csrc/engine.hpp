@@ -27,6 +27,8 @@
 
 namespace dpb {
 
+struct Dist; // dist.cpp: slab decomposition + NCCL halo exchange
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
@@ -82,6 +84,9 @@ struct Engine {
   DevBuf<double> vel3;
   DevBuf<int32_t> types;
   std::vector<int32_t> h_types;
+  std::vector<uint8_t> h_center;  // 1 = centre evaluated here (owned), 0 = ghost (halo only)
+  DevBuf<uint8_t> center;
+  int64_t n_centers = 0;
   std::vector<int> seg_start, seg_count, seg_rows; // slots per centre type (padded to 64)
   int64_t n_slots = 0;
   DevBuf<int32_t> slot_of; // atom -> slot
@@ -155,12 +160,15 @@ struct Engine {
     int64_t n_rec = 0;
   } scratch;
 
+  Dist* dist = nullptr; // non-null when this handle is one rank of a domain-decomposed run
+  void md_upload_atoms(const double* vel_local);
+
   // lifecycle
   void create(const dp_model_desc* md, const dp_table_desc* td, int device, int precision);
   void destroy();
   // configuration upload (host AoS positions); resets the list when n/types/box change
   void set_config(int64_t n, const double* pos, const int32_t* types, const double* box,
-                  const uint8_t* pbc);
+                  const uint8_t* pbc, const uint8_t* center_mask = nullptr);
   void upload_positions(const double* pos);
   // neighbour list at `cutoff`, device resident
   void build_list(double cutoff);
@@ -196,5 +204,17 @@ void launch_kick(Engine& E, double half);
 void launch_stale_check(Engine& E, double half_buffer);
 double host_max_drift(Engine& E);
 void launch_thermo(Engine& E, int64_t step, dp_thermo* dst, double* mass_atom, double* ke_scratch);
+
+// dist.cpp
+void dist_init(Engine& E, int rank, int world, const void* uid);
+void dist_destroy(Engine& E);
+void dist_md_begin(Engine& E, int64_t N, const double* pos, const double* vel, const int32_t* types,
+                   const double* box, const uint8_t* pbc, const dp_md_config* cfg);
+void dist_rebuild(Engine& E);
+void dist_halo_forward(Engine& E);
+void dist_halo_reverse(Engine& E);
+void dist_allreduce_sum(Engine& E, double* dev, int count);
+int64_t dist_n_total(const Engine& E);
+void dist_md_end(Engine& E, double* gpos, double* gvel);
 
 } // namespace dpb

@@ -277,6 +277,7 @@ void Engine::launch_fitting() {
       std::swap(dyc, dyn);
     }
   }
+  if (n_centers < n) DPB_CUDA(cudaMemsetAsync(e_atom.p, 0, n * sizeof(double), stream));
   k_scatter_energy<<<ceil_div(n_slots, 256), 256, 0, stream>>>(n_slots, atom_of.p, e_slot.p, e_atom.p);
   ++launches;
 }

@@ -153,9 +153,10 @@ __global__ void k_pos4(int64_t n, const double* __restrict__ p3, double4* __rest
 // First half kick and drift (md.cpp:205-208): v += (dt/2 F) acc, x += dt v.
 __global__ void k_kick_drift(int64_t n, double half, double dt, const double* __restrict__ f,
                              const double* __restrict__ accf, double* __restrict__ v,
-                             double* __restrict__ x, double4* __restrict__ p4) {
+                             double* __restrict__ x, double4* __restrict__ p4,
+                             const uint8_t* __restrict__ center) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= n) return;
+  if (i >= n || !center[i]) return;
   double r[3];
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
@@ -169,9 +170,10 @@ __global__ void k_kick_drift(int64_t n, double half, double dt, const double* __
 
 // Second half kick (md.cpp:220-222).
 __global__ void k_kick(int64_t n, double half, const double* __restrict__ f,
-                       const double* __restrict__ accf, double* __restrict__ v) {
+                       const double* __restrict__ accf, double* __restrict__ v,
+                       const uint8_t* __restrict__ center) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= n) return;
+  if (i >= n || !center[i]) return;
 #pragma unroll
   for (int c = 0; c < 3; ++c)
     v[3 * i + c] = __dadd_rn(v[3 * i + c], __dmul_rn(__dmul_rn(half, f[3 * i + c]), accf[i]));
@@ -179,10 +181,11 @@ __global__ void k_kick(int64_t n, double half, const double* __restrict__ f,
 
 // max_i |x_i - x_i^ref|^2 (md.cpp:136-147) via integer max on the non-negative bit pattern.
 __global__ void k_drift2(int64_t n, const double* __restrict__ x, const double* __restrict__ ref,
-                         unsigned long long* out) {
+                         const uint8_t* __restrict__ center, unsigned long long* out) {
   unsigned long long best = 0;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (!center[i]) continue;
     double d2 = 0.0;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -209,9 +212,13 @@ __global__ void k_stale_check(const unsigned long long* d2bits, double half_buff
 
 // Kinetic energy per atom: 0.5 m v^2 MVV (md.cpp:172-178).
 __global__ void k_ke_atoms(int64_t n, const double* __restrict__ v, const double* __restrict__ mass,
-                           double mvv, double* __restrict__ ke) {
+                           double mvv, const uint8_t* __restrict__ center, double* __restrict__ ke) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= n) return;
+  if (!center[i]) {
+    ke[i] = 0.0;
+    return;
+  }
   const double v2 = v[3 * i] * v[3 * i] + v[3 * i + 1] * v[3 * i + 1] + v[3 * i + 2] * v[3 * i + 2];
   ke[i] = 0.5 * mass[i] * v2 * mvv;
 }
@@ -257,12 +264,13 @@ void launch_pos4(Engine& E) {
 
 void launch_kick_drift(Engine& E, double half, double dt) {
   k_kick_drift<<<ceil_div(E.n, 256), 256, 0, E.stream>>>(E.n, half, dt, E.forces.p, E.acc_fac.p,
-                                                         E.vel3.p, E.pos3.p, E.pos4.p);
+                                                         E.vel3.p, E.pos3.p, E.pos4.p, E.center.p);
   ++E.launches;
 }
 
 void launch_kick(Engine& E, double half) {
-  k_kick<<<ceil_div(E.n, 256), 256, 0, E.stream>>>(E.n, half, E.forces.p, E.acc_fac.p, E.vel3.p);
+  k_kick<<<ceil_div(E.n, 256), 256, 0, E.stream>>>(E.n, half, E.forces.p, E.acc_fac.p, E.vel3.p,
+                                                   E.center.p);
   ++E.launches;
 }
 
@@ -272,7 +280,7 @@ void launch_stale_check(Engine& E, double half_buffer) {
   unsigned long long* bits = reinterpret_cast<unsigned long long*>(E.red.p + 12);
   DPB_CUDA(cudaMemsetAsync(bits, 0, sizeof(unsigned long long), E.stream));
   const int blocks = std::max(1, std::min(ceil_div(E.n, 256), 1184));
-  k_drift2<<<blocks, 256, 0, E.stream>>>(E.n, E.pos3.p, E.ref_pos.p, bits);
+  k_drift2<<<blocks, 256, 0, E.stream>>>(E.n, E.pos3.p, E.ref_pos.p, E.center.p, bits);
   k_stale_check<<<1, 1, 0, E.stream>>>(bits, half_buffer, E.red.p + 11, E.err.p);
   E.launches += 2;
 }
@@ -282,7 +290,7 @@ double host_max_drift(Engine& E) {
   unsigned long long* bits = reinterpret_cast<unsigned long long*>(E.red.p + 12);
   DPB_CUDA(cudaMemsetAsync(bits, 0, sizeof(unsigned long long), E.stream));
   const int blocks = std::max(1, std::min(ceil_div(E.n, 256), 1184));
-  k_drift2<<<blocks, 256, 0, E.stream>>>(E.n, E.pos3.p, E.ref_pos.p, bits);
+  k_drift2<<<blocks, 256, 0, E.stream>>>(E.n, E.pos3.p, E.ref_pos.p, E.center.p, bits);
   ++E.launches;
   unsigned long long h = 0;
   DPB_CUDA(cudaMemcpyAsync(&h, bits, sizeof(h), cudaMemcpyDeviceToHost, E.stream));
@@ -294,13 +302,22 @@ double host_max_drift(Engine& E) {
 
 void launch_thermo(Engine& E, int64_t step, dp_thermo* dst, double* mass_atom, double* ke_scratch) {
   k_ke_atoms<<<ceil_div(E.n, 256), 256, 0, E.stream>>>(E.n, E.vel3.p, mass_atom, units::MVV_TO_EV,
-                                                       ke_scratch);
+                                                       E.center.p, ke_scratch);
   double* partial = E.red.p + 64;
   const int nb = static_cast<int>(std::min<int64_t>(RED_BLOCKS, std::max<int64_t>(1, E.n / 64)));
   k_reduce_cols<<<nb, RED_THREADS, 0, E.stream>>>(E.n, 1, ke_scratch, 1, partial);
   k_reduce_final<<<1, RED_BLOCKS, 0, E.stream>>>(nb, 1, partial, E.red.p + 10);
-  k_thermo<<<1, 1, 0, E.stream>>>(step, E.n, E.cell.vol, E.red.p, E.red.p + 10, dst);
-  E.launches += 4;
+  E.launches += 3;
+  const int64_t n_total = E.dist ? dist_n_total(E) : E.n;
+  if (E.dist) {
+    // energy, virial and kinetic energy summed over ranks (in scratch, red[0..10] stays local)
+    DPB_CUDA(cudaMemcpyAsync(E.red.p + 32, E.red.p, 11 * sizeof(double), cudaMemcpyDeviceToDevice, E.stream));
+    dist_allreduce_sum(E, E.red.p + 32, 11);
+    k_thermo<<<1, 1, 0, E.stream>>>(step, n_total, E.cell.vol, E.red.p + 32, E.red.p + 42, dst);
+  } else {
+    k_thermo<<<1, 1, 0, E.stream>>>(step, n_total, E.cell.vol, E.red.p, E.red.p + 10, dst);
+  }
+  ++E.launches;
 }
 
 } // namespace dpb

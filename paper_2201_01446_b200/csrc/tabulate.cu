@@ -37,6 +37,7 @@ struct TabParams {
   const int64_t* row_off;
   const uint64_t* keys;
   const int32_t* eown;  // [E] centre of each list entry
+  const uint8_t* center; // [n] 1 = evaluated centre, 0 = ghost
   int32_t* ebin;        // [E] global bin t*tn + interval of a real entry, -1 otherwise
   double* erc;          // [5][E] SoA: R0..R3, u of real entries
   int32_t* egrp;        // [E] group index of a real entry inside its centre
@@ -207,7 +208,8 @@ __device__ __forceinline__ double rs32(double* v, int lane) {
 __global__ void __launch_bounds__(256) k_env_fwd(TabParams p) {
   const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   bool ext = false;
-  if (e < p.E) {
+  if (e < p.E && !p.center[p.eown[e]]) p.ebin[e] = -1;
+  if (e < p.E && p.center[p.eown[e]]) {
     const int i = p.eown[e];
     const uint64_t key = p.keys[e];
     int sh[3];
@@ -544,8 +546,9 @@ __global__ void __launch_bounds__(64, 8) k_tab_fwd(TabParams p) {
         ts[a * p.Mp + f0 + q] = tacc[a][q];
       }
     __syncwarp();
-    double* Drow = p.D + static_cast<size_t>(p.slot_of[i]) * p.K0p;
-    if (f0 < p.M) {
+    const int slot = p.slot_of[i];
+    double* Drow = p.D + static_cast<size_t>(slot < 0 ? 0 : slot) * p.K0p;
+    if (slot >= 0 && f0 < p.M) {
       for (int qq = 0; qq < p.mlt; ++qq) {
         const double t0 = ts[qq], t1 = ts[p.Mp + qq], t2 = ts[2 * p.Mp + qq], t3 = ts[3 * p.Mp + qq];
         double dv[F];
@@ -602,8 +605,9 @@ __global__ void __launch_bounds__(64, 6) k_tab_bwd_P(TabParams p) {
         dT[a][q] = 0.0;
       }
     __syncwarp();
-    const double* dDrow = p.dD + static_cast<size_t>(p.slot_of[i]) * p.K0p;
-    const bool fon = f0 < p.M;
+    const int slot = p.slot_of[i];
+    const double* dDrow = p.dD + static_cast<size_t>(slot < 0 ? 0 : slot) * p.K0p;
+    const bool fon = f0 < p.M && slot >= 0;
     for (int q0 = 0; q0 < p.mlt; q0 += 8) {
       double part[32];
 #pragma unroll
@@ -747,6 +751,7 @@ TabParams make_params(Engine& E) {
   p.row_off = E.row_off.p;
   p.keys = E.keys.p;
   p.eown = E.eown.p;
+  p.center = E.center.p;
   p.ebin = E.ebin.p;
   p.erc = E.erc.p;
   p.egrp = E.egrp.p;

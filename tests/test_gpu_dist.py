@@ -1,0 +1,35 @@
+"""Multi-GPU domain decomposition (NCCL halo exchange) reproduces the single-GPU trajectory."""
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def n_gpus():
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+@pytest.mark.skipif(n_gpus() < 2, reason="needs >= 2 GPUs")
+def test_two_rank_md_matches_single_gpu(tmp_path):
+    out = tmp_path / "dist.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29611",
+           str(ROOT / "tests" / "dist" / "dist_md_check.py"), str(out)]
+    subprocess.run(cmd, check=True, timeout=600, cwd=ROOT)
+    r = json.loads(out.read_text())
+    assert r["force_evals"][0] == r["force_evals"][1] == 61
+    assert r["counters"][0] == r["counters"][1]
+    for a, b in r["pe"]:
+        assert abs(a - b) <= 1e-10 * abs(b)
+    for a, b in r["ke"]:
+        assert abs(a - b) <= 1e-9 * abs(b)
+    assert r["pos_normwise"] <= 1e-10 and r["vel_normwise"] <= 1e-8
