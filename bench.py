@@ -206,7 +206,7 @@ def run_ours(args, world, rank, local, dist):
     gvel = dp.init_velocities(gcfg, m, 330.0, 99)
     n_total = gcfg.n_atoms
     n = n_total // world
-    pot = dp.DeepPot(m, t, device=local)
+    pot = dp.DeepPot(m, t, device=local, precision=args.precision)
     if world > 1:
         uid = [dp.DeepPot.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
@@ -311,9 +311,12 @@ def run_ours(args, world, rank, local, dist):
                          "compute_energy_forces_virial_tabulated x3 + cell list /50"}
     if rank == 0:
         out = {
-            "metric": "MD atom-steps/s (Cu, FP64)", "value": value, "unit": "atom-steps/s",
+            "metric": "MD atom-steps/s (Cu, FP64)" if args.precision == "fp64" else
+                      "MD atom-steps/s (Cu, mixed: tcgen05 3xTF32 fitting + tanh table, 1e-5)",
+            "value": value, "unit": "atom-steps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64" if args.precision == "fp64" else "f64 env/tabulate, tf32x3 fitting",
             "data": "synthetic",
             "config": {"workload": spec["label"] + (" per GPU (weak scaling, slabs along x)" if world > 1 else ""),
                        "atoms_per_gpu": n, "atoms_total": n_total,
@@ -354,6 +357,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=30)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "mixed"])
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -17,6 +17,14 @@ namespace {
 
 int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
+// Fitting widths are padded (zero weights) to a GEMM-friendly size: a multiple of 16 that the
+// 80- or 64-column tiles divide (240 stays 240), else a multiple of 64.
+int pad_width(int w) {
+  const int w16 = round_up(w, 16);
+  if (w16 % 80 == 0 || w16 % 64 == 0) return w16;
+  return round_up(w, 64);
+}
+
 void raise_device_error(int code) {
   switch (code) {
     case DEV_OK: return;
@@ -75,14 +83,14 @@ void Engine::create(const dp_model_desc* md, const dp_table_desc* td, int dev, i
   }
   const int L = f0.n_layers;
   layers.resize(L);
-  widthp_max = 64;
+  widthp_max = 16;
   for (int k = 0; k < L; ++k) {
     FitLayer& fl = layers[k];
     fl.in = f0.widths[k];
     fl.out = f0.widths[k + 1];
     if (fl.out <= 0) throw InputErr("fitting layer widths are inconsistent");
-    fl.inp = k == 0 ? K0p : round_up(fl.in, 64);
-    fl.outp = round_up(fl.out, 64);
+    fl.inp = k == 0 ? K0p : pad_width(fl.in);
+    fl.outp = pad_width(fl.out);
     fl.shortcut = fl.in == fl.out;
     widthp_max = std::max(widthp_max, fl.outp);
   }
@@ -141,6 +149,7 @@ void Engine::create(const dp_model_desc* md, const dp_table_desc* td, int dev, i
     DPB_CUDA(cudaMemcpy(fit_wout[t].p, wo.data(), wo.size() * 8, cudaMemcpyHostToDevice));
     b_out[t] = f.b_out;
   }
+  if (precision == 1) prepare_mixed();
   d_max_nbr.ensure(n_types);
   DPB_CUDA(cudaMemcpy(d_max_nbr.p, max_nbr.data(), n_types * sizeof(int), cudaMemcpyHostToDevice));
   err.ensure(1);
@@ -176,6 +185,10 @@ void Engine::destroy() {
   scratch.ke.release();
   scratch.rec.release();
   if (dist) dist_destroy(*this);
+  for (auto* v : {&tc_wf, &tc_wb, &tc_bias, &tc_wout, &tc_t, &tc_y})
+    for (auto& b : *v) b.release();
+  tc_tanh.release(); tc_a3.release(); tc_y3a.release(); tc_y3b.release(); tc_dz3.release();
+  tc_dz3b.release(); tc_dy.release(); tc_dy2.release();
   if (stream) cudaStreamDestroy(stream);
   stream = nullptr;
 }
@@ -237,7 +250,7 @@ void Engine::set_config(int64_t nn, const double* pos, const int32_t* ty, const 
     int64_t at = 0;
     for (int t = 0; t < n_types; ++t) {
       seg_start[t] = static_cast<int>(at);
-      seg_rows[t] = round_up(seg_count[t], 64);
+      seg_rows[t] = round_up(seg_count[t], 128);
       at += seg_rows[t];
     }
     n_slots = at;
@@ -312,7 +325,10 @@ void Engine::evaluate() {
   phase_begin(1);
   launch_tab_fwd();
   phase_begin(2);
-  launch_fitting();
+  if (precision == 1)
+    launch_fitting_mixed();
+  else
+    launch_fitting();
   phase_begin(3);
   launch_tab_bwd();
   phase_begin(4);

@@ -184,6 +184,11 @@ struct Engine {
   void launch_nlist(double cutoff);
   void launch_tab_fwd();
   void launch_fitting();
+  void launch_fitting_mixed();
+  void prepare_mixed();
+  // mixed precision (tcgen05 3xTF32) buffers
+  std::vector<DevBuf<float>> tc_wf, tc_wb, tc_bias, tc_wout, tc_t, tc_y;
+  DevBuf<float> tc_tanh, tc_a3, tc_y3a, tc_y3b, tc_dz3, tc_dz3b, tc_dy, tc_dy2;
   void launch_tab_bwd();
   void launch_forces();
   // MD
@@ -196,6 +201,9 @@ struct Engine {
 
 // Small launch helpers.
 inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+// fitting.cu
+void scatter_energy(Engine& E);
 
 // force.cu
 void launch_pos4(Engine& E);

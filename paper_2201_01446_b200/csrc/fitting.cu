@@ -18,7 +18,7 @@ namespace dpb {
 
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, PITCH = BK + 4, STAGES = 3;
+constexpr int BM = 64, BK = 16, PITCH = BK + 4, STAGES = 3;
 
 enum Epi : int { EPI_FWD = 0, EPI_BWD = 1 };
 
@@ -55,8 +55,10 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-template <int EPI>
+// BN = 64 (4 DMMA column tiles per warp) or 80 (5): 240-wide layers tile exactly with 80.
+template <int EPI, int BN>
 __global__ void __launch_bounds__(128) k_gemm(GemmArgs g) {
+  constexpr int NT = BN / 16; // 8-wide column tiles per warp (2 warps across BN)
   extern __shared__ __align__(16) double sm[];
   double* As = sm;                                // [STAGES][BM][PITCH]
   double* Bs = sm + STAGES * BM * PITCH;          // [STAGES][BN][PITCH]
@@ -75,18 +77,23 @@ __global__ void __launch_bounds__(128) k_gemm(GemmArgs g) {
     double* bs = Bs + stage * BN * PITCH;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      const int idx = tid + c * 128; // 512 chunks of 2 doubles per operand
+      const int idx = tid + c * 128; // 512 chunks of 2 doubles for the A tile
       const int row = idx >> 3, col = (idx & 7) * 2;
       cp_async16(as + row * PITCH + col, A + static_cast<size_t>(row) * g.lda + k0 + col);
+    }
+#pragma unroll
+    for (int c = 0; c < BN / 16; ++c) {
+      const int idx = tid + c * 128; // BN*8 chunks for the B tile
+      const int row = idx >> 3, col = (idx & 7) * 2;
       cp_async16(bs + row * PITCH + col, B + static_cast<size_t>(row) * g.ldb + k0 + col);
     }
   };
 
-  double acc[4][4][2];
+  double acc[4][NT][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
@@ -100,29 +107,29 @@ __global__ void __launch_bounds__(128) k_gemm(GemmArgs g) {
     if (nk < KT) load_stage(nk % STAGES, nk);
     cp_commit();
     const double* as = As + (kt % STAGES) * BM * PITCH + (wm * 32 + gid) * PITCH + tig;
-    const double* bs = Bs + (kt % STAGES) * BN * PITCH + (wn * 32 + gid) * PITCH + tig;
+    const double* bs = Bs + (kt % STAGES) * BN * PITCH + (wn * (BN / 2) + gid) * PITCH + tig;
 #pragma unroll
     for (int kk = 0; kk < BK / 4; ++kk) {
-      double af[4], bf[4];
+      double af[4], bf[NT];
 #pragma unroll
       for (int i = 0; i < 4; ++i) af[i] = as[i * 8 * PITCH + kk * 4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = bs[j * 8 * PITCH + kk * 4];
+      for (int j = 0; j < NT; ++j) bf[j] = bs[j * 8 * PITCH + kk * 4];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
   }
   cp_wait<0>();
 
-  // Epilogue: thread holds rows (m0 + wm*32 + i*8 + gid), cols (n0 + wn*32 + j*8 + 2*tig + {0,1}).
+  // Epilogue: thread holds rows (m0 + wm*32 + i*8 + gid), cols (n0 + wn*BN/2 + j*8 + 2*tig + {0,1}).
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int row = m0 + wm * 32 + i * 8 + gid;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int col = n0 + wn * 32 + j * 8 + 2 * tig;
+    for (int j = 0; j < NT; ++j) {
+      const int col = n0 + wn * (BN / 2) + j * 8 + 2 * tig;
       const size_t o = static_cast<size_t>(row) * g.ldc + col;
       if (EPI == EPI_FWD) {
         const double2 b = *reinterpret_cast<const double2*>(g.bias + col);
@@ -185,30 +192,37 @@ __global__ void k_scatter_energy(int64_t slots, const int32_t* __restrict__ atom
   if (a >= 0) e_atom[a] = e_slot[s];
 }
 
-void run_gemm(int epi, const GemmArgs& a, int rows, int N, cudaStream_t st) {
+template <int EPI, int BN>
+void launch_gemm(const GemmArgs& a, int rows, int N, cudaStream_t st) {
   const size_t bytes = static_cast<size_t>(STAGES) * (BM + BN) * PITCH * sizeof(double);
-  dim3 grid(N / BN, rows / BM);
-  if (epi == EPI_FWD) {
-    static bool init = false;
-    if (!init) {
-      DPB_CUDA(cudaFuncSetAttribute(k_gemm<EPI_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(bytes)));
-      init = true;
-    }
-    k_gemm<EPI_FWD><<<grid, 128, bytes, st>>>(a);
-  } else {
-    static bool init = false;
-    if (!init) {
-      DPB_CUDA(cudaFuncSetAttribute(k_gemm<EPI_BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(bytes)));
-      init = true;
-    }
-    k_gemm<EPI_BWD><<<grid, 128, bytes, st>>>(a);
+  static bool init = false;
+  if (!init) {
+    DPB_CUDA(cudaFuncSetAttribute(k_gemm<EPI, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(bytes)));
+    init = true;
   }
+  k_gemm<EPI, BN><<<dim3(N / BN, rows / BM), 128, bytes, st>>>(a);
   DPB_CUDA(cudaGetLastError());
 }
 
+// N is a multiple of 80 or 64 (widths are padded by pad_width()).
+void run_gemm(int epi, const GemmArgs& a, int rows, int N, cudaStream_t st) {
+  const bool b80 = N % 80 == 0;
+  if (epi == EPI_FWD) {
+    if (b80) launch_gemm<EPI_FWD, 80>(a, rows, N, st);
+    else launch_gemm<EPI_FWD, 64>(a, rows, N, st);
+  } else {
+    if (b80) launch_gemm<EPI_BWD, 80>(a, rows, N, st);
+    else launch_gemm<EPI_BWD, 64>(a, rows, N, st);
+  }
+}
+
 } // namespace
+
+void scatter_energy(Engine& E) {
+  k_scatter_energy<<<ceil_div(E.n_slots, 256), 256, 0, E.stream>>>(E.n_slots, E.atom_of.p, E.e_slot.p, E.e_atom.p);
+  ++E.launches;
+}
 
 void Engine::launch_fitting() {
   const int L = static_cast<int>(layers.size());
@@ -278,8 +292,7 @@ void Engine::launch_fitting() {
     }
   }
   if (n_centers < n) DPB_CUDA(cudaMemsetAsync(e_atom.p, 0, n * sizeof(double), stream));
-  k_scatter_energy<<<ceil_div(n_slots, 256), 256, 0, stream>>>(n_slots, atom_of.p, e_slot.p, e_atom.p);
-  ++launches;
+  scatter_energy(*this);
 }
 
 } // namespace dpb

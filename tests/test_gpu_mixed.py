@@ -1,0 +1,58 @@
+"""Mixed-precision mode (tcgen05 3xTF32 fitting net + tanh table) within 1e-5 of the FP64 oracle
+("Mixed: same metrics at 1e-5")."""
+import numpy as np
+import pytest
+
+import oracle_lib as O
+import paper_2201_01446_b200 as dp
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+
+def check(r, ro):
+    assert abs(r.energy - ro.energy) <= TOL * abs(ro.energy), (r.energy, ro.energy)
+    assert O.normwise(r.forces, ro.forces) <= TOL
+    assert O.normwise(r.virial, ro.virial) <= TOL
+    assert O.normwise(r.per_atom_energy, ro.per_atom_energy) <= TOL
+
+
+def test_mixed_c1():
+    m = dp.gen_model("copper-like", 7)
+    t = dp.build_tables(m, 0.01)
+    c = dp.gen_config("copper-like", 8, 8, 8, 0.1, 11)
+    ro, co = O.or_compute(c, m, t)
+    pot = dp.DeepPot(m, t, precision="mixed")
+    r = pot.compute(c)
+    check(r, ro)
+    assert pot.counters == co
+
+
+@pytest.mark.parametrize("seed", [500, 501])
+def test_mixed_two_types(seed):
+    m = dp.make_test_model(2, 6, 8, 20, 2, [18, 18], 6.0, 5.0, 401)
+    t = dp.build_tables(m, 0.05)
+    c = dp.make_random_config(10, 2, 9.0, 1.8, seed)
+    ro, _ = O.or_compute(c, m, t)
+    check(dp.DeepPot(m, t, precision="mixed").compute(c), ro)
+
+
+def test_mixed_water():
+    m = dp.gen_model("water-like", 3)
+    t = dp.build_tables(m, 0.01)
+    c = dp.gen_config("water-like", 4, 4, 4, 0.1, 4)
+    ro, _ = O.or_compute(c, m, t)
+    check(dp.DeepPot(m, t, precision="mixed").compute(c), ro)
+
+
+def test_mixed_md_thermo():
+    m = dp.gen_model("copper-like", 7)
+    t = dp.build_tables(m, 0.01)
+    c = dp.gen_config("copper-like", 3, 3, 3, 0.1, 11)
+    v = dp.init_velocities(c, m, 330.0, 99)
+    mc = dp.MDConfig(n_steps=20, dt=1.0, buffer=2.0, rebuild_every=10, thermo_every=5)
+    a = dp.DeepPot(m, t, precision="mixed").run_md(c.copy(), v.copy(), mc)
+    b = O.or_run_md(c.copy(), v.copy(), m, t, mc)
+    for x, y in zip(a.thermo, b.thermo):
+        assert abs(x.pe - y.pe) <= TOL * abs(y.pe)
+        assert abs(x.ke - y.ke) <= 1e-4 * abs(y.ke)
