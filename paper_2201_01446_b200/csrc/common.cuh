@@ -26,6 +26,7 @@ enum DevErr : int {
   DEV_SHIFT_RANGE = 4, // image shift outside the packed key range
   DEV_ROW_CAP = 5,     // neighbour row longer than the sort capacity
   DEV_STALE = 6,       // list stale in MD (md.cpp:211-217)
+  DEV_PBUF = 7,        // tabulate group buffer too small (grows at the next list rebuild)
 };
 
 // Cell as the kernels see it (geom.hpp:14-44).

@@ -33,6 +33,7 @@ void raise_device_error(int code) {
     case DEV_TABLE_LOW: throw InputErr("table input below domain start");
     case DEV_SHIFT_RANGE: throw InputErr("image shift outside +-511 cells (positions too far from the box)");
     case DEV_ROW_CAP: throw NumErr("neighbour row exceeds the kernel capacity");
+    case DEV_PBUF: throw NumErr("tabulate group buffer overflow (retry: it grows at the next rebuild)");
     case DEV_STALE: throw NumErr("neighbor list stale: an atom moved more than half the buffer since the last rebuild");
     default: throw CudaErr("unknown device error " + std::to_string(code));
   }
@@ -170,7 +171,7 @@ void Engine::destroy() {
   types.release(); center.release(); slot_of.release(); atom_of.release(); row_off.release(); keys.release();
   rev.release(); bin_of.release(); bin_start.release(); bin_atoms.release(); bin_fill.release();
   frac.release(); ref_pos.release(); row_len.release(); nl_len.release(); scan_tmp.release();
-  skeys.release(); eown.release(); ebin.release(); egrp.release(); erc.release(); n_grp.release(); goff.release(); Pbuf.release(); n_real.release(); T.release(); D.release(); dD.release(); rel(act_t);
+  skeys.release(); eown.release(); ebin.release(); egrp.release(); erc.release(); n_grp.release(); goff.release(); Pbuf.release(); pbuf_cap = 0; n_real.release(); T.release(); D.release(); dD.release(); rel(act_t);
   rel(act_y); dz.release(); dy.release(); dz2.release(); dy2.release(); e_slot.release();
   e_atom.release(); g.release(); vpart.release(); forces.release();
   red.release(); counters.release(); err.release(); acc_fac.release();
@@ -230,6 +231,7 @@ void Engine::set_config(int64_t nn, const double* pos, const int32_t* ty, const 
   if (!same) {
     n = nn;
     list_valid = false;
+    pbuf_cap = 0; // resize the group buffer from the next evaluation's exact total
     h_types.assign(ty, ty + nn);
     types.ensure(n);
     DPB_CUDA(cudaMemcpyAsync(types.p, ty, n * sizeof(int32_t), cudaMemcpyHostToDevice, stream));
@@ -311,8 +313,9 @@ void Engine::upload_positions(const double* pos) {
 
 void Engine::build_list(double cutoff) {
   phase_begin(0);
-  launch_nlist(cutoff);
+  launch_nlist(cutoff); // synchronises: the last evaluation's group total is final here
   phase_end();
+  if (pbuf_cap > 0) grow_pbuf();
   skeys.ensure(n_entries + 1);
   ebin.ensure(n_entries + 1);
   egrp.ensure(n_entries + 1);

@@ -115,6 +115,9 @@ struct Engine {
   DevBuf<int32_t> n_grp;        // [n+1]
   DevBuf<int64_t> goff;         // [n+1]
   DevBuf<double> Pbuf;          // [groups][24]
+  int64_t pbuf_cap = 0;
+  int64_t* h_gtotal = nullptr;  // pinned: total groups of the last evaluation
+  void grow_pbuf();
   DevBuf<int32_t> n_real;
   DevBuf<double> T;
   DevBuf<double> D, dD;
@@ -188,7 +191,8 @@ struct Engine {
   void prepare_mixed();
   // mixed precision (tcgen05 3xTF32) buffers
   std::vector<DevBuf<float>> tc_wf, tc_wb, tc_bias, tc_wout, tc_t, tc_y;
-  DevBuf<float> tc_tanh, tc_a3, tc_y3a, tc_y3b, tc_dz3, tc_dz3b, tc_dy, tc_dy2;
+  DevBuf<double> tc_tanh;
+  DevBuf<float> tc_a3, tc_y3a, tc_y3b, tc_dz3, tc_dz3b, tc_dy, tc_dy2;
   void launch_tab_bwd();
   void launch_forces();
   // MD

@@ -30,7 +30,7 @@ struct TArgs {
   // forward
   const float* bias;    // [N]
   const float* xin;     // shortcut source [M][ldx] or null
-  float* tout;          // [M][ldc]
+  float* tout;          // [M][ldc] tanh'(z) = 1 - t^2 (evaluated in FP64: no cancellation near |t| = 1)
   float* yout;          // [M][ldc]
   float* y3;            // [M][3*ldc] split of y for the next layer (or null)
   // backward
@@ -40,7 +40,7 @@ struct TArgs {
   float* dz3;           // [M][3*ld3] split of dz for the next GEMM (or null)
   double* dD;           // [M][ldD] final layer-0 adjoint (FP64) or null
   int ldc, ldx, ld3, ldD;
-  const float* tanh_c;  // [8193][3]
+  const double* tanh_c; // [8193][3]
 };
 
 __device__ __forceinline__ float tf32r(float x) {
@@ -57,16 +57,16 @@ __device__ __forceinline__ void split_store(float* base, int K, int col, float x
   base[2 * K + col] = lo;
 }
 
-// TanhTable::operator() (tanh_table.hpp:18-30) in FP32.
-__device__ __forceinline__ float tanh_tab(const float* c, float x) {
-  const float ax = fabsf(x);
-  float t;
-  if (ax > 8.0f) {
-    t = 1.0f;
+// TanhTable::operator() (tanh_table.hpp:18-30).
+__device__ __forceinline__ double tanh_tab(const double* c, double x) {
+  const double ax = fabs(x);
+  double t;
+  if (ax > 8.0) {
+    t = 1.0;
   } else {
-    const int k = static_cast<int>(ax * 1024.0f);
-    const float u = ax - static_cast<float>(k) * (1.0f / 1024.0f);
-    const float* q = c + 3 * k;
+    const int k = static_cast<int>(ax * 1024.0);
+    const double u = ax - k * (1.0 / 1024.0);
+    const double* q = c + 3 * k;
     t = q[0] + u * (q[1] + u * q[2]);
   }
   return signbit(x) ? -t : t;
@@ -149,9 +149,9 @@ __global__ void __launch_bounds__(192, 2) k_tc_gemm(const __grid_constant__ CUte
         const float acc = __uint_as_float(v[j]);
         const size_t o = static_cast<size_t>(row) * g.ldc + col;
         if (EPI == T_FWD) {
-          const float t = tanh_tab(g.tanh_c, acc + g.bias[col]);
-          const float y = (g.xin ? g.xin[static_cast<size_t>(row) * g.ldx + col] : 0.0f) + t;
-          g.tout[o] = t;
+          const double td = tanh_tab(g.tanh_c, static_cast<double>(acc) + g.bias[col]);
+          const float y = (g.xin ? g.xin[static_cast<size_t>(row) * g.ldx + col] : 0.0f) + static_cast<float>(td);
+          g.tout[o] = static_cast<float>((1.0 - td) * (1.0 + td));
           g.yout[o] = y;
           if (g.y3) split_store(g.y3 + static_cast<size_t>(row) * 3 * g.ld3, g.ld3, col, y);
         } else {
@@ -160,8 +160,7 @@ __global__ void __launch_bounds__(192, 2) k_tc_gemm(const __grid_constant__ CUte
             g.dD[static_cast<size_t>(row) * g.ldD + col] = static_cast<double>(vv);
           } else {
             g.dyout[o] = vv;
-            const float tp = g.tprev[o];
-            split_store(g.dz3 + static_cast<size_t>(row) * 3 * g.ld3, g.ld3, col, vv * (1.0f - tp * tp));
+            split_store(g.dz3 + static_cast<size_t>(row) * 3 * g.ld3, g.ld3, col, vv * g.tprev[o]);
           }
         }
       }
@@ -192,8 +191,7 @@ __global__ void k_readout_tc(int rows, int ld, int width, const float* __restric
   for (int c = lane; c < ld; c += 32) {
     const float w = c < width ? wout[c] : 0.0f;
     acc += static_cast<double>(y[static_cast<size_t>(r) * ld + c]) * w;
-    const float tt = t[static_cast<size_t>(r) * ld + c];
-    split_store(dz3 + static_cast<size_t>(r) * 3 * ld, ld, c, w * (1.0f - tt * tt));
+    split_store(dz3 + static_cast<size_t>(r) * 3 * ld, ld, c, w * t[static_cast<size_t>(r) * ld + c]);
     dy[static_cast<size_t>(r) * ld + c] = w;
   }
   acc = warp_sum(acc);
@@ -336,9 +334,8 @@ void Engine::prepare_mixed() {
   }
   std::vector<double> tt(3 * 8193);
   dp_tanh_table(tt.data());
-  std::vector<float> tf(tt.begin(), tt.end());
-  tc_tanh.ensure(tf.size());
-  DPB_CUDA(cudaMemcpy(tc_tanh.p, tf.data(), tf.size() * 4, cudaMemcpyHostToDevice));
+  tc_tanh.ensure(tt.size());
+  DPB_CUDA(cudaMemcpy(tc_tanh.p, tt.data(), tt.size() * 8, cudaMemcpyHostToDevice));
 }
 
 void Engine::launch_fitting_mixed() {

@@ -46,6 +46,7 @@ struct TabParams {
   int32_t* n_grp;       // [n+1] groups per centre -> (scanned) offsets into Pbuf
   const int64_t* goff;  // [n+1] exclusive scan of n_grp
   double* Pbuf;         // [sum groups][24]
+  int64_t pcap;         // groups Pbuf can hold
   const double* tab;    // [type][interval][6][Mp]
   const int* max_nbr;
   DevCell c;
@@ -590,7 +591,11 @@ __global__ void __launch_bounds__(64, 6) k_tab_bwd_P(TabParams p) {
   for (int i = blockIdx.x * wpb + wid; i < p.n; i += gridDim.x * wpb) {
     const int64_t off = p.row_off[i];
     const int nreal = p.n_real[i];
-    const int G = p.n_grp[i];
+    int G = p.n_grp[i];
+    if (p.goff[i] + G > p.pcap) {
+      if (lane == 0) raise_err(p.err, DEV_PBUF);
+      G = 0;
+    }
     const uint64_t* sk = p.skeys + off;
     double* Pout = p.Pbuf + p.goff[i] * 24;
     // --- dT = adjoint of D = T<^T T (contract.hpp:21-38) ---
@@ -712,7 +717,13 @@ __global__ void __launch_bounds__(256) k_tab_bwd_g(TabParams p) {
   Env ev;
   env_of(p, ld_pos(p.pos, i), p.keys[e], ev);
   const int th = bin % p.tn;
-  const double* P = p.Pbuf + (p.goff[i] + p.egrp[e]) * 24;
+  const int64_t gi = p.goff[i] + p.egrp[e];
+  if (gi >= p.pcap) {
+    raise_err(p.err, DEV_PBUF);
+    ge[0] = ge[1] = ge[2] = 0.0;
+    return;
+  }
+  const double* P = p.Pbuf + gi * 24;
   const double R[4] = {ev.s, ev.s * ev.u[0], ev.s * ev.u[1], ev.s * ev.u[2]};
   const double uu = ev.s - node_x(p.x0, p.h, th);
   double drow[4], dsum = 0.0;
@@ -760,6 +771,7 @@ TabParams make_params(Engine& E) {
   p.n_grp = E.n_grp.p;
   p.goff = E.goff.p;
   p.Pbuf = E.Pbuf.p;
+  p.pcap = E.pbuf_cap;
   p.tab = E.tab.p;
   p.max_nbr = E.d_max_nbr.p;
   p.c = E.cell;
@@ -845,10 +857,22 @@ void Engine::launch_tab_fwd() {
   scan_tmp.ensure(tb + 1);
   cub::DeviceScan::ExclusiveSum(scan_tmp.p, tb, n_grp.p, goff.p, n + 1, stream);
   ++launches;
-  int64_t total = 0;
-  DPB_CUDA(cudaMemcpyAsync(&total, goff.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
-  DPB_CUDA(cudaStreamSynchronize(stream));
-  Pbuf.ensure(static_cast<size_t>(total) * 24 + 24);
+  // Pbuf capacity: sized with one sync on first use, re-checked at every list rebuild (which
+  // synchronises anyway); the backward kernel refuses to write past it (DEV_PBUF).
+  if (!h_gtotal) DPB_CUDA(cudaMallocHost(&h_gtotal, sizeof(int64_t)));
+  DPB_CUDA(cudaMemcpyAsync(h_gtotal, goff.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+  if (pbuf_cap == 0 || !md_active) { // single evaluations size it exactly (they sync anyway)
+    DPB_CUDA(cudaStreamSynchronize(stream));
+    grow_pbuf();
+  }
+}
+
+void Engine::grow_pbuf() {
+  const int64_t want = *h_gtotal + *h_gtotal / 4 + 1024;
+  if (want > pbuf_cap) {
+    Pbuf.ensure(static_cast<size_t>(want) * 24);
+    pbuf_cap = want;
+  }
 }
 
 void Engine::launch_tab_bwd() {
