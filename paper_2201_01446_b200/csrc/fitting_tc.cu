@@ -7,7 +7,7 @@
 // The activation is the reference's quadratic tanh table (tanh_table.cpp:5-21, mixed mode only).
 //
 // Kernel: CTA 128 x BN tile (UMMA M=128, N=BN <= 256), warp-specialized: warp 0 issues TMA tile
-// loads (16-byte K chunks, canonical K-major interleaved layout), warp 1 issues tcgen05.mma from
+// loads (128-byte K atoms, SWIZZLE_128B canonical K-major layout), warp 1 issues tcgen05.mma from
 // one thread, warps 2-5 drain the TMEM accumulator (tcgen05.ld 32x32b) and run the fused epilogue.
 // 4-stage smem ring with full/empty mbarriers; tcgen05.commit releases stages.
 #include <cuda.h>
@@ -21,7 +21,7 @@ namespace dpb {
 
 namespace {
 
-constexpr int TBM = 128, TBKB = 64, TST = 4;
+constexpr int TBM = 128, TBKB = 128, TST = 4; // one 128-byte swizzle atom of K per stage
 
 enum TEpi : int { T_FWD = 0, T_BWD = 1 };
 
@@ -73,12 +73,15 @@ __device__ __forceinline__ double tanh_tab(const double* c, double x) {
 }
 
 template <int EPI, int BN>
-__global__ void __launch_bounds__(192, 2) k_tc_gemm(const __grid_constant__ CUtensorMap ta,
+__global__ void __launch_bounds__(192, 1) k_tc_gemm(const __grid_constant__ CUtensorMap ta,
                                                    const __grid_constant__ CUtensorMap tb, TArgs g) {
   using namespace tc;
   constexpr int A_ST = TBM * TBKB, B_ST = BN * TBKB;
   constexpr int TCOLS = BN <= 128 ? 128 : 256;
-  extern __shared__ __align__(1024) unsigned char smem[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // SWIZZLE_128B tiles need 1024-byte aligned bases
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   unsigned char* sa = smem;
   unsigned char* sb = smem + TST * A_ST;
   uint64_t* full = reinterpret_cast<uint64_t*>(sb + TST * B_ST);
@@ -87,7 +90,7 @@ __global__ void __launch_bounds__(192, 2) k_tc_gemm(const __grid_constant__ CUte
   uint32_t* tslot = reinterpret_cast<uint32_t*>(accf + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * TBM, n0 = blockIdx.y * BN;
-  const int KT = g.K3bytes / TBKB;
+  const int KT = (g.K3bytes + TBKB - 1) / TBKB; // TMA zero-fills the tail of the last block
   if (warp == 0) {
     tmem_alloc<TCOLS>(tslot);
     if (lane == 0) {
@@ -112,11 +115,8 @@ __global__ void __launch_bounds__(192, 2) k_tc_gemm(const __grid_constant__ CUte
       const int s = kt % TST;
       if (kt >= TST) mbar_wait(empty + s, ((kt / TST) - 1) & 1);
       mbar_expect_tx(full + s, A_ST + B_ST);
-#pragma unroll
-      for (int c = 0; c < TBKB / 16; ++c) {
-        tma_load_2d(sa + s * A_ST + c * TBM * 16, &ta, kt * TBKB + c * 16, m0, full + s);
-        tma_load_2d(sb + s * B_ST + c * BN * 16, &tb, kt * TBKB + c * 16, n0, full + s);
-      }
+      tma_load_2d(sa + s * A_ST, &ta, kt * TBKB, m0, full + s);
+      tma_load_2d(sb + s * B_ST, &tb, kt * TBKB, n0, full + s);
     }
   } else if (warp == 1 && lane == 0) {
     constexpr uint32_t idesc = make_idesc(TBM, BN, 2, 1);
@@ -127,9 +127,7 @@ __global__ void __launch_bounds__(192, 2) k_tc_gemm(const __grid_constant__ CUte
       const uint32_t a0 = smem_u32(sa + s * A_ST), b0 = smem_u32(sb + s * B_ST);
 #pragma unroll
       for (int k = 0; k < TBKB / 32; ++k) {
-        const uint64_t ad = make_desc(a0 + k * 2 * TBM * 16, TBM * 16, 128);
-        const uint64_t bd = make_desc(b0 + k * 2 * BN * 16, BN * 16, 128);
-        mma_tf32(tmem, ad, bd, idesc, (kt | k) ? 1u : 0u);
+        mma_tf32(tmem, make_desc_sw128(a0 + k * 32), make_desc_sw128(b0 + k * 32), idesc, (kt | k) ? 1u : 0u);
       }
       commit(empty + s);
     }
@@ -216,15 +214,15 @@ EncodeFn encoder() {
   return fn;
 }
 
-// Byte-level 2-D map over [rows][row_bytes] with 16-byte x box_rows boxes.
+// Byte-level 2-D map over [rows][row_bytes] with 128-byte x box_rows boxes, 128B swizzle.
 CUtensorMap byte_map(const void* ptr, uint64_t rows, uint64_t row_bytes, uint32_t box_rows) {
   CUtensorMap m;
   cuuint64_t dims[2] = {row_bytes, rows};
   cuuint64_t strides[1] = {row_bytes};
-  cuuint32_t box[2] = {16, box_rows};
+  cuuint32_t box[2] = {128, box_rows};
   cuuint32_t es[2] = {1, 1};
   const CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(ptr), dims, strides, box,
-                               es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                               es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaErr("cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
   return m;
@@ -232,7 +230,7 @@ CUtensorMap byte_map(const void* ptr, uint64_t rows, uint64_t row_bytes, uint32_
 
 template <int EPI, int BN>
 void launch_tc(const float* A3, const float* B3, int rows, int N, int K, TArgs g, cudaStream_t st) {
-  const size_t smem = static_cast<size_t>(TST) * (TBM + BN) * TBKB + 8 * (2 * TST + 1) + 16;
+  const size_t smem = static_cast<size_t>(TST) * (TBM + BN) * TBKB + 8 * (2 * TST + 1) + 16 + 1024;
   static bool init = false;
   if (!init) {
     DPB_CUDA(cudaFuncSetAttribute(k_tc_gemm<EPI, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,

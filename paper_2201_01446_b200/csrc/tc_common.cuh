@@ -27,6 +27,19 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo_bytes
   return d;
 }
 
+// Shared-memory matrix descriptor for the K-major SWIZZLE_128B canonical layout: rows of 128 B
+// (TMA box inner size 128 B with CU_TENSOR_MAP_SWIZZLE_128B), 8-row atoms 1024 B apart (SBO).
+// Tile base must be 1024-byte aligned; K steps inside the atom advance the start by 32 B.
+__device__ __forceinline__ uint64_t make_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>(1) << 16;                   // LBO (unused for swizzled K-major)
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;           // SBO = 1024 B
+  d |= static_cast<uint64_t>(1) << 46;                   // version
+  d |= static_cast<uint64_t>(2) << 61;                   // SWIZZLE_128B
+  return d;
+}
+
 // Instruction descriptor: F32 accumulate, A/B format (TF32 = 2 for kind::tf32; for kind::i8
 // 0 = u8, 1 = s8 with c_format 2 = S32), both K-major, N >> 3, M >> 4.
 __host__ __device__ constexpr uint32_t make_idesc(int M, int N, int ab_format, int c_format) {
