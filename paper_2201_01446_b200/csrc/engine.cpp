@@ -186,10 +186,10 @@ void Engine::destroy() {
   scratch.ke.release();
   scratch.rec.release();
   if (dist) dist_destroy(*this);
-  for (auto* v : {&tc_wf, &tc_wb, &tc_bias, &tc_wout, &tc_t, &tc_y})
+  for (auto* v : {&tc_wf, &tc_wb, &tc_bias, &tc_wout, &tc_t})
     for (auto& b : *v) b.release();
-  tc_tanh.release(); tc_a3.release(); tc_y3a.release(); tc_y3b.release(); tc_dz3.release();
-  tc_dz3b.release(); tc_dy.release(); tc_dy2.release();
+  tc_tanh.release(); tc_d2.release(); tc_y2a.release(); tc_y2b.release(); tc_dz2a.release();
+  tc_dz2b.release(); tc_dya.release(); tc_dyb.release();
   if (stream) cudaStreamDestroy(stream);
   stream = nullptr;
 }
@@ -282,18 +282,22 @@ void Engine::ensure_step_buffers() {
   const int L = static_cast<int>(layers.size());
   T.ensure(static_cast<size_t>(n) * 4 * Mp);
   const size_t dsz = static_cast<size_t>(n_slots) * K0p;
-  const bool grow = D.n < dsz;
-  D.ensure(dsz);
   dD.ensure(dsz);
-  if (grow || true) DPB_CUDA(cudaMemsetAsync(D.p, 0, D.n * sizeof(double), stream));
-  act_t.resize(L);
-  act_y.resize(L);
-  const size_t asz = static_cast<size_t>(n_slots) * widthp_max;
-  for (int k = 0; k < L; ++k) {
-    act_t[k].ensure(asz);
-    act_y[k].ensure(asz);
+  if (precision == 1) {
+    // mixed: the tabulate kernel writes D directly as the split FP32 operand of the tcgen05 GEMM
+    ensure_mixed_buffers();
+  } else {
+    D.ensure(dsz);
+    DPB_CUDA(cudaMemsetAsync(D.p, 0, D.n * sizeof(double), stream));
+    act_t.resize(L);
+    act_y.resize(L);
+    const size_t asz = static_cast<size_t>(n_slots) * widthp_max;
+    for (int k = 0; k < L; ++k) {
+      act_t[k].ensure(asz);
+      act_y[k].ensure(asz);
+    }
+    dz.ensure(asz); dy.ensure(asz); dz2.ensure(asz); dy2.ensure(asz);
   }
-  dz.ensure(asz); dy.ensure(asz); dz2.ensure(asz); dy2.ensure(asz);
   e_slot.ensure(n_slots);
   e_atom.ensure(n);
 

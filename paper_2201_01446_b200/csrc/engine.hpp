@@ -188,11 +188,12 @@ struct Engine {
   void launch_tab_fwd();
   void launch_fitting();
   void launch_fitting_mixed();
+  void ensure_mixed_buffers();
   void prepare_mixed();
   // mixed precision (tcgen05 3xTF32) buffers
-  std::vector<DevBuf<float>> tc_wf, tc_wb, tc_bias, tc_wout, tc_t, tc_y;
+  std::vector<DevBuf<float>> tc_wf, tc_wb, tc_bias, tc_wout, tc_t;
   DevBuf<double> tc_tanh;
-  DevBuf<float> tc_a3, tc_y3a, tc_y3b, tc_dz3, tc_dz3b, tc_dy, tc_dy2;
+  DevBuf<float> tc_d2, tc_y2a, tc_y2b, tc_dz2a, tc_dz2b, tc_dya, tc_dyb;
   void launch_tab_bwd();
   void launch_forces();
   // MD

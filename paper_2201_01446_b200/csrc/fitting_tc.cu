@@ -21,25 +21,35 @@ namespace dpb {
 
 namespace {
 
-constexpr int TBM = 128, TBKB = 128, TST = 4; // one 128-byte swizzle atom of K per stage
+constexpr int TBM = 128, TBKB = 128, TST = 2; // one 128-byte swizzle atom of K per stage; 2 CTAs/SM
+constexpr int CW = 16;                          // epilogue column chunk
+constexpr int SP = CW + 4;                      // staging row pitch in floats (conflict-free v4 access)
+constexpr int SPD = CW + 2;                     // staging row pitch in doubles
+constexpr int STAGE_IN = 2 * TBM * SP * 4;      // two input arrays
+constexpr int STAGE_OUT = 3 * TBM * SP * 4;     // three output arrays (one buffer)
+constexpr int STAGE_BYTES = STAGE_IN + 2 * STAGE_OUT;
 
 enum TEpi : int { T_FWD = 0, T_BWD = 1 };
 
+// Operands are stored as [hi | lo] halves of kseg floats each (kseg a multiple of 32 so every
+// 128-byte TMA box lies inside one half); the 3xTF32 product A.B ~= Ahi.Bhi + Ahi.Blo + Alo.Bhi
+// is three K segments of ONE accumulation chain, selected by the TMA x coordinate.
 struct TArgs {
-  int K3bytes;          // 3*K*4
+  int kseg;             // floats per half of an A / B row
   // forward
   const float* bias;    // [N]
-  const float* xin;     // shortcut source [M][ldx] or null
-  float* tout;          // [M][ldc] tanh'(z) = 1 - t^2 (evaluated in FP64: no cancellation near |t| = 1)
-  float* yout;          // [M][ldc]
-  float* y3;            // [M][3*ldc] split of y for the next layer (or null)
+  const float* xin2;    // shortcut source y_{k-1} as [M][2*ldx] (hi|lo) or null
+  int ldx;
+  float* tout;          // [M][ldc] tanh'(z) = (1 - t)(1 + t), t from the FP64 table (no cancellation)
+  float* y2;            // [M][2*ld2] (hi|lo) split of y for the next layer / readout
   // backward
-  const float* dyin;    // [M][ldc] or null
-  const float* tprev;   // [M][ldc] or null
-  float* dyout;         // [M][ldc] or null
-  float* dz3;           // [M][3*ld3] split of dz for the next GEMM (or null)
-  double* dD;           // [M][ldD] final layer-0 adjoint (FP64) or null
-  int ldc, ldx, ld3, ldD;
+  const float* dyin;    // [M][ldc] shortcut adjoint or null
+  const float* dyvec;   // [N] row-independent shortcut adjoint (readout's dy = w_out) or null
+  const float* tprev;   // [M][ldc] tanh' of the previous layer (null for layer 0)
+  float* dyout;         // [M][ldc]
+  float* dz2;           // [M][2*ld2] (hi|lo) split of dz for the next GEMM
+  double* dD;           // [M][ldD] layer-0 adjoint (FP64) or null
+  int ldc, ld2, ldD;
   const double* tanh_c; // [8193][3]
 };
 
@@ -47,14 +57,6 @@ __device__ __forceinline__ float tf32r(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
-}
-
-__device__ __forceinline__ void split_store(float* base, int K, int col, float x) {
-  const float hi = tf32r(x);
-  const float lo = tf32r(x - hi);
-  base[col] = hi;
-  base[K + col] = hi;
-  base[2 * K + col] = lo;
 }
 
 // TanhTable::operator() (tanh_table.hpp:18-30).
@@ -72,25 +74,47 @@ __device__ __forceinline__ double tanh_tab(const double* c, double x) {
   return signbit(x) ? -t : t;
 }
 
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
+
+// Coalesced [128 x CW] float tile copies between global (row pitch ld floats) and staging.
+__device__ __forceinline__ void tile_in(float* s, const float* g, size_t ld, int et) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int idx = et + 128 * j, r = idx >> 2, c4 = idx & 3;
+    *reinterpret_cast<float4*>(s + r * SP + 4 * c4) =
+        __ldg(reinterpret_cast<const float4*>(g + r * ld + 4 * c4));
+  }
+}
+__device__ __forceinline__ void tile_out(float* g, const float* s, size_t ld, int et) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int idx = et + 128 * j, r = idx >> 2, c4 = idx & 3;
+    *reinterpret_cast<float4*>(g + r * ld + 4 * c4) = *reinterpret_cast<const float4*>(s + r * SP + 4 * c4);
+  }
+}
+
 template <int EPI, int BN>
-__global__ void __launch_bounds__(192, 1) k_tc_gemm(const __grid_constant__ CUtensorMap ta,
+__global__ void __launch_bounds__(192, 2) k_tc_gemm(const __grid_constant__ CUtensorMap ta,
                                                    const __grid_constant__ CUtensorMap tb, TArgs g) {
   using namespace tc;
   constexpr int A_ST = TBM * TBKB, B_ST = BN * TBKB;
-  constexpr int TCOLS = BN <= 128 ? 128 : 256;
+  constexpr int PIPE = TST * (A_ST + B_ST);
+  constexpr int BODY = PIPE > STAGE_BYTES ? PIPE : STAGE_BYTES;
+  constexpr int TCOLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // SWIZZLE_128B tiles need 1024-byte aligned bases
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   unsigned char* sa = smem;
   unsigned char* sb = smem + TST * A_ST;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sb + TST * B_ST);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + BODY);
   uint64_t* empty = full + TST;
   uint64_t* accf = empty + TST;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(accf + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * TBM, n0 = blockIdx.y * BN;
-  const int KT = (g.K3bytes + TBKB - 1) / TBKB; // TMA zero-fills the tail of the last block
+  const int KB = g.kseg / 32;   // 128-byte blocks per half
+  const int KT = 3 * KB;
   if (warp == 0) {
     tmem_alloc<TCOLS>(tslot);
     if (lane == 0) {
@@ -111,12 +135,14 @@ __global__ void __launch_bounds__(192, 1) k_tc_gemm(const __grid_constant__ CUte
   fence_after();
   const uint32_t tmem = *tslot;
   if (warp == 0 && lane == 0) {
+    const int half = g.kseg * 4;
     for (int kt = 0; kt < KT; ++kt) {
       const int s = kt % TST;
+      const int seg = kt / KB, kb = kt - seg * KB;
       if (kt >= TST) mbar_wait(empty + s, ((kt / TST) - 1) & 1);
       mbar_expect_tx(full + s, A_ST + B_ST);
-      tma_load_2d(sa + s * A_ST, &ta, kt * TBKB, m0, full + s);
-      tma_load_2d(sb + s * B_ST, &tb, kt * TBKB, n0, full + s);
+      tma_load_2d(sa + s * A_ST, &ta, (seg == 2 ? half : 0) + kb * TBKB, m0, full + s);
+      tma_load_2d(sb + s * B_ST, &tb, (seg == 1 ? half : 0) + kb * TBKB, n0, full + s);
     }
   } else if (warp == 1 && lane == 0) {
     constexpr uint32_t idesc = make_idesc(TBM, BN, 2, 1);
@@ -135,33 +161,96 @@ __global__ void __launch_bounds__(192, 1) k_tc_gemm(const __grid_constant__ CUte
   } else if (warp >= 2) {
     mbar_wait(accf, 0);
     fence_after();
+    // the operand ring is drained: reuse it as epilogue staging
+    float* sin0 = reinterpret_cast<float*>(smem);
+    float* sin1 = sin0 + TBM * SP;
+    float* sout = sin0 + 2 * TBM * SP;
     const int q = warp & 3;
-    const int row = m0 + q * 32 + lane;
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      uint32_t v[16];
-      tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + c0, v);
-      tmem_wait_ld();
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int col = n0 + c0 + j;
-        const float acc = __uint_as_float(v[j]);
-        const size_t o = static_cast<size_t>(row) * g.ldc + col;
-        if (EPI == T_FWD) {
-          const double td = tanh_tab(g.tanh_c, static_cast<double>(acc) + g.bias[col]);
-          const float y = (g.xin ? g.xin[static_cast<size_t>(row) * g.ldx + col] : 0.0f) + static_cast<float>(td);
-          g.tout[o] = static_cast<float>((1.0 - td) * (1.0 + td));
-          g.yout[o] = y;
-          if (g.y3) split_store(g.y3 + static_cast<size_t>(row) * 3 * g.ld3, g.ld3, col, y);
-        } else {
-          const float vv = acc + (g.dyin ? g.dyin[o] : 0.0f);
-          if (g.dD) {
-            g.dD[static_cast<size_t>(row) * g.ldD + col] = static_cast<double>(vv);
-          } else {
-            g.dyout[o] = vv;
-            split_store(g.dz3 + static_cast<size_t>(row) * 3 * g.ld3, g.ld3, col, vv * g.tprev[o]);
-          }
+    const int et = threadIdx.x - 64;         // 0..127 epilogue thread
+    const int r = q * 32 + lane;             // tile row owned after tcgen05.ld (TMEM lane)
+    const size_t row0 = static_cast<size_t>(m0);
+    for (int c0 = 0, ci = 0; c0 < BN; c0 += CW, ++ci) {
+      const int col0 = n0 + c0;
+      float* so = sout + (ci & 1) * 3 * TBM * SP;
+      // stage the inputs of this chunk (coalesced)
+      bool staged = false;
+      if (EPI == T_FWD) {
+        if (g.xin2) {
+          const size_t ld = 2 * static_cast<size_t>(g.ldx);
+          tile_in(sin0, g.xin2 + row0 * ld + col0, ld, et);
+          tile_in(sin1, g.xin2 + row0 * ld + g.ldx + col0, ld, et);
+          staged = true;
+        }
+      } else {
+        if (g.dyin) {
+          tile_in(sin0, g.dyin + row0 * g.ldc + col0, g.ldc, et);
+          staged = true;
+        }
+        if (g.tprev) {
+          tile_in(sin1, g.tprev + row0 * g.ldc + col0, g.ldc, et);
+          staged = true;
         }
       }
+      uint32_t v[CW];
+      tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + c0, v);
+      tmem_wait_ld();
+      if (staged) epi_bar();
+      if (EPI == T_FWD) {
+#pragma unroll
+        for (int j = 0; j < CW; ++j) {
+          const double z = static_cast<double>(__uint_as_float(v[j])) + static_cast<double>(g.bias[col0 + j]);
+          const double td = tanh_tab(g.tanh_c, z);
+          double y = td;
+          if (g.xin2) y += static_cast<double>(sin0[r * SP + j]) + static_cast<double>(sin1[r * SP + j]);
+          const float yf = static_cast<float>(y);
+          const float hi = tf32r(yf);
+          so[r * SP + j] = static_cast<float>((1.0 - td) * (1.0 + td));
+          so[TBM * SP + r * SP + j] = hi;
+          so[2 * TBM * SP + r * SP + j] = tf32r(yf - hi);
+        }
+        epi_bar();
+        tile_out(g.tout + row0 * g.ldc + col0, so, g.ldc, et);
+        if (g.y2) {
+          const size_t ld = 2 * static_cast<size_t>(g.ld2);
+          tile_out(g.y2 + row0 * ld + col0, so + TBM * SP, ld, et);
+          tile_out(g.y2 + row0 * ld + g.ld2 + col0, so + 2 * TBM * SP, ld, et);
+        }
+      } else if (g.dD) {
+        double* sd = reinterpret_cast<double*>(so);
+#pragma unroll
+        for (int j = 0; j < CW; ++j) {
+          float vv = __uint_as_float(v[j]);
+          if (g.dyin) vv += sin0[r * SP + j];
+          else if (g.dyvec) vv += g.dyvec[col0 + j];
+          sd[r * SPD + j] = static_cast<double>(vv);
+        }
+        epi_bar();
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          const int idx = et + 128 * jj, rr = idx >> 3, c2 = idx & 7;
+          *reinterpret_cast<double2*>(g.dD + (row0 + rr) * g.ldD + col0 + 2 * c2) =
+              *reinterpret_cast<const double2*>(sd + rr * SPD + 2 * c2);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < CW; ++j) {
+          float vv = __uint_as_float(v[j]);
+          if (g.dyin) vv += sin0[r * SP + j];
+          else if (g.dyvec) vv += g.dyvec[col0 + j];
+          const float dz = vv * sin1[r * SP + j];
+          const float hi = tf32r(dz);
+          so[r * SP + j] = vv;
+          so[TBM * SP + r * SP + j] = hi;
+          so[2 * TBM * SP + r * SP + j] = tf32r(dz - hi);
+        }
+        epi_bar();
+        tile_out(g.dyout + row0 * g.ldc + col0, so, g.ldc, et);
+        const size_t ld = 2 * static_cast<size_t>(g.ld2);
+        tile_out(g.dz2 + row0 * ld + col0, so + TBM * SP, ld, et);
+        tile_out(g.dz2 + row0 * ld + g.ld2 + col0, so + 2 * TBM * SP, ld, et);
+      }
+      // the next chunk overwrites sin0/sin1: every thread must be done reading them
+      if (staged) epi_bar();
     }
   }
   fence_before();
@@ -169,28 +258,23 @@ __global__ void __launch_bounds__(192, 1) k_tc_gemm(const __grid_constant__ CUte
   if (warp == 0) tmem_free<TCOLS>(tmem);
 }
 
-// FP64 D rows -> 3xTF32 split [hi|hi|lo] along K.
-__global__ void k_split_d(int64_t rows, int K, const double* __restrict__ D, float* __restrict__ X3) {
-  const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (idx >= rows * K) return;
-  const int64_t r = idx / K;
-  const int c = static_cast<int>(idx % K);
-  split_store(X3 + r * 3 * K, K, c, static_cast<float>(D[idx]));
-}
-
-// Readout: E = b_out + y . w_out; dz_L = w_out (1 - t^2) (split), dy_L = w_out.
-__global__ void k_readout_tc(int rows, int ld, int width, const float* __restrict__ y,
+// Readout: E = b_out + y . w_out (y = hi + lo); dz_L = w_out tanh'(z_L) split (hi|lo).
+__global__ void k_readout_tc(int rows, int ld, int ld2, int width, const float* __restrict__ y2,
                              const float* __restrict__ t, const float* __restrict__ wout, double bout,
-                             double* __restrict__ e, float* __restrict__ dz3, float* __restrict__ dy) {
+                             double* __restrict__ e, float* __restrict__ dz2) {
   const int lane = threadIdx.x & 31;
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= rows) return;
+  const float* yr = y2 + static_cast<size_t>(r) * 2 * ld2;
+  float* dr = dz2 + static_cast<size_t>(r) * 2 * ld2;
   double acc = 0.0;
   for (int c = lane; c < ld; c += 32) {
     const float w = c < width ? wout[c] : 0.0f;
-    acc += static_cast<double>(y[static_cast<size_t>(r) * ld + c]) * w;
-    split_store(dz3 + static_cast<size_t>(r) * 3 * ld, ld, c, w * t[static_cast<size_t>(r) * ld + c]);
-    dy[static_cast<size_t>(r) * ld + c] = w;
+    acc += (static_cast<double>(yr[c]) + static_cast<double>(yr[ld2 + c])) * w;
+    const float dz = w * t[static_cast<size_t>(r) * ld + c];
+    const float hi = tf32r(dz);
+    dr[c] = hi;
+    dr[ld2 + c] = tf32r(dz - hi);
   }
   acc = warp_sum(acc);
   if (lane == 0) e[r] = bout + acc;
@@ -229,81 +313,84 @@ CUtensorMap byte_map(const void* ptr, uint64_t rows, uint64_t row_bytes, uint32_
 }
 
 template <int EPI, int BN>
-void launch_tc(const float* A3, const float* B3, int rows, int N, int K, TArgs g, cudaStream_t st) {
-  const size_t smem = static_cast<size_t>(TST) * (TBM + BN) * TBKB + 8 * (2 * TST + 1) + 16 + 1024;
+void launch_tc(const float* A2, const float* B2, int rows, int N, TArgs g, cudaStream_t st) {
+  constexpr int PIPE = TST * (TBM + BN) * TBKB;
+  const size_t smem = static_cast<size_t>(PIPE > STAGE_BYTES ? PIPE : STAGE_BYTES) + 8 * (2 * TST + 1) + 16 + 1024;
   static bool init = false;
   if (!init) {
     DPB_CUDA(cudaFuncSetAttribute(k_tc_gemm<EPI, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     init = true;
   }
-  g.K3bytes = 3 * K * 4;
-  const CUtensorMap ta = byte_map(A3, rows, static_cast<uint64_t>(3) * K * 4, TBM);
-  const CUtensorMap tb = byte_map(B3, N, static_cast<uint64_t>(3) * K * 4, BN);
+  const uint64_t row_bytes = static_cast<uint64_t>(2) * g.kseg * 4;
+  const CUtensorMap ta = byte_map(A2, rows, row_bytes, TBM);
+  const CUtensorMap tb = byte_map(B2, N, row_bytes, BN);
   k_tc_gemm<EPI, BN><<<dim3(rows / TBM, N / BN), 192, smem, st>>>(ta, tb, g);
   DPB_CUDA(cudaGetLastError());
 }
 
-void run_tc(int epi, const float* A3, const float* B3, int rows, int N, int K, const TArgs& g, cudaStream_t st) {
-  if (N % 240 == 0 && N <= 240) {
-    if (epi == T_FWD) launch_tc<T_FWD, 240>(A3, B3, rows, N, K, g, st);
-    else launch_tc<T_BWD, 240>(A3, B3, rows, N, K, g, st);
-  } else if (N % 256 == 0) {
-    if (epi == T_FWD) launch_tc<T_FWD, 256>(A3, B3, rows, N, K, g, st);
-    else launch_tc<T_BWD, 256>(A3, B3, rows, N, K, g, st);
-  } else if (N % 128 == 0) {
-    if (epi == T_FWD) launch_tc<T_FWD, 128>(A3, B3, rows, N, K, g, st);
-    else launch_tc<T_BWD, 128>(A3, B3, rows, N, K, g, st);
-  } else if (N % 64 == 0) {
-    if (epi == T_FWD) launch_tc<T_FWD, 64>(A3, B3, rows, N, K, g, st);
-    else launch_tc<T_BWD, 64>(A3, B3, rows, N, K, g, st);
-  } else if (N % 16 == 0 && N <= 256) {
-    // single tile of N columns: round the tile to the next supported size is not allowed (the
-    // map would read past the operand), so widths are padded to 64 by the engine in mixed mode
-    throw InputErr("mixed precision needs fitting widths padded to 64");
-  } else {
-    throw InputErr("unsupported fitting width for the tensor-core path");
-  }
+template <int EPI>
+void run_tc_epi(const float* A2, const float* B2, int rows, int N, const TArgs& g, cudaStream_t st) {
+  if (N % 240 == 0 && N <= 240) launch_tc<EPI, 240>(A2, B2, rows, N, g, st);
+  else if (N % 256 == 0) launch_tc<EPI, 256>(A2, B2, rows, N, g, st);
+  else if (N % 160 == 0 && N <= 160) launch_tc<EPI, 160>(A2, B2, rows, N, g, st);
+  else if (N % 128 == 0) launch_tc<EPI, 128>(A2, B2, rows, N, g, st);
+  else if (N % 80 == 0) launch_tc<EPI, 80>(A2, B2, rows, N, g, st);
+  else if (N % 64 == 0) launch_tc<EPI, 64>(A2, B2, rows, N, g, st);
+  else throw InputErr("unsupported fitting width for the tensor-core path");
 }
 
+void run_tc(int epi, const float* A2, const float* B2, int rows, int N, const TArgs& g, cudaStream_t st) {
+  if (epi == T_FWD) run_tc_epi<T_FWD>(A2, B2, rows, N, g, st);
+  else run_tc_epi<T_BWD>(A2, B2, rows, N, g, st);
+}
+
+} // namespace
+
+namespace {
+int seg32(int k) { return (k + 31) / 32 * 32; }
+
+// host tf32 round-to-nearest-away (matches cvt.rna): add half a tf32 ulp and truncate
+float rna_tf32(float v) {
+  uint32_t b;
+  std::memcpy(&b, &v, 4);
+  b = (b + 0x1000u) & 0xFFFFE000u;
+  float o;
+  std::memcpy(&o, &b, 4);
+  return o;
+}
+
+// rows x K (row-major FP64) -> rows x [hi(kseg) | lo(kseg)] FP32, zero padded
+void split2(std::vector<float>& dst, const std::vector<double>& src, int rows, int K, int kseg) {
+  dst.assign(static_cast<size_t>(rows) * 2 * kseg, 0.f);
+  for (int r = 0; r < rows; ++r)
+    for (int c = 0; c < K; ++c) {
+      const float x = static_cast<float>(src[static_cast<size_t>(r) * K + c]);
+      const float hi = rna_tf32(x);
+      float* d = dst.data() + static_cast<size_t>(r) * 2 * kseg;
+      d[c] = hi;
+      d[kseg + c] = rna_tf32(x - hi);
+    }
+}
+
+void ensure_zeroed(DevBuf<float>& b, size_t count, cudaStream_t st) {
+  if (count <= b.n) return;
+  b.ensure(count);
+  DPB_CUDA(cudaMemsetAsync(b.p, 0, b.n * sizeof(float), st));
+}
 } // namespace
 
 void Engine::prepare_mixed() {
   for (size_t k = 1; k < layers.size(); ++k)
     if (layers[k].outp != widthp_max || layers[k].inp != widthp_max)
       throw InputErr("mixed precision needs equal hidden widths");
-  // weights: forward B = W^T rows [out][in] -> [hi|lo|hi] along in; backward B = W rows [in][out]
+  if (K0p % 32 != 0) throw InputErr("mixed precision needs a descriptor width that is a multiple of 32");
+  // forward B = W^T rows [out][in] split along in; backward B = W rows [in][out] split along out
   const int L = static_cast<int>(layers.size());
   tc_wf.resize(n_types * L);
   tc_wb.resize(n_types * L);
   tc_bias.resize(n_types * L);
   tc_wout.resize(n_types);
-  std::vector<double> hw;
-  auto split3 = [](std::vector<float>& dst, const std::vector<double>& src, int rows, int K) {
-    dst.assign(static_cast<size_t>(rows) * 3 * K, 0.f);
-    for (int r = 0; r < rows; ++r)
-      for (int c = 0; c < K; ++c) {
-        const float x = static_cast<float>(src[static_cast<size_t>(r) * K + c]);
-        uint32_t xb;
-        std::memcpy(&xb, &x, 4);
-        // host tf32 round-to-nearest-away (cvt.rna): add half an ulp of tf32 and truncate
-        auto rna = [](float v) {
-          uint32_t b;
-          std::memcpy(&b, &v, 4);
-          b = (b + 0x1000u) & 0xFFFFE000u;
-          float o;
-          std::memcpy(&o, &b, 4);
-          return o;
-        };
-        const float hi = rna(x);
-        const float lo = rna(x - hi);
-        float* d = dst.data() + static_cast<size_t>(r) * 3 * K;
-        d[c] = hi;
-        d[K + c] = lo;
-        d[2 * K + c] = hi;
-        (void)xb;
-      }
-  };
   for (int t = 0; t < n_types; ++t)
     for (int k = 0; k < L; ++k) {
       const FitLayer& fl = layers[k];
@@ -312,10 +399,10 @@ void Engine::prepare_mixed() {
       DPB_CUDA(cudaMemcpy(wt.data(), fit_wt[t * L + k].p, wt.size() * 8, cudaMemcpyDeviceToHost));
       DPB_CUDA(cudaMemcpy(b.data(), fit_b[t * L + k].p, b.size() * 8, cudaMemcpyDeviceToHost));
       std::vector<float> f;
-      split3(f, wt, fl.outp, fl.inp);
+      split2(f, wt, fl.outp, fl.inp, seg32(fl.inp));
       tc_wf[t * L + k].ensure(f.size());
       DPB_CUDA(cudaMemcpy(tc_wf[t * L + k].p, f.data(), f.size() * 4, cudaMemcpyHostToDevice));
-      split3(f, w, fl.inp, fl.outp);
+      split2(f, w, fl.inp, fl.outp, seg32(fl.outp));
       tc_wb[t * L + k].ensure(f.size());
       DPB_CUDA(cudaMemcpy(tc_wb[t * L + k].p, f.data(), f.size() * 4, cudaMemcpyHostToDevice));
       std::vector<float> bf(b.begin(), b.end());
@@ -336,85 +423,85 @@ void Engine::prepare_mixed() {
   DPB_CUDA(cudaMemcpy(tc_tanh.p, tt.data(), tt.size() * 8, cudaMemcpyHostToDevice));
 }
 
+// Mixed-mode buffers. Pad columns of the split operands must stay zero: they are cleared once
+// at allocation and never written (the epilogues write only the real N columns).
+void Engine::ensure_mixed_buffers() {
+  const int L = static_cast<int>(layers.size());
+  const int wpm = widthp_max, s2 = seg32(wpm);
+  ensure_zeroed(tc_d2, static_cast<size_t>(n_slots) * 2 * K0p, stream);
+  ensure_zeroed(tc_y2a, static_cast<size_t>(n_slots) * 2 * s2, stream);
+  ensure_zeroed(tc_y2b, static_cast<size_t>(n_slots) * 2 * s2, stream);
+  ensure_zeroed(tc_dz2a, static_cast<size_t>(n_slots) * 2 * s2, stream);
+  ensure_zeroed(tc_dz2b, static_cast<size_t>(n_slots) * 2 * s2, stream);
+  tc_t.resize(L);
+  for (int k = 0; k < L; ++k) tc_t[k].ensure(static_cast<size_t>(n_slots) * wpm);
+  tc_dya.ensure(static_cast<size_t>(n_slots) * wpm);
+  tc_dyb.ensure(static_cast<size_t>(n_slots) * wpm);
+}
+
 void Engine::launch_fitting_mixed() {
   const int L = static_cast<int>(layers.size());
-  const int wpm = widthp_max;
-  const size_t kmax = static_cast<size_t>(std::max(K0p, wpm));
-  tc_a3.ensure(static_cast<size_t>(n_slots) * 3 * kmax);
-  tc_dz3.ensure(static_cast<size_t>(n_slots) * 3 * wpm);
-  tc_dz3b.ensure(static_cast<size_t>(n_slots) * 3 * wpm);
-  tc_t.resize(L);
-  tc_y.resize(L);
-  for (int k = 0; k < L; ++k) {
-    tc_t[k].ensure(static_cast<size_t>(n_slots) * wpm);
-    tc_y[k].ensure(static_cast<size_t>(n_slots) * wpm);
-  }
-  tc_y3a.ensure(static_cast<size_t>(n_slots) * 3 * wpm);
-  tc_y3b.ensure(static_cast<size_t>(n_slots) * 3 * wpm);
-  tc_dy.ensure(static_cast<size_t>(n_slots) * wpm);
-  tc_dy2.ensure(static_cast<size_t>(n_slots) * wpm);
-  // the layer-0 input: D rows (FP64) -> split3
-  {
-    const int64_t tot = n_slots * static_cast<int64_t>(K0p);
-    k_split_d<<<ceil_div(tot, 256), 256, 0, stream>>>(n_slots, K0p, D.p, tc_a3.p);
-    ++launches;
-  }
+  const int wpm = widthp_max, s2 = seg32(wpm);
   for (int t = 0; t < n_types; ++t) {
     const int rows = seg_rows[t];
     if (rows == 0) continue;
     const size_t r0 = static_cast<size_t>(seg_start[t]);
-    // forward: layer 0 reads the split D from a3, layer k > 0 the split y_{k-1} (ping-pong)
-    const float* xin_prev = nullptr;
-    const float* A3 = tc_a3.p + r0 * 3 * static_cast<size_t>(K0p);
-    int ldk = K0p;
+    // forward: layer 0 reads the split D (written by the tabulate kernel), layer k > 0 the split
+    // y_{k-1} (ping-pong), which is also the shortcut source
+    const float* A2 = tc_d2.p + r0 * 2 * K0p;
+    const float* yprev = nullptr;
     for (int k = 0; k < L; ++k) {
       const FitLayer& fl = layers[k];
       TArgs g{};
+      g.kseg = k == 0 ? K0p : s2;
       g.bias = tc_bias[t * L + k].p;
-      g.xin = fl.shortcut ? xin_prev : nullptr;
-      g.ldx = wpm;
+      g.xin2 = fl.shortcut ? yprev : nullptr;
+      g.ldx = s2;
       g.tout = tc_t[k].p + r0 * wpm;
-      g.yout = tc_y[k].p + r0 * wpm;
       g.ldc = wpm;
-      float* y3 = (k & 1 ? tc_y3b.p : tc_y3a.p) + r0 * 3 * static_cast<size_t>(wpm);
-      g.y3 = k + 1 < L ? y3 : nullptr;
-      g.ld3 = wpm;
+      float* y2 = (k & 1 ? tc_y2b.p : tc_y2a.p) + r0 * 2 * s2;
+      g.y2 = y2;
+      g.ld2 = s2;
       g.tanh_c = tc_tanh.p;
-      run_tc(T_FWD, A3, tc_wf[t * L + k].p, rows, fl.outp, ldk, g, stream);
+      run_tc(T_FWD, A2, tc_wf[t * L + k].p, rows, fl.outp, g, stream);
       ++launches;
-      xin_prev = g.yout;
-      A3 = y3;
-      ldk = fl.outp;
+      yprev = y2;
+      A2 = y2;
     }
     // readout
     const FitLayer& last = layers[L - 1];
-    float* dz3c = tc_dz3.p + r0 * 3 * wpm;
-    float* dz3n = tc_dz3b.p + r0 * 3 * wpm;
-    float* dyc = tc_dy.p + r0 * wpm;
-    float* dyn = tc_dy2.p + r0 * wpm;
-    k_readout_tc<<<ceil_div(rows, 4), 128, 0, stream>>>(rows, wpm, last.out, tc_y[L - 1].p + r0 * wpm,
-                                                        tc_t[L - 1].p + r0 * wpm, tc_wout[t].p, b_out[t],
-                                                        e_slot.p + r0, dz3c, dyc);
+    float* dzc = tc_dz2a.p + r0 * 2 * s2;
+    float* dzn = tc_dz2b.p + r0 * 2 * s2;
+    float* dyc = tc_dya.p + r0 * wpm;
+    float* dyn = tc_dyb.p + r0 * wpm;
+    k_readout_tc<<<ceil_div(rows, 4), 128, 0, stream>>>(rows, wpm, s2, last.out, yprev, tc_t[L - 1].p + r0 * wpm,
+                                                        tc_wout[t].p, b_out[t], e_slot.p + r0, dzc);
     ++launches;
+    const float* dy_mat = nullptr;     // dy of the layer above (matrix), null at the top
+    const float* dy_vec = tc_wout[t].p; // dy_L = w_out for every row
     for (int k = L - 1; k >= 0; --k) {
       const FitLayer& fl = layers[k];
       TArgs g{};
-      g.dyin = fl.shortcut ? dyc : nullptr;
+      g.kseg = s2;
       g.ldc = wpm;
-      g.tanh_c = tc_tanh.p;
+      g.ld2 = s2;
+      if (fl.shortcut) {
+        g.dyin = dy_mat;
+        g.dyvec = dy_mat ? nullptr : dy_vec;
+      }
       if (k > 0) {
         g.tprev = tc_t[k - 1].p + r0 * wpm;
         g.dyout = dyn;
-        g.dz3 = dz3n;
-        g.ld3 = wpm;
+        g.dz2 = dzn;
       } else {
         g.dD = dD.p + r0 * K0p;
         g.ldD = K0p;
       }
-      run_tc(T_BWD, dz3c, tc_wb[t * L + k].p, rows, fl.inp, fl.outp, g, stream);
+      run_tc(T_BWD, dzc, tc_wb[t * L + k].p, rows, fl.inp, g, stream);
       ++launches;
-      std::swap(dz3c, dz3n);
+      std::swap(dzc, dzn);
       std::swap(dyc, dyn);
+      dy_mat = dyc;
     }
   }
   if (n_centers < n) DPB_CUDA(cudaMemsetAsync(e_atom.p, 0, n * sizeof(double), stream));

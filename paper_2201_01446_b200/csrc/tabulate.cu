@@ -57,13 +57,20 @@ struct TabParams {
   int64_t E;
   const int32_t* slot_of;
   double* T;            // [n][4][Mp]
-  double* D;            // [slots][K0p]
+  double* D;            // [slots][K0p] (FP64 mode)
+  float* D2;            // [slots][2*K0p] mixed mode: tf32 split (hi | lo) of D, the tcgen05 operand
   const double* dD;
   double* g;            // [E][3]
   unsigned long long* counters;
   int* err;
   int scap;
 };
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
 
 __device__ __forceinline__ double node_x(double x0, double h, int th) {
   return __dadd_rn(x0, __dmul_rn(static_cast<double>(th), h));
@@ -561,6 +568,17 @@ __global__ void __launch_bounds__(64, 8) k_tab_fwd(TabParams p) {
           acc += t3 * tacc[3][q];
           dv[q] = acc;
         }
+        if (p.D2) {
+          float* d2 = p.D2 + static_cast<size_t>(slot) * 2 * p.K0p + qq * p.M + f0;
+#pragma unroll
+          for (int q = 0; q < F; ++q) {
+            const float x = static_cast<float>(dv[q]);
+            const float hi = tf32_rna(x);
+            d2[q] = hi;
+            d2[p.K0p + q] = tf32_rna(x - hi);
+          }
+          continue;
+        }
         double* dst = Drow + qq * p.M + f0;
         if constexpr (F % 2 == 0) {
           if ((p.M & 1) == 0) {
@@ -791,7 +809,8 @@ TabParams make_params(Engine& E) {
   p.E = E.n_entries;
   p.slot_of = E.slot_of.p;
   p.T = E.T.p;
-  p.D = E.D.p;
+  p.D = E.precision == 1 ? nullptr : E.D.p;
+  p.D2 = E.precision == 1 ? E.tc_d2.p : nullptr;
   p.dD = E.dD.p;
   p.g = E.g.p;
   p.counters = E.counters.p;
