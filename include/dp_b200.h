@@ -112,6 +112,42 @@ int dp_destroy(dp_handle* h);
 const char* dp_last_error(const dp_handle* h);
 const char* dp_version(void);
 
+/* ---- exact (untabulated) path, GPU table build, rmse tooling ---- */
+
+/* EmbeddingNet (model.hpp:14-20) of one neighbour type: 1 -> d1 -> 2 d1 -> 4 d1, row-major
+ * w1[d1][2 d1], w2[2 d1][4 d1]. */
+typedef struct {
+  int d1;
+  const double *w0, *b0, *w1, *b1, *w2, *b2;
+} dp_embedding_desc;
+
+/* Attach the embedding nets (n_types of them, indexed by neighbour type) to a handle; needed by
+ * dp_compute_exact and dp_build_tables_gpu. dp_create accepts tables == NULL when the tables
+ * are to be built on the device. */
+int dp_set_embedding(dp_handle* h, const dp_embedding_desc* nets);
+
+/* compute_energy_forces_virial (exact.cpp:155-173): the full embedding net per neighbour, on the
+ * GPU. Same arguments and outputs as dp_compute; the list cutoff is r_cut (+ skin). */
+int dp_compute_exact(dp_handle* h, int64_t n, const double* pos, const int32_t* types, const double box[9],
+                     const uint8_t pbc[3], double* energy, double* forces, double* virial,
+                     double* atom_energy);
+
+/* build_tables (table.cpp:77-162) on the GPU from the attached embedding nets: domain
+ * [0, table_domain_end(model, 0.5)], step h. First call with coeffs == NULL returns n_intervals
+ * and x_end; coeffs (n_types * n * ceil(4 d1 / 16) * 6 * 16 doubles, block B = 16) is filled on
+ * the second call. install != 0 makes these the handle's tables. A table that does not
+ * reproduce the net at a node within 1e-10 returns DP_NUMERICAL_ERROR (table.cpp:133-147). */
+int dp_build_tables_gpu(dp_handle* h, double step, uint64_t* n_intervals, double* x_end, double* coeffs,
+                        int install);
+
+/* rmse_sweep (rmse.cpp:63-97): for every step in h_list, build + install tables on the GPU and
+ * compare the tabulated path with the exact path on every configuration (lists at r_cut).
+ * Configurations are concatenated: n_atoms[c] atoms each, pos/types/box/pbc back to back.
+ * Outputs rmse_e (eV/atom) and rmse_f (eV/A) per step. The handle keeps the last tables. */
+int dp_rmse_sweep(dp_handle* h, int n_configs, const int64_t* n_atoms, const double* pos, const int32_t* types,
+                  const double* boxes, const uint8_t* pbcs, int n_h, const double* h_list, double* rmse_e,
+                  double* rmse_f);
+
 /* Neighbor-list skin for dp_compute: lists are built at r_cut + skin and reused while every atom
  * stayed within skin/2 of its build position (same staleness rule as run_md, md.cpp:211-217).
  * skin = 0 (default) rebuilds on every call, i.e. list = build_neighbor_list(cfg, r_cut). */

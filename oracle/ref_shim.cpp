@@ -26,6 +26,7 @@
 #include "dpmd/md.hpp"
 #include "dpmd/model_io.hpp"
 #include "dpmd/neighbor.hpp"
+#include "dpmd/rmse.hpp"
 #include "dpmd/table.hpp"
 #include "helpers.hpp"
 
@@ -343,6 +344,42 @@ int ref_partition_domain(int64_t n, const double* pos, const double* box, const 
       for (int i : part.workers[w].owned) owner[i] = static_cast<int32_t>(w);
       for (int i : part.workers[w].ghosts) ghost_mask[w * n + i] = 1;
     }
+  });
+}
+
+// rmse_sweep (rmse.cpp:63-97) over concatenated configurations; loglog_slope (rmse.cpp:99-116).
+int ref_rmse_sweep(const dp_preset* s, const double* blob, int n_configs, const int64_t* n_atoms,
+                   const double* pos, const int32_t* types, const double* boxes, const uint8_t* pbcs,
+                   int n_h, const double* h_list, double* rmse_e, double* rmse_f, double* slope) {
+  return guarded([&] {
+    auto m = blob_to_model(*s, blob);
+    std::vector<AtomicConfig> cfgs;
+    int64_t at = 0;
+    for (int c = 0; c < n_configs; ++c) {
+      cfgs.push_back(make_cfg(n_atoms[c], pos + 3 * at, types + at, boxes + 9 * c, pbcs + 3 * c, s->n_types));
+      at += n_atoms[c];
+    }
+    std::vector<double> hl(h_list, h_list + n_h);
+    auto rows = rmse_sweep(m, hl, cfgs, 1);
+    for (int k = 0; k < n_h; ++k) {
+      rmse_e[k] = rows[k].rmse_e;
+      rmse_f[k] = rows[k].rmse_f;
+    }
+    *slope = loglog_slope(rows);
+  });
+}
+
+// write_model / read_model (model_io.cpp:226-283).
+int ref_write_model(const char* path, const dp_preset* s, const double* blob, const char* preset, uint64_t seed) {
+  return guarded([&] { write_model(path, blob_to_model(*s, blob), preset, seed); });
+}
+
+int ref_read_model(const char* path, const dp_preset* s, double* blob, uint64_t* seed) {
+  return guarded([&] {
+    ModelFile mf = read_model(path);
+    if (mf.model.n_types() != s->n_types || mf.model.d1() != s->d1) throw InputError("shape mismatch");
+    model_to_blob(mf.model, blob);
+    *seed = mf.seed;
   });
 }
 

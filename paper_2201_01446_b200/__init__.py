@@ -21,6 +21,7 @@ present, the GPU entry points raise instead of computing anything on the host.
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 from dataclasses import dataclass, field
 from pathlib import Path
@@ -70,6 +71,10 @@ class _TableDesc(C.Structure):
     _fields_ = [("n_tables", C.c_int), ("x0", C.c_double), ("h", C.c_double),
                 ("n", C.c_uint64), ("m", C.c_int), ("block", C.c_int),
                 ("coeffs", C.POINTER(C.POINTER(C.c_double)))]
+
+
+class _EmbDesc(C.Structure):
+    _fields_ = [("d1", C.c_int)] + [(k, C.POINTER(C.c_double)) for k in ("w0", "b0", "w1", "b1", "w2", "b2")]
 
 
 class _Counters(C.Structure):
@@ -156,6 +161,10 @@ def _lib():
                                    C.POINTER(U64), D, D], I),
         "dp_read_tables": ([C.c_char_p, D], I),
         "dp_tanh_table": ([D], I),
+        "dp_set_embedding": ([P, C.POINTER(_EmbDesc)], I),
+        "dp_compute_exact": ([P, I64, D, I32P, D, U8P, D, D, D, D], I),
+        "dp_build_tables_gpu": ([P, C.c_double, C.POINTER(U64), D, D, I], I),
+        "dp_rmse_sweep": ([P, I, C.POINTER(I64), D, I32P, D, U8P, I, D, D, D], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -294,6 +303,13 @@ class DPModel:
         shape = Preset(s.name, s.n_types, list(s.masses), list(s.max_nbr), s.r_cut, s.r_smooth,
                        s.d1, s.m_lt, s.fit_width, s.fit_hidden, s.lattice_a, list(s.site_pattern))
         return DPModel(shape, self.blob.copy())
+
+    def embedding_desc(self):
+        """ctypes dp_embedding_desc[n_types] (model.hpp:14-20) plus the arrays it points into."""
+        arr = (_EmbDesc * self.shape.n_types)()
+        for t, e in enumerate(self.embedding):
+            arr[t] = _EmbDesc(self.shape.d1, *[_dp(e[k]) for k in ("w0", "b0", "w1", "b1", "w2", "b2")])
+        return arr, [self.blob]
 
     def desc(self):
         """ctypes dp_model_desc (plus the objects that keep its pointers alive)."""
@@ -535,17 +551,24 @@ class MDResult:
 class DeepPot:
     """One dp_handle: model + tables resident on one B200, evaluation on sm_100a kernels."""
 
-    def __init__(self, model: DPModel, tables: Tables, device: int = 0, precision: str = "fp64"):
+    def __init__(self, model: DPModel, tables: Optional[Tables] = None, device: int = 0,
+                 precision: str = "fp64"):
+        """tables=None: build them on the GPU later with build_tables_gpu(h)."""
         if precision not in ("fp64", "mixed"):
             raise InputError("precision must be 'fp64' or 'mixed'")
         self.model, self.tables = model, tables
         md, self._mkeep = model.desc()
-        td, self._tkeep = tables.desc()
+        if tables is not None:
+            td, self._tkeep = tables.desc()
+            tdp = C.byref(td)
+        else:
+            tdp = None
         h = C.c_void_p()
-        rc = _lib().dp_create(C.byref(md), C.byref(td), device, 0 if precision == "fp64" else 1,
-                              C.byref(h))
+        rc = _lib().dp_create(C.byref(md), tdp, device, 0 if precision == "fp64" else 1, C.byref(h))
         _check(rc, None)
         self._h = h
+        ed, keep = model.embedding_desc()
+        _check(_lib().dp_set_embedding(self._h, ed), self._h)
         self.counters = FusedCounters()
 
     def close(self) -> None:
@@ -605,6 +628,54 @@ class DeepPot:
         _lib().dp_counters_get(self._h, C.byref(c))
         self.counters = FusedCounters(c.rows_forward, c.rows_backward, c.extrapolations)
         return EvalResult(e.value, ae, f, v)
+
+    def compute_exact(self, cfg: AtomicConfig) -> EvalResult:
+        """compute_energy_forces_virial (exact.cpp:155-173): full embedding net, on the GPU."""
+        n = cfg.n_atoms
+        e = C.c_double()
+        f = np.empty((n, 3), dtype=np.float64)
+        v = np.empty(9, dtype=np.float64)
+        ae = np.empty(n, dtype=np.float64)
+        rc = _lib().dp_compute_exact(self._h, n, _dp(cfg.pos), _ip(cfg.type), _dp(cfg.h),
+                                     _u8(cfg.periodic), C.byref(e), _dp(f), _dp(v), _dp(ae))
+        _check(rc, self._h)
+        return EvalResult(e.value, ae, f, v)
+
+    def build_tables_gpu(self, h: float, install: bool = True) -> Tables:
+        """build_tables (table.cpp:77-162) on the GPU from this handle's embedding nets."""
+        n = C.c_uint64()
+        xe = C.c_double()
+        _check(_lib().dp_build_tables_gpu(self._h, h, C.byref(n), C.byref(xe), None, 0), self._h)
+        m = 4 * self.model.shape.d1
+        stride = ((m + 15) // 16) * 6 * 16
+        coeffs = np.empty((self.model.shape.n_types, n.value * stride), dtype=np.float64)
+        _check(_lib().dp_build_tables_gpu(self._h, h, C.byref(n), C.byref(xe), _dp(coeffs),
+                                          1 if install else 0), self._h)
+        tabs = Tables(0.0, h, n.value, m, 16, coeffs)
+        if install:
+            self.tables = tabs
+        return tabs
+
+    def rmse_sweep(self, h_list: Sequence[float], configs: Sequence[AtomicConfig]) -> List["SweepRow"]:
+        """rmse_sweep (rmse.cpp:63-97): GPU tables per step vs the GPU exact path."""
+        if len(h_list) == 0:
+            raise InputError("sweep needs at least one step size")
+        na = np.array([c.n_atoms for c in configs], dtype=np.int64)
+        pos = np.ascontiguousarray(np.concatenate([c.pos.reshape(-1) for c in configs]) if configs else
+                                   np.zeros(1), dtype=np.float64)
+        typ = np.ascontiguousarray(np.concatenate([c.type for c in configs]) if configs else
+                                   np.zeros(1, dtype=np.int32), dtype=np.int32)
+        box = np.ascontiguousarray(np.concatenate([c.h.reshape(-1) for c in configs]) if configs else
+                                   np.zeros(9), dtype=np.float64)
+        pbc = np.ascontiguousarray(np.concatenate([c.periodic for c in configs]) if configs else
+                                   np.zeros(3, dtype=np.uint8), dtype=np.uint8)
+        hl = np.ascontiguousarray(h_list, dtype=np.float64)
+        re = np.empty(len(hl), dtype=np.float64)
+        rf = np.empty(len(hl), dtype=np.float64)
+        _check(_lib().dp_rmse_sweep(self._h, len(configs), na.ctypes.data_as(C.POINTER(C.c_int64)), _dp(pos),
+                                    _ip(typ), _dp(box), _u8(pbc), len(hl), _dp(hl), _dp(re), _dp(rf)),
+               self._h)
+        return [SweepRow(float(h), float(e), float(f)) for h, e, f in zip(hl, re, rf)]
 
     def neighbor_list(self, cfg: AtomicConfig, cutoff: float) -> NeighborList:
         total = C.c_int64()
@@ -766,3 +837,96 @@ def run_md(cfg: AtomicConfig, vel: np.ndarray, model: DPModel, tables: Tables,
     if mc.n_workers < 1:
         raise InputError("worker count must be at least 1")
     return _pot(model, tables).run_md(cfg, vel, mc)
+
+
+# ---------------------------------------------------------------- exact path and rmse tooling
+@dataclass
+class RmseReport:
+    """RmseReport (rmse.hpp:15-19)."""
+    rmse_e: float = 0.0
+    rmse_f: float = 0.0
+    n_configs: int = 0
+
+
+@dataclass
+class SweepRow:
+    """SweepRow (rmse.hpp:24-28)."""
+    h: float = 0.0
+    rmse_e: float = 0.0
+    rmse_f: float = 0.0
+
+
+def _exact_pot(model: DPModel) -> DeepPot:
+    key = ("exact", id(model))
+    p = _pots.get(key)
+    if p is None or p.model is not model:
+        p = DeepPot(model, None)
+        _pots[key] = p
+    return p
+
+
+def compute_energy_forces_virial(cfg: AtomicConfig, model: DPModel, nlist=None) -> EvalResult:
+    """compute_energy_forces_virial (exact.cpp:155-173) on the GPU: full embedding nets."""
+    pot = _exact_pot(model)
+    cutoff = model.r_cut
+    if isinstance(nlist, NeighborList):
+        cutoff = nlist.cutoff
+    elif nlist is not None:
+        cutoff = float(nlist)
+    pot.set_skin(max(0.0, cutoff - model.r_cut))
+    return pot.compute_exact(cfg)
+
+
+def build_tables_gpu(model: DPModel, h: float) -> Tables:
+    """build_tables (table.cpp:77-162) evaluated on the GPU."""
+    return _exact_pot(model).build_tables_gpu(h, install=False)
+
+
+def rmse_compare(model: DPModel, tables: Tables, configs: Sequence[AtomicConfig],
+                 n_workers: int = 1) -> RmseReport:
+    """rmse_compare (rmse.cpp:48-59): tabulated vs exact energies / forces, both on the GPU."""
+    sde2 = sdf2 = 0.0
+    ncomp = 0
+    nat = 0
+    for cfg in configs:
+        ref = compute_energy_forces_virial(cfg, model)
+        tab = compute_energy_forces_virial_tabulated(cfg, model, tables, n_workers=n_workers)
+        de = ref.energy - tab.energy
+        sde2 += de * de
+        df = np.asarray(ref.forces).reshape(-1) - np.asarray(tab.forces).reshape(-1)
+        sdf2 += float(np.dot(df, df))
+        ncomp += df.size
+        nat = cfg.n_atoms
+    r = RmseReport(n_configs=len(configs))
+    if configs:
+        r.rmse_e = float(np.sqrt(sde2 / len(configs)) / nat)
+        r.rmse_f = float(np.sqrt(sdf2 / ncomp))
+    return r
+
+
+def rmse_sweep(model: DPModel, h_list: Sequence[float], configs: Sequence[AtomicConfig],
+               n_workers: int = 1) -> List[SweepRow]:
+    """rmse_sweep (rmse.cpp:63-97) on the GPU (a fresh handle; tables built per step on device)."""
+    pot = DeepPot(model, None)
+    try:
+        return pot.rmse_sweep(h_list, configs)
+    finally:
+        pot.close()
+
+
+def loglog_slope(rows: Sequence[SweepRow]) -> float:
+    """loglog_slope (rmse.cpp:99-116): least-squares slope of log(rmse_e) vs log(h)."""
+    sx = sy = sxx = sxy = 0.0
+    n = 0
+    for r in rows:
+        if not (r.h > 0.0) or not (r.rmse_e > 0.0):
+            continue
+        x, y = math.log(r.h), math.log(r.rmse_e)
+        sx += x
+        sy += y
+        sxx += x * x
+        sxy += x * y
+        n += 1
+    if n < 2:
+        return 0.0
+    return (n * sxy - sx * sy) / (n * sxx - sx * sx)

@@ -1,6 +1,8 @@
 // C-ABI of dp_b200 (include/dp_b200.h). Every entry point maps exceptions to the reference
 // CLI's exit codes (tools/dpmd.cpp:434-443): InputError -> 2, NumericalError -> 1.
+#include <cmath>
 #include <cstring>
+#include <vector>
 
 #include "engine.hpp"
 
@@ -69,6 +71,91 @@ int dp_compute(dp_handle* h, int64_t n, const double* pos, const int32_t* types,
     E.check_err();
     E.fetch_results(energy, forces, virial, atom_energy);
     E.read_counters();
+  });
+}
+
+int dp_set_embedding(dp_handle* h, const dp_embedding_desc* nets) {
+  if (!h) return DP_INPUT_ERROR;
+  return guard_call(&h->eng.last_error, [&] { h->eng.set_embedding(nets); });
+}
+
+int dp_compute_exact(dp_handle* h, int64_t n, const double* pos, const int32_t* types, const double box[9],
+                     const uint8_t pbc[3], double* energy, double* forces, double* virial,
+                     double* atom_energy) {
+  if (!h) return DP_INPUT_ERROR;
+  return guard_call(&h->eng.last_error, [&] {
+    dpb::Engine& E = h->eng;
+    if (!energy || !forces || !virial) throw InputErr("null output array");
+    E.set_config(n, pos, types, box, pbc);
+    E.build_list(E.r_cut + h->skin);
+    E.evaluate_exact();
+    E.check_err();
+    E.fetch_results(energy, forces, virial, atom_energy);
+  });
+}
+
+int dp_build_tables_gpu(dp_handle* h, double step, uint64_t* n_intervals, double* x_end, double* coeffs,
+                        int install) {
+  if (!h) return DP_INPUT_ERROR;
+  return guard_call(&h->eng.last_error,
+                    [&] { h->eng.build_tables_gpu(step, n_intervals, x_end, coeffs, install != 0); });
+}
+
+int dp_rmse_sweep(dp_handle* h, int n_configs, const int64_t* n_atoms, const double* pos, const int32_t* types,
+                  const double* boxes, const uint8_t* pbcs, int n_h, const double* h_list, double* rmse_e,
+                  double* rmse_f) {
+  if (!h) return DP_INPUT_ERROR;
+  return guard_call(&h->eng.last_error, [&] {
+    dpb::Engine& E = h->eng;
+    if (n_h < 1) throw InputErr("sweep needs at least one step size");   // rmse.cpp:65
+    if (n_configs < 0 || (n_configs > 0 && (!n_atoms || !pos || !types || !boxes || !pbcs)))
+      throw InputErr("null configuration arrays");
+    // reference energies / forces once per configuration (rmse.cpp:67-75)
+    std::vector<double> ref_e(n_configs);
+    std::vector<std::vector<double>> ref_f(n_configs);
+    std::vector<double> vir(9);
+    int64_t at = 0;
+    for (int c = 0; c < n_configs; ++c) {
+      const int64_t na = n_atoms[c];
+      ref_f[c].resize(3 * na);
+      E.set_config(na, pos + 3 * at, types + at, boxes + 9 * c, pbcs + 3 * c);
+      E.build_list(E.r_cut);
+      E.evaluate_exact();
+      E.check_err();
+      E.fetch_results(&ref_e[c], ref_f[c].data(), vir.data(), nullptr);
+      at += na;
+    }
+    std::vector<double> f(0);
+    for (int k = 0; k < n_h; ++k) {
+      E.build_tables_gpu(h_list[k], nullptr, nullptr, nullptr, true);
+      // Accum (rmse.cpp:11-37)
+      double sde2 = 0.0, sdf2 = 0.0;
+      int64_t ncomp = 0, natoms_last = 0;
+      at = 0;
+      for (int c = 0; c < n_configs; ++c) {
+        const int64_t na = n_atoms[c];
+        f.resize(3 * na);
+        double e = 0.0;
+        E.set_config(na, pos + 3 * at, types + at, boxes + 9 * c, pbcs + 3 * c);
+        E.build_list(E.r_cut);
+        E.reset_counters();
+        E.evaluate();
+        E.check_err();
+        E.fetch_results(&e, f.data(), vir.data(), nullptr);
+        E.read_counters();
+        const double de = ref_e[c] - e;
+        sde2 += de * de;
+        for (int64_t q = 0; q < 3 * na; ++q) {
+          const double df = ref_f[c][q] - f[q];
+          sdf2 += df * df;
+        }
+        ncomp += 3 * na;
+        natoms_last = na;
+        at += na;
+      }
+      rmse_e[k] = n_configs ? std::sqrt(sde2 / n_configs) / static_cast<double>(natoms_last) : 0.0;
+      rmse_f[k] = n_configs ? std::sqrt(sdf2 / static_cast<double>(ncomp)) : 0.0;
+    }
   });
 }
 

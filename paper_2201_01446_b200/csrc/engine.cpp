@@ -34,6 +34,7 @@ void raise_device_error(int code) {
     case DEV_SHIFT_RANGE: throw InputErr("image shift outside +-511 cells (positions too far from the box)");
     case DEV_ROW_CAP: throw NumErr("neighbour row exceeds the kernel capacity");
     case DEV_PBUF: throw NumErr("tabulate group buffer overflow (retry: it grows at the next rebuild)");
+    case DEV_TABLE_VERIFY: throw NumErr("table verification failed at a node");
     case DEV_STALE: throw NumErr("neighbor list stale: an atom moved more than half the buffer since the last rebuild");
     default: throw CudaErr("unknown device error " + std::to_string(code));
   }
@@ -41,16 +42,42 @@ void raise_device_error(int code) {
 
 } // namespace
 
+void Engine::upload_tables(const dp_table_desc& tdr) {
+  const dp_table_desc* td = &tdr;
+  // tables -> [type][interval][6][Mp]
+  tab_x0 = td->x0;
+  tab_h = td->h;
+  tab_n = td->n;
+  const int B = td->block;
+  const int nb = (td->m + B - 1) / B;
+  const size_t src_stride = static_cast<size_t>(nb) * 6 * B;
+  const size_t dst_stride = static_cast<size_t>(6) * Mp;
+  std::vector<double> tbuf(static_cast<size_t>(n_types) * tab_n * dst_stride, 0.0);
+  for (int t = 0; t < n_types; ++t)
+    for (uint64_t th = 0; th < tab_n; ++th) {
+      const double* src = td->coeffs[t] + th * src_stride;
+      double* dst = tbuf.data() + (static_cast<size_t>(t) * tab_n + th) * dst_stride;
+      for (int p = 0; p < M; ++p)
+        for (int m = 0; m < 6; ++m)
+          dst[m * Mp + p] = src[static_cast<size_t>(p / B) * 6 * B + m * B + (p % B)];
+    }
+  tab.ensure(tbuf.size());
+  DPB_CUDA(cudaMemcpy(tab.p, tbuf.data(), tbuf.size() * sizeof(double), cudaMemcpyHostToDevice));
+  tab_block = B;
+  pbuf_cap = 0;
+}
+
 void Engine::create(const dp_model_desc* md, const dp_table_desc* td, int dev, int prec) {
-  if (!md || !td) throw InputErr("null model or table descriptor");
+  // td may be NULL: tables are then built on the device (dp_build_tables_gpu) before use
+  if (!md) throw InputErr("null model descriptor");
   if (md->n_types < 1 || md->n_types > 63) throw InputErr("model needs 1..63 species");
   if (!(md->r_cut > 0.0) || !(md->r_smooth >= 0.0) || !(md->r_smooth < md->r_cut))
     throw InputErr("model cutoffs must satisfy 0 <= r_smooth < r_cut");
   if (md->d1 < 1) throw InputErr("embedding width must be positive");
   if (md->m_lt < 1 || md->m_lt > 4 * md->d1) throw InputErr("m_lt must lie in [1, 4*d1]");
-  if (td->n_tables != md->n_types) throw InputErr("need one table per neighbor type");
-  if (td->m != 4 * md->d1) throw InputErr("table feature width does not match 4*d1");
-  if (td->block < 1 || td->n < 1 || !(td->h > 0.0)) throw InputErr("table header is inconsistent");
+  if (td && td->n_tables != md->n_types) throw InputErr("need one table per neighbor type");
+  if (td && td->m != 4 * md->d1) throw InputErr("table feature width does not match 4*d1");
+  if (td && (td->block < 1 || td->n < 1 || !(td->h > 0.0))) throw InputErr("table header is inconsistent");
   if (prec != 0 && prec != 1) throw InputErr("precision must be 0 (fp64) or 1 (mixed)");
   precision = prec;
   device = dev;
@@ -95,25 +122,7 @@ void Engine::create(const dp_model_desc* md, const dp_table_desc* td, int dev, i
     fl.shortcut = fl.in == fl.out;
     widthp_max = std::max(widthp_max, fl.outp);
   }
-  // tables -> [type][interval][6][Mp]
-  tab_x0 = td->x0;
-  tab_h = td->h;
-  tab_n = td->n;
-  const int B = td->block;
-  const int nb = (td->m + B - 1) / B;
-  const size_t src_stride = static_cast<size_t>(nb) * 6 * B;
-  const size_t dst_stride = static_cast<size_t>(6) * Mp;
-  std::vector<double> tbuf(static_cast<size_t>(n_types) * tab_n * dst_stride, 0.0);
-  for (int t = 0; t < n_types; ++t)
-    for (uint64_t th = 0; th < tab_n; ++th) {
-      const double* src = td->coeffs[t] + th * src_stride;
-      double* dst = tbuf.data() + (static_cast<size_t>(t) * tab_n + th) * dst_stride;
-      for (int p = 0; p < M; ++p)
-        for (int m = 0; m < 6; ++m)
-          dst[m * Mp + p] = src[static_cast<size_t>(p / B) * 6 * B + m * B + (p % B)];
-    }
-  tab.ensure(tbuf.size());
-  DPB_CUDA(cudaMemcpy(tab.p, tbuf.data(), tbuf.size() * sizeof(double), cudaMemcpyHostToDevice));
+  if (td) upload_tables(*td);
   // fitting weights, zero padded
   fit_wt.resize(n_types * L);
   fit_w.resize(n_types * L);
@@ -155,6 +164,7 @@ void Engine::create(const dp_model_desc* md, const dp_table_desc* td, int dev, i
   DPB_CUDA(cudaMemcpy(d_max_nbr.p, max_nbr.data(), n_types * sizeof(int), cudaMemcpyHostToDevice));
   err.ensure(1);
   counters.ensure(3);
+  exact_ctr.ensure(3);
   red.ensure(256 * 10 + 64);
   DPB_CUDA(cudaMemset(err.p, 0, sizeof(int)));
   DPB_CUDA(cudaMemset(counters.p, 0, 3 * sizeof(unsigned long long)));
@@ -329,6 +339,7 @@ void Engine::build_list(double cutoff) {
 
 void Engine::evaluate() {
   if (!list_valid) throw InputErr("no neighbour list");
+  if (tab_n == 0) throw InputErr("no compression tables: pass them to dp_create or build them with dp_build_tables_gpu");
   phase_begin(1);
   launch_tab_fwd();
   phase_begin(2);

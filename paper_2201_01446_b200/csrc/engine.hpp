@@ -53,6 +53,11 @@ struct FitLayer {
   bool shortcut = false;
 };
 
+// Device pointers of one embedding net (model.hpp:14-20) inside Engine::emb_w.
+struct EmbPtrs {
+  const double *w0, *b0, *w1, *b1, *w2, *b2;
+};
+
 struct Engine {
   // ---- model (immutable after create) ----
   int precision = 0;
@@ -67,7 +72,14 @@ struct Engine {
   // tables, device layout [type][interval][6][Mp]
   double tab_x0 = 0, tab_h = 0;
   uint64_t tab_n = 0;
+  int tab_block = 16;
   DevBuf<double> tab;
+  // embedding nets (exact path, GPU table build), optional: dp_set_embedding
+  bool has_embedding = false;
+  DevBuf<double> emb_w;
+  DevBuf<EmbPtrs> emb_ptrs;
+  std::vector<EmbPtrs> emb_ptrs_host;
+  DevBuf<unsigned long long> exact_ctr;
   DevBuf<float> tab32; // mixed mode copy
   // fitting weights per type and layer: wt = W^T [outp][inp], w = W [inp][outp]
   std::vector<DevBuf<double>> fit_wt, fit_w, fit_b;
@@ -188,6 +200,11 @@ struct Engine {
   void launch_tab_fwd();
   void launch_fitting();
   void launch_fitting_mixed();
+  void set_embedding(const dp_embedding_desc* nets);
+  void upload_tables(const dp_table_desc& td);
+  void evaluate_exact();
+  void launch_env_exact();
+  void build_tables_gpu(double step, uint64_t* n_out, double* x_end_out, double* coeffs_out, bool install);
   void ensure_mixed_buffers();
   void prepare_mixed();
   // mixed precision (tcgen05 3xTF32) buffers

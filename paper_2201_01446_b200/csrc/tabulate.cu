@@ -26,191 +26,11 @@
 // All reductions have a fixed order, so results are bitwise reproducible run to run.
 #include <cub/cub.cuh>
 
-#include "engine.hpp"
+#include "tab_common.cuh"
 
 namespace dpb {
 
 namespace {
-
-struct TabParams {
-  const double4* pos;
-  const int64_t* row_off;
-  const uint64_t* keys;
-  const int32_t* eown;  // [E] centre of each list entry
-  const uint8_t* center; // [n] 1 = evaluated centre, 0 = ghost
-  int32_t* ebin;        // [E] global bin t*tn + interval of a real entry, -1 otherwise
-  double* erc;          // [5][E] SoA: R0..R3, u of real entries
-  int32_t* egrp;        // [E] group index of a real entry inside its centre
-  uint64_t* skeys;      // [E] per row: reals sorted by bin, (bin << 32 | entry)
-  int32_t* n_real;      // [n]
-  int32_t* n_grp;       // [n+1] groups per centre -> (scanned) offsets into Pbuf
-  const int64_t* goff;  // [n+1] exclusive scan of n_grp
-  double* Pbuf;         // [sum groups][24]
-  int64_t pcap;         // groups Pbuf can hold
-  const double* tab;    // [type][interval][6][Mp]
-  const int* max_nbr;
-  DevCell c;
-  double rc2, rs, rc;
-  double x0, h, x_end;
-  int tn;
-  int n, n_types, M, Mp, mlt, K0p;
-  int64_t E;
-  const int32_t* slot_of;
-  double* T;            // [n][4][Mp]
-  double* D;            // [slots][K0p] (FP64 mode)
-  float* D2;            // [slots][2*K0p] mixed mode: tf32 split (hi | lo) of D, the tcgen05 operand
-  const double* dD;
-  double* g;            // [E][3]
-  unsigned long long* counters;
-  int* err;
-  int scap;
-};
-
-__device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
-
-__device__ __forceinline__ double node_x(double x0, double h, int th) {
-  return __dadd_rn(x0, __dmul_rn(static_cast<double>(th), h));
-}
-
-// locate (table.cpp:20-32): floor, then nudge so node(th) <= x < node(th+1) in the exact
-// arithmetic of the nodes; clamp past the end and flag extrapolation.
-__device__ __forceinline__ int locate(const TabParams& p, double x, bool& ext, int* err) {
-  if (!(x >= p.x0)) {
-    raise_err(err, DEV_TABLE_LOW);
-    ext = false;
-    return 0;
-  }
-  const double tf = floor(__ddiv_rn(__dsub_rn(x, p.x0), p.h));
-  if (!(tf < static_cast<double>(p.tn) + 2.0)) {  // far past the end (or inf): clamp directly
-    ext = true;
-    return p.tn - 1;
-  }
-  int th = static_cast<int>(tf);
-  while (node_x(p.x0, p.h, th + 1) <= x) ++th;
-  while (th > 0 && node_x(p.x0, p.h, th) > x) --th;
-  ext = false;
-  if (th >= p.tn) {
-    th = p.tn - 1;
-    ext = x > p.x_end;
-  }
-  return th;
-}
-
-__device__ __forceinline__ double switch_fn(double r, double rs, double rc) {
-  if (r >= rc) return 0.0;
-  if (r <= rs) return 1.0;
-  const double u = (r - rs) / (rc - rs);
-  const double uu = u * u;
-  return fmax(0.0, uu * u * (-6.0 * uu + 15.0 * u - 10.0) + 1.0);
-}
-
-__device__ __forceinline__ double switch_deriv(double r, double rs, double rc) {
-  if (r >= rc || r <= rs) return 0.0;
-  const double inv = 1.0 / (rc - rs);
-  const double u = (r - rs) * inv;
-  const double um1 = u - 1.0;
-  return -30.0 * u * u * um1 * um1 * inv;
-}
-
-// Environment of one real neighbour (env_mat.cpp:29-71).
-struct Env {
-  double d[3], r, ir, s, sd, u[3];
-};
-
-__device__ __forceinline__ void env_of(const TabParams& p, double3 ri, uint64_t key, Env& e) {
-  int sh[3];
-  key_shift(key, sh);
-  disp_exact(p.c, ri, ld_pos(p.pos, key_j(key)), sh[0], sh[1], sh[2], e.d);
-  const double r2 = norm2_exact(e.d);
-  e.r = sqrt(r2);
-  const double w = switch_fn(e.r, p.rs, p.rc);
-  e.ir = 1.0 / e.r;
-  e.s = w * e.ir;
-  e.sd = switch_deriv(e.r, p.rs, p.rc) * e.ir - w * e.ir * e.ir;
-#pragma unroll
-  for (int x = 0; x < 3; ++x) e.u[x] = e.d[x] * e.ir;
-}
-
-__device__ __forceinline__ int warp_min(int v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-__device__ __forceinline__ int warp_max(int v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-
-// Exclusive warp scan of non-negative ints.
-__device__ __forceinline__ int warp_excl_scan(int v, int lane, int* total) {
-  int x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  *total = __shfl_sync(0xffffffffu, x, 31);
-  return x - v;
-}
-
-// Reduce-scatter of 24 per-lane partials: afterwards every lane holds the full warp sums of
-// entries base..base+2 with base = 12*b4 + 6*b3 + 3*b2 (b = lane bits). Deterministic.
-__device__ __forceinline__ int rs24(double* v, int lane) {
-  {
-    const bool hi = lane & 16;
-#pragma unroll
-    for (int i = 0; i < 12; ++i) {
-      const double send = hi ? v[i] : v[i + 12];
-      const double keep = hi ? v[i + 12] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
-  }
-  {
-    const bool hi = lane & 8;
-#pragma unroll
-    for (int i = 0; i < 6; ++i) {
-      const double send = hi ? v[i] : v[i + 6];
-      const double keep = hi ? v[i + 6] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-  }
-  {
-    const bool hi = lane & 4;
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      const double send = hi ? v[i] : v[i + 3];
-      const double keep = hi ? v[i + 3] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    v[i] += __shfl_xor_sync(0xffffffffu, v[i], 2);
-    v[i] += __shfl_xor_sync(0xffffffffu, v[i], 1);
-  }
-  return ((lane >> 4) & 1) * 12 + ((lane >> 3) & 1) * 6 + ((lane >> 2) & 1) * 3;
-}
-
-// Reduce-scatter of 32 per-lane partials: afterwards lane l holds the warp sum of entry l.
-__device__ __forceinline__ double rs32(double* v, int lane) {
-#pragma unroll
-  for (int lvl = 16; lvl >= 1; lvl >>= 1) {
-    const bool hi = lane & lvl;
-#pragma unroll
-    for (int i = 0; i < lvl; ++i) {
-      const double send = hi ? v[i] : v[i + lvl];
-      const double keep = hi ? v[i + lvl] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, lvl);
-    }
-  }
-  return v[0];
-}
-
 
 // ---------------------------------------------------------------- k_env_fwd (thread per entry)
 __global__ void __launch_bounds__(256) k_env_fwd(TabParams p) {
@@ -228,6 +48,16 @@ __global__ void __launch_bounds__(256) k_env_fwd(TabParams p) {
     int bin = -1;
     if (r2 < 1e-12) {
       raise_err(p.err, DEV_OVERLAP); // env_mat.cpp:33 throws before any table lookup
+    } else if (r2 < p.rc2 && p.tn == 0) {
+      // exact path: no table; the real entry is tagged with its neighbour type
+      const double r = sqrt(r2);
+      const double ir = 1.0 / r;
+      const double s = switch_fn(r, p.rs, p.rc) * ir;
+      bin = key_type(key);
+      p.erc[e] = s;
+      p.erc[p.E + e] = s * (d[0] * ir);
+      p.erc[2 * p.E + e] = s * (d[1] * ir);
+      p.erc[3 * p.E + e] = s * (d[2] * ir);
     } else if (r2 < p.rc2) {
       const double r = sqrt(r2);
       const double ir = 1.0 / r;
@@ -774,53 +604,6 @@ __global__ void __launch_bounds__(256) k_tab_bwd_g(TabParams p) {
 }
 
 // ---------------------------------------------------------------- host side
-TabParams make_params(Engine& E) {
-  TabParams p{};
-  p.pos = E.pos4.p;
-  p.row_off = E.row_off.p;
-  p.keys = E.keys.p;
-  p.eown = E.eown.p;
-  p.center = E.center.p;
-  p.ebin = E.ebin.p;
-  p.erc = E.erc.p;
-  p.egrp = E.egrp.p;
-  p.skeys = E.skeys.p;
-  p.n_real = E.n_real.p;
-  p.n_grp = E.n_grp.p;
-  p.goff = E.goff.p;
-  p.Pbuf = E.Pbuf.p;
-  p.pcap = E.pbuf_cap;
-  p.tab = E.tab.p;
-  p.max_nbr = E.d_max_nbr.p;
-  p.c = E.cell;
-  p.rc2 = E.r_cut * E.r_cut;
-  p.rs = E.r_smooth;
-  p.rc = E.r_cut;
-  p.x0 = E.tab_x0;
-  p.h = E.tab_h;
-  p.x_end = E.tab_x0 + E.tab_h * static_cast<double>(E.tab_n);
-  p.tn = static_cast<int>(E.tab_n);
-  p.n = static_cast<int>(E.n);
-  p.n_types = E.n_types;
-  p.M = E.M;
-  p.Mp = E.Mp;
-  p.mlt = E.mlt;
-  p.K0p = E.K0p;
-  p.E = E.n_entries;
-  p.slot_of = E.slot_of.p;
-  p.T = E.T.p;
-  p.D = E.precision == 1 ? nullptr : E.D.p;
-  p.D2 = E.precision == 1 ? E.tc_d2.p : nullptr;
-  p.dD = E.dD.p;
-  p.g = E.g.p;
-  p.counters = E.counters.p;
-  p.err = E.err.p;
-  int scap = 32;
-  while (scap < E.max_row) scap <<= 1;
-  p.scap = scap;
-  return p;
-}
-
 int sm_count(int dev) {
   int s = 0;
   cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
@@ -883,6 +666,16 @@ void Engine::launch_tab_fwd() {
   if (pbuf_cap == 0 || !md_active) { // single evaluations size it exactly (they sync anyway)
     DPB_CUDA(cudaStreamSynchronize(stream));
     grow_pbuf();
+  }
+}
+
+void Engine::launch_env_exact() {
+  TabParams p = make_params(*this);
+  p.tn = 0;
+  p.counters = exact_ctr.p;
+  if (p.E > 0) {
+    k_env_fwd<<<ceil_div(p.E, 256), 256, 0, stream>>>(p);
+    ++launches;
   }
 }
 

@@ -235,3 +235,54 @@ def normwise(a: np.ndarray, b: np.ndarray) -> float:
     b = np.asarray(b, dtype=np.float64)
     scale = max(float(np.max(np.abs(b))), 1e-300)
     return float(np.max(np.abs(a - b))) / scale
+
+
+def ref_compute_exact(cfg: dp.AtomicConfig, model: dp.DPModel) -> dp.EvalResult:
+    """compute_energy_forces_virial (exact.cpp:155-173) of the compiled reference."""
+    n = cfg.n_atoms
+    e = C.c_double()
+    f = np.empty((n, 3))
+    v = np.empty(9)
+    ae = np.empty(n)
+    _chk(ref().ref_compute_exact(C.byref(model.shape._c()), _dp(model.blob), n, _dp(cfg.pos), _ip(cfg.type),
+                                 _dp(cfg.h), _u8(cfg.periodic), C.byref(e), _dp(f), _dp(v), _dp(ae)),
+         ref(), "ref_last_error")
+    return dp.EvalResult(e.value, ae, f, v)
+
+
+def ref_rmse_sweep(model: dp.DPModel, h_list, configs):
+    """rmse_sweep + loglog_slope (rmse.cpp:63-116) of the compiled reference."""
+    L = ref()
+    D, I64 = C.POINTER(C.c_double), C.c_int64
+    L.ref_rmse_sweep.argtypes = [C.POINTER(dp._Preset), D, C.c_int, C.POINTER(I64), D, C.POINTER(C.c_int32), D,
+                                 C.POINTER(C.c_uint8), C.c_int, D, D, D, D]
+    na = np.array([c.n_atoms for c in configs], dtype=np.int64)
+    pos = np.ascontiguousarray(np.concatenate([c.pos.reshape(-1) for c in configs]))
+    typ = np.ascontiguousarray(np.concatenate([c.type for c in configs]).astype(np.int32))
+    box = np.ascontiguousarray(np.concatenate([c.h.reshape(-1) for c in configs]))
+    pbc = np.ascontiguousarray(np.concatenate([c.periodic for c in configs]).astype(np.uint8))
+    hl = np.ascontiguousarray(h_list, dtype=np.float64)
+    re, rf, sl = np.empty(len(hl)), np.empty(len(hl)), np.empty(1)
+    _chk(L.ref_rmse_sweep(C.byref(model.shape._c()), _dp(model.blob), len(configs),
+                          na.ctypes.data_as(C.POINTER(I64)), _dp(pos), _ip(typ), _dp(box), _u8(pbc), len(hl),
+                          _dp(hl), _dp(re), _dp(rf), _dp(sl)), L, "ref_last_error")
+    return re, rf, float(sl[0])
+
+
+def ref_write_model(path: str, model: dp.DPModel, preset: str, seed: int) -> None:
+    L = ref()
+    L.ref_write_model.argtypes = [C.c_char_p, C.POINTER(dp._Preset), C.POINTER(C.c_double), C.c_char_p,
+                                  C.c_uint64]
+    _chk(L.ref_write_model(path.encode(), C.byref(model.shape._c()), _dp(model.blob), preset.encode(), seed),
+         L, "ref_last_error")
+
+
+def ref_read_model(path: str, model_like: dp.DPModel):
+    L = ref()
+    L.ref_read_model.argtypes = [C.c_char_p, C.POINTER(dp._Preset), C.POINTER(C.c_double),
+                                 C.POINTER(C.c_uint64)]
+    blob = np.empty_like(model_like.blob)
+    seed = C.c_uint64()
+    _chk(L.ref_read_model(path.encode(), C.byref(model_like.shape._c()), _dp(blob), C.byref(seed)), L,
+         "ref_last_error")
+    return blob, seed.value
