@@ -253,6 +253,15 @@ int dp_read_tables_header(const char* path, int* n_tables, int* m, int* block, u
                           double* x0, double* h);
 int dp_read_tables(const char* path, double* coeffs /* n_tables * n * stride */);
 
+/* JSON model files, write_model / read_model (model_io.cpp:226-283). species_csv: comma-separated
+ * species names (NULL: "A", "B", ...). The reader fills the shape first; call it again with a blob
+ * of dp_model_blob_size(shape) doubles to get the weights. Non-uniform fitting widths are
+ * rejected (the blob layout has one width). Errors: DP_INPUT_ERROR as the reference's InputError. */
+int dp_write_model_json(const char* path, const dp_preset* shape, const double* blob, const char* species_csv,
+                        const char* preset, uint64_t seed);
+int dp_read_model_json(const char* path, dp_preset* shape, double* blob, int64_t blob_cap, char* species_csv,
+                       int species_cap, char* preset, int preset_cap, uint64_t* seed);
+
 /* TanhTable (tanh_table.cpp:5-21) coefficients, 3 * 8193 doubles; mixed-precision mode only. */
 int dp_tanh_table(double* coef);
 

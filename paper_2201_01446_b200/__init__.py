@@ -162,6 +162,9 @@ def _lib():
         "dp_read_tables": ([C.c_char_p, D], I),
         "dp_tanh_table": ([D], I),
         "dp_set_embedding": ([P, C.POINTER(_EmbDesc)], I),
+        "dp_write_model_json": ([C.c_char_p, C.POINTER(_Preset), D, C.c_char_p, C.c_char_p, U64], I),
+        "dp_read_model_json": ([C.c_char_p, C.POINTER(_Preset), D, I64, C.c_char_p, I, C.c_char_p, I,
+                                C.POINTER(U64)], I),
         "dp_compute_exact": ([P, I64, D, I32P, D, U8P, D, D, D, D], I),
         "dp_build_tables_gpu": ([P, C.c_double, C.POINTER(U64), D, D, I], I),
         "dp_rmse_sweep": ([P, I, C.POINTER(I64), D, I32P, D, U8P, I, D, D, D], I),
@@ -362,6 +365,39 @@ def make_test_model(n_types: int, d1: int, m_lt: int, fit_width: int, n_hidden: 
     blob = np.empty(_blob_size(p), dtype=np.float64)
     _check(_lib().dp_gen_test_model(C.byref(p._c()), seed, fit_scale, _dp(blob)))
     return DPModel(p, blob)
+
+
+@dataclass
+class ModelFile:
+    """ModelFile (model_io.hpp:52-56)."""
+    model: "DPModel"
+    preset: str = ""
+    seed: int = 0
+    species: List[str] = field(default_factory=list)
+
+
+def write_model(path: str, model: DPModel, preset: str = "", seed: int = 0,
+                species: Optional[Sequence[str]] = None) -> None:
+    """write_model (model_io.cpp:226-250): JSON, shortest round-trip doubles."""
+    csv = ",".join(species) if species else None
+    _check(_lib().dp_write_model_json(path.encode(), C.byref(model.shape._c()), _dp(model.blob),
+                                      csv.encode() if csv else None, preset.encode(), seed))
+
+
+def read_model(path: str) -> ModelFile:
+    """read_model (model_io.cpp:252-283): InputError on unreadable / malformed / inconsistent files."""
+    shp = _Preset()
+    sp = C.create_string_buffer(512)
+    pr = C.create_string_buffer(256)
+    sd = C.c_uint64()
+    _check(_lib().dp_read_model_json(path.encode(), C.byref(shp), None, 0, sp, 512, pr, 256, C.byref(sd)))
+    p = Preset(pr.value.decode(), shp.n_types, [shp.masses[t] for t in range(shp.n_types)],
+               [shp.max_nbr[t] for t in range(shp.n_types)], shp.r_cut, shp.r_smooth, shp.d1, shp.m_lt,
+               shp.fit_width, shp.fit_hidden)
+    blob = np.empty(_blob_size(p), dtype=np.float64)
+    _check(_lib().dp_read_model_json(path.encode(), C.byref(shp), _dp(blob), blob.size, sp, 512, pr, 256,
+                                     C.byref(sd)))
+    return ModelFile(DPModel(p, blob), pr.value.decode(), int(sd.value), sp.value.decode().split(","))
 
 
 # ---------------------------------------------------------------- tables
