@@ -14,6 +14,9 @@
 //   reverse halo   ghost force partials -> owners, accumulated in peer order (deterministic)
 // At a rebuild every rank all-gathers the owned (id, x, v), repartitions identically and
 // rebuilds its local system. No collective touches the data path except these exchanges.
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <nccl.h>
 
 #include <algorithm>
@@ -232,9 +235,16 @@ void make_plan(const Dist& D, int r, Plan& P) {
 
 // Build the local system for this rank from the global state and upload it.
 void build_local(Engine& E) {
+  static const bool trace = std::getenv("DPB_TRACE") != nullptr;
+  auto now = [&] {
+    if (trace) cudaStreamSynchronize(E.stream);
+    return std::chrono::steady_clock::now();
+  };
+  const auto t0 = now();
   Dist& D = *E.dist;
   Plan P;
   make_plan(D, D.rank, P);
+  const auto t1 = now();
   D.lgid.swap(P.lgid);
   D.lcenter.swap(P.lcenter);
   D.soff = P.soff;
@@ -262,9 +272,18 @@ void build_local(Engine& E) {
     }
     lt[k] = D.gtypes[j];
   }
+  const auto t2 = now();
   E.set_config(nl, lp.data(), lt.data(), D.box, D.pbc, D.lcenter.data());
+  const auto t3 = now();
   E.md_upload_atoms(lv.data());
+  const auto t4 = now();
   E.build_list(E.r_cut + E.md.buffer);
+  const auto t5 = now();
+  if (trace) {
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "[dpb rank %d] local: plan %.2f, arrays %.2f, set_config %.2f, upload %.2f, list %.2f ms\n",
+                 D.rank, ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4), ms(t4, t5));
+  }
 }
 
 void exchange(Engine& E, const std::vector<int64_t>& out_off, const std::vector<int64_t>& in_off) {
@@ -389,8 +408,20 @@ static void gather_global(Engine& E) {
 }
 
 void dist_rebuild(Engine& E) {
+  static const bool trace = std::getenv("DPB_TRACE") != nullptr;
+  auto now = [&] {
+    if (trace) cudaStreamSynchronize(E.stream);
+    return std::chrono::steady_clock::now();
+  };
+  const auto t0 = now();
   gather_global(E);
+  const auto t1 = now();
   build_local(E);
+  const auto t2 = now();
+  if (trace)
+    std::fprintf(stderr, "[dpb rank %d] rebuild: gather %.2f ms, local %.2f ms\n", E.dist->rank,
+                 std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                 std::chrono::duration<double, std::milli>(t2 - t1).count());
 }
 
 void dist_md_end(Engine& E, double* gpos, double* gvel) {

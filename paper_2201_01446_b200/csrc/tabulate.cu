@@ -24,6 +24,10 @@
 //   k_tab_bwd_P  one warp per centre: dT from dD, interval projections P per group
 //   k_tab_bwd_g  one thread per list entry: dE_i/dd_ij from P, written at the entry   [parallel]
 // All reductions have a fixed order, so results are bitwise reproducible run to run.
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include <cub/cub.cuh>
 
 #include "tab_common.cuh"
@@ -664,8 +668,18 @@ void Engine::launch_tab_fwd() {
   if (!h_gtotal) DPB_CUDA(cudaMallocHost(&h_gtotal, sizeof(int64_t)));
   DPB_CUDA(cudaMemcpyAsync(h_gtotal, goff.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
   if (pbuf_cap == 0 || !md_active) { // single evaluations size it exactly (they sync anyway)
+    static const bool trace = std::getenv("DPB_TRACE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     DPB_CUDA(cudaStreamSynchronize(stream));
+    const auto t1 = std::chrono::steady_clock::now();
     grow_pbuf();
+    if (trace) {
+      DPB_CUDA(cudaStreamSynchronize(stream));
+      const auto t2 = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[dpb] pbuf sizing: wait %.2f ms, grow %.2f ms (cap %lld)\n",
+                   std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                   std::chrono::duration<double, std::milli>(t2 - t1).count(), static_cast<long long>(pbuf_cap));
+    }
   }
 }
 
