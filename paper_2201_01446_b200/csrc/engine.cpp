@@ -200,6 +200,7 @@ void Engine::destroy() {
     for (auto& b : *v) b.release();
   tc_tanh.release(); tc_d2.release(); tc_y2a.release(); tc_y2b.release(); tc_dz2a.release();
   tc_dz2b.release(); tc_dya.release(); tc_dyb.release();
+  dTbuf.release(); fb_list.release(); emb_w.release(); emb_ptrs.release(); exact_ctr.release();
   if (stream) cudaStreamDestroy(stream);
   stream = nullptr;
 }

@@ -80,6 +80,8 @@ struct Engine {
   DevBuf<EmbPtrs> emb_ptrs;
   std::vector<EmbPtrs> emb_ptrs_host;
   DevBuf<unsigned long long> exact_ctr;
+  DevBuf<double> dTbuf;  // [n][4][Mp] adjoint of T (tabulate backward)
+  DevBuf<int> fb_list;   // atom blocks left to the per-warp projection kernel (+ count)
   DevBuf<float> tab32; // mixed mode copy
   // fitting weights per type and layer: wt = W^T [outp][inp], w = W [inp][outp]
   std::vector<DevBuf<double>> fit_wt, fit_w, fit_b;

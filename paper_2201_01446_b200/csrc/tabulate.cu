@@ -31,6 +31,7 @@
 #include <cub/cub.cuh>
 
 #include "tab_common.cuh"
+#include "tc_common.cuh"
 
 namespace dpb {
 
@@ -429,28 +430,42 @@ __global__ void __launch_bounds__(64, 8) k_tab_fwd(TabParams p) {
   }
 }
 
-// ---------------------------------------------------------------- k_tab_bwd_P (warp per centre)
+// Reduce-scatter of 16 per-lane partials: afterwards lane l holds the warp sum of entry l & 15.
+__device__ __forceinline__ double rs16(double* v, int lane) {
+#pragma unroll
+  for (int lvl = 8; lvl >= 1; lvl >>= 1) {
+    const bool hi = lane & lvl;
+#pragma unroll
+    for (int i = 0; i < lvl; ++i) {
+      const double send = hi ? v[i] : v[i + lvl];
+      const double keep = hi ? v[i + lvl] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, lvl);
+    }
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
+}
+
+// ---------------------------------------------------------------- k_tab_dT (warp per centre)
+// dT = adjoint of D = T<^T T (contract.hpp:21-38): dT[a][p] = sum_{q<mlt} dD[q][p] T[a][q]
+// + [p < mlt] sum_r dD[p][r] T[a][r]. Written to dTg[i][4][Mp] for the projection kernels.
 template <int F>
-__global__ void __launch_bounds__(64, 6) k_tab_bwd_P(TabParams p) {
+__global__ void __launch_bounds__(256, 2) k_tab_dT(TabParams p, double* __restrict__ dTg) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
   const int wpb = blockDim.x >> 5;
   double* ts = reinterpret_cast<double*>(smem) + wid * (4 * p.Mp + 4 * p.mlt);
   double* S = ts + 4 * p.Mp;
-  const size_t istride = static_cast<size_t>(6) * p.Mp;
   const int f0 = F * lane;
   for (int i = blockIdx.x * wpb + wid; i < p.n; i += gridDim.x * wpb) {
-    const int64_t off = p.row_off[i];
-    const int nreal = p.n_real[i];
-    int G = p.n_grp[i];
-    if (p.goff[i] + G > p.pcap) {
-      if (lane == 0) raise_err(p.err, DEV_PBUF);
-      G = 0;
+    double* out = dTg + static_cast<size_t>(i) * 4 * p.Mp;
+    if (!p.center[i]) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int q = 0; q < F; ++q) out[a * p.Mp + f0 + q] = 0.0;
+      continue;
     }
-    const uint64_t* sk = p.skeys + off;
-    double* Pout = p.Pbuf + p.goff[i] * 24;
-    // --- dT = adjoint of D = T<^T T (contract.hpp:21-38) ---
     const double* Ti = p.T + static_cast<size_t>(i) * 4 * p.Mp;
     double tv[4][F], dT[4][F];
 #pragma unroll
@@ -465,12 +480,12 @@ __global__ void __launch_bounds__(64, 6) k_tab_bwd_P(TabParams p) {
     const int slot = p.slot_of[i];
     const double* dDrow = p.dD + static_cast<size_t>(slot < 0 ? 0 : slot) * p.K0p;
     const bool fon = f0 < p.M && slot >= 0;
-    for (int q0 = 0; q0 < p.mlt; q0 += 8) {
-      double part[32];
+    for (int q0 = 0; q0 < p.mlt; q0 += 4) {
+      double part[16];
 #pragma unroll
-      for (int k = 0; k < 32; ++k) part[k] = 0.0;
+      for (int k = 0; k < 16; ++k) part[k] = 0.0;
 #pragma unroll
-      for (int ql = 0; ql < 8; ++ql) {
+      for (int ql = 0; ql < 4; ++ql) {
         const int qq = q0 + ql;
         if (qq < p.mlt) {
           double dq[F];
@@ -487,8 +502,8 @@ __global__ void __launch_bounds__(64, 6) k_tab_bwd_P(TabParams p) {
           }
         }
       }
-      const double s = rs32(part, lane);
-      if (q0 + (lane >> 2) < p.mlt) S[(q0 + (lane >> 2)) * 4 + (lane & 3)] = s;
+      const double s = rs16(part, lane);
+      if (lane < 16 && q0 + (lane >> 2) < p.mlt) S[(q0 + (lane >> 2)) * 4 + (lane & 3)] = s;
     }
     __syncwarp();
 #pragma unroll
@@ -498,8 +513,47 @@ __global__ void __launch_bounds__(64, 6) k_tab_bwd_P(TabParams p) {
 #pragma unroll
         for (int a = 0; a < 4; ++a) dT[a][q] += S[f * 4 + a];
     }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int q = 0; q < F; ++q) out[a * p.Mp + f0 + q] = dT[a][q];
     __syncwarp();
-    if (lane == 0) atomicAdd(p.counters + 1, static_cast<unsigned long long>(nreal));
+    if (lane == 0) atomicAdd(p.counters + 1, static_cast<unsigned long long>(p.n_real[i]));
+  }
+}
+
+// ---------------------------------------------------------------- k_tab_bwd_P (warp per centre)
+// Per-warp projections P[a][m] = sum_p dT[a][p] C[th][m][p] of every group of a centre (FMA +
+// reduce-scatter). Used for the atom blocks whose interval union is too wide for the tensor-core
+// kernel below (fb_list, e.g. fine tables), or for feature widths above 128.
+template <int F>
+__global__ void __launch_bounds__(64, 6) k_tab_bwd_P(TabParams p, const double* __restrict__ dTg,
+                                                     const int* __restrict__ fb_list, const int* __restrict__ fb_count,
+                                                     int na) {
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  const int wpb = blockDim.x >> 5;
+  const size_t istride = static_cast<size_t>(6) * p.Mp;
+  const int f0 = F * lane;
+  const int total = fb_list ? *fb_count * na : p.n;
+  for (int idx = blockIdx.x * wpb + wid; idx < total; idx += gridDim.x * wpb) {
+    const int i = fb_list ? fb_list[idx / na] * na + idx % na : idx;
+    if (i >= p.n) continue;
+    const int64_t off = p.row_off[i];
+    const int nreal = p.n_real[i];
+    int G = p.n_grp[i];
+    if (p.goff[i] + G > p.pcap) {
+      if (lane == 0) raise_err(p.err, DEV_PBUF);
+      G = 0;
+    }
+    const uint64_t* sk = p.skeys + off;
+    double* Pout = p.Pbuf + p.goff[i] * 24;
+    const double* dTi = dTg + static_cast<size_t>(i) * 4 * p.Mp;
+    double dT[4][F];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int q = 0; q < F; ++q) dT[a][q] = dTi[a * p.Mp + f0 + q];
     // --- P[a][m] = sum_p dT[a][p] C[m][p] per group (reduce-scatter over the feature lanes) ---
     int g = 0;
     for (int base = 0; base < nreal && g < G; base += 32) {
@@ -549,6 +603,263 @@ __global__ void __launch_bounds__(64, 6) k_tab_bwd_P(TabParams p) {
         }
         ++g;
       }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- k_tab_bwd_P2 (CTA, FP64 tensor pipe)
+// The projections of 32 consecutive centres at once: every interval touched by any of them (the
+// union, ~44 for Cu at h = 0.01 vs ~29 per centre) is staged ONCE in shared memory (cp.async,
+// double-buffered, 4 intervals = 24 coefficient rows per stage) and contracted with the 128 dT rows
+// (32 centres x 4) on DMMA.8x8x4: P[(i,a)][(th,m)] = sum_p dT[i][a][p] C[th][m][p]. The per-warp
+// kernel re-read 6 KB of coefficients per (centre, interval) through L1 and reduced with shuffles;
+// here coefficient traffic drops by ~20x and the MACs run on the tensor pipe. Only the (centre,
+// interval) pairs the centre really has are written (Pbuf, same layout as the per-warp kernel).
+constexpr int P2_NA = 32, P2_CB = 4, P2_UCAP = 128, P2_UW = P2_UCAP / 32, P2_BMW = 256;
+
+__host__ __device__ inline size_t p2_smem_bytes(int Mp) {
+  const int pitch = Mp + 4;
+  return static_cast<size_t>(4 * P2_NA + 2 * 6 * P2_CB) * pitch * sizeof(double) +
+         (2 * P2_BMW + P2_UCAP + 2 * P2_NA * P2_UW + 4) * sizeof(int);
+}
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double* __restrict__ dTg,
+                                                       int* __restrict__ fb_list, int* __restrict__ fb_count, int dbg) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int Mp = p.Mp, pitch = Mp + 4, units = Mp / 2;
+  double* dTs = reinterpret_cast<double*>(smem);              // [128][pitch]
+  double* Cs = dTs + 4 * P2_NA * pitch;                         // [2][24][pitch]
+  uint32_t* bm = reinterpret_cast<uint32_t*>(Cs + 2 * 6 * P2_CB * pitch); // [BMW]
+  int* wpre = reinterpret_cast<int*>(bm + P2_BMW);              // [BMW]
+  int* ubin = wpre + P2_BMW;                                    // [UCAP]
+  uint32_t* amask = reinterpret_cast<uint32_t*>(ubin + P2_UCAP); // [NA][UW]
+  int* apre = reinterpret_cast<int*>(amask + P2_NA * P2_UW);   // [NA][UW]
+  int* misc = apre + P2_NA * P2_UW;                             // bmin, bmax, U
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int nblk = (p.n + P2_NA - 1) / P2_NA;
+  for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const int i0 = blk * P2_NA;
+    // dT rows of the 32 centres (contiguous in dTg)
+    for (int q = tid; q < 4 * P2_NA * units; q += 256) {
+      const int row = q / units, c2 = q - row * units;
+      double* dst = dTs + row * pitch + 2 * c2;
+      if (i0 + (row >> 2) < p.n)
+        tc::cp_async16(dst, dTg + (static_cast<size_t>(i0) * 4 + row) * Mp + 2 * c2);
+      else
+        dst[0] = dst[1] = 0.0;
+    }
+    tc::cp_commit();
+    if (tid == 0) {
+      misc[0] = 0x7fffffff;
+      misc[1] = -1;
+    }
+    __syncthreads();
+    // interval range of the block (heads of each centre's sorted reals)
+    for (int al = warp * 4; al < warp * 4 + 4; ++al) {
+      const int i = i0 + al;
+      if (i >= p.n) break;
+      const int nreal = p.n_real[i];
+      const uint64_t* sk = p.skeys + p.row_off[i];
+      int lo = 0x7fffffff, hi = -1;
+      for (int k = lane; k < nreal; k += 32) {
+        const int b = static_cast<int>(sk[k] >> 32);
+        lo = min(lo, b);
+        hi = max(hi, b);
+      }
+      lo = warp_min(lo);
+      hi = warp_max(hi);
+      if (lane == 0 && hi >= 0) {
+        atomicMin(misc, lo);
+        atomicMax(misc + 1, hi);
+      }
+    }
+    __syncthreads();
+    const int bmin = misc[0], bmax = misc[1];
+    const int range = bmax < 0 ? 0 : bmax - bmin + 1;
+    const int nw = (range + 31) >> 5;
+    bool fallback = nw > P2_BMW;
+    if (!fallback)
+      for (int w = tid; w < nw; w += 256) bm[w] = 0u;
+    __syncthreads();
+    if (!fallback) {
+      for (int al = warp * 4; al < warp * 4 + 4; ++al) {
+        const int i = i0 + al;
+        if (i >= p.n) break;
+        const int nreal = p.n_real[i];
+        const uint64_t* sk = p.skeys + p.row_off[i];
+        for (int k = lane; k < nreal; k += 32) {
+          const int b = static_cast<int>(sk[k] >> 32) - bmin;
+          if (k == 0 || static_cast<int>(sk[k - 1] >> 32) - bmin != b) atomicOr(bm + (b >> 5), 1u << (b & 31));
+        }
+      }
+    }
+    __syncthreads();
+    if (!fallback && warp == 0) {
+      // exclusive prefix of the bitmap popcounts -> union list in ascending bin order
+      constexpr int PER = P2_BMW / 32;
+      int c[PER], s = 0;
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int w = lane * PER + k;
+        c[k] = w < nw ? __popc(bm[w]) : 0;
+        s += c[k];
+      }
+      int tot;
+      int ex = warp_excl_scan(s, lane, &tot);
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int w = lane * PER + k;
+        if (w < nw) {
+          wpre[w] = ex;
+          uint32_t bits = bm[w];
+          int at = ex;
+          while (bits) {
+            const int bit = __ffs(bits) - 1;
+            bits &= bits - 1;
+            if (at < P2_UCAP) ubin[at] = bmin + 32 * w + bit;
+            ++at;
+          }
+        }
+        ex += c[k];
+      }
+      if (lane == 0) misc[2] = tot;
+    }
+    __syncthreads();
+    const int U = range == 0 ? 0 : misc[2];
+    if (fallback || U > P2_UCAP) {
+      if (tid == 0) fb_list[atomicAdd(fb_count, 1)] = blk;
+      tc::cp_wait<0>();
+      __syncthreads();
+      continue;
+    }
+    // membership of each centre in the union (bit u of amask[al]) and per-word prefix counts
+    for (int w = tid; w < P2_NA * P2_UW; w += 256) amask[w] = 0u;
+    __syncthreads();
+    for (int al = warp * 4; al < warp * 4 + 4; ++al) {
+      const int i = i0 + al;
+      if (i >= p.n) break;
+      const int nreal = p.n_real[i];
+      const uint64_t* sk = p.skeys + p.row_off[i];
+      for (int k = lane; k < nreal; k += 32) {
+        const int b = static_cast<int>(sk[k] >> 32) - bmin;
+        if (k == 0 || static_cast<int>(sk[k - 1] >> 32) - bmin != b) {
+          const int u = wpre[b >> 5] + __popc(bm[b >> 5] & ((1u << (b & 31)) - 1u));
+          atomicOr(amask + al * P2_UW + (u >> 5), 1u << (u & 31));
+        }
+      }
+    }
+    __syncthreads();
+    for (int q = tid; q < P2_NA * P2_UW; q += 256) {
+      const int al = q / P2_UW, w = q - al * P2_UW;
+      int s = 0;
+      for (int x = 0; x < w; ++x) s += __popc(amask[al * P2_UW + x]);
+      apre[q] = s;
+    }
+    // coefficient chunks: CB intervals x 6 rows, double-buffered
+    const int nch = (U + P2_CB - 1) / P2_CB;
+    auto stage = [&](int ch, int buf) {
+      double* dst0 = Cs + buf * 6 * P2_CB * pitch;
+      for (int q = tid; q < 6 * P2_CB * units; q += 256) {
+        const int row = q / units, c2 = q - row * units;
+        const int u = ch * P2_CB + row / 6, m = row % 6;
+        double* dst = dst0 + row * pitch + 2 * c2;
+        if (u < U)
+          tc::cp_async16(dst, p.tab + static_cast<size_t>(ubin[u]) * 6 * Mp + m * Mp + 2 * c2);
+        else
+          dst[0] = dst[1] = 0.0;
+      }
+      tc::cp_commit();
+    };
+    if (nch > 0) stage(0, 0);
+    for (int ch = 0; ch < nch; ++ch) {
+      if (ch + 1 < nch) {
+        stage(ch + 1, (ch + 1) & 1);
+        tc::cp_wait<1>();
+      } else {
+        tc::cp_wait<0>();
+      }
+      __syncthreads();
+      const double* cs = Cs + (ch & 1) * 6 * P2_CB * pitch;
+      double acc[2][3][2];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 3; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+      const double* a0 = dTs + (warp * 16 + gid) * pitch + tig;
+      const double* b0 = cs + gid * pitch + tig;
+      // n-tile nt of this chunk covers union slots [ch*CB + (8 nt)/6, ch*CB + (8 nt + 7)/6]; an m-tile
+      // (2 centres) needs it only if one of its centres touches one of those intervals
+      unsigned use = 0u;
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const int al0 = warp * 4 + mt * 2;
+#pragma unroll
+        for (int nt = 0; nt < 3; ++nt) {
+          bool any = false;
+          for (int u = ch * P2_CB + (8 * nt) / 6; u <= ch * P2_CB + (8 * nt + 7) / 6 && u < U; ++u) {
+            const uint32_t bit = 1u << (u & 31);
+            any |= (amask[al0 * P2_UW + (u >> 5)] & bit) || (amask[(al0 + 1) * P2_UW + (u >> 5)] & bit);
+          }
+          if (any) use |= 1u << (mt * 3 + nt);
+        }
+      }
+      if (dbg & 1) use = 0u;
+      if (use == 0x3fu) {
+#pragma unroll 4
+        for (int k = 0; k < Mp; k += 4) {
+          const double av0 = a0[k], av1 = a0[8 * pitch + k];
+          const double bv0 = b0[k], bv1 = b0[8 * pitch + k], bv2 = b0[16 * pitch + k];
+          dmma884(acc[0][0][0], acc[0][0][1], av0, bv0);
+          dmma884(acc[0][1][0], acc[0][1][1], av0, bv1);
+          dmma884(acc[0][2][0], acc[0][2][1], av0, bv2);
+          dmma884(acc[1][0][0], acc[1][0][1], av1, bv0);
+          dmma884(acc[1][1][0], acc[1][1][1], av1, bv1);
+          dmma884(acc[1][2][0], acc[1][2][1], av1, bv2);
+        }
+      } else if (use) {
+#pragma unroll 2
+        for (int k = 0; k < Mp; k += 4) {
+          const double av0 = a0[k], av1 = a0[8 * pitch + k];
+          const double bv0 = b0[k], bv1 = b0[8 * pitch + k], bv2 = b0[16 * pitch + k];
+          if (use & 1u) dmma884(acc[0][0][0], acc[0][0][1], av0, bv0);
+          if (use & 2u) dmma884(acc[0][1][0], acc[0][1][1], av0, bv1);
+          if (use & 4u) dmma884(acc[0][2][0], acc[0][2][1], av0, bv2);
+          if (use & 8u) dmma884(acc[1][0][0], acc[1][0][1], av1, bv0);
+          if (use & 16u) dmma884(acc[1][1][0], acc[1][1][1], av1, bv1);
+          if (use & 32u) dmma884(acc[1][2][0], acc[1][2][1], av1, bv2);
+        }
+      }
+      // scatter the (centre, interval) pairs that exist into Pbuf
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const int r = warp * 16 + mt * 8 + gid;
+        const int al = r >> 2, a = r & 3;
+        const int i = i0 + al;
+        if (i >= p.n) continue;
+        const int64_t gbase = p.goff[i];
+        const bool ok = gbase + p.n_grp[i] <= p.pcap;
+        if (!ok && a == 0 && tig == 0) raise_err(p.err, DEV_PBUF);
+#pragma unroll
+        for (int nt = 0; nt < 3; ++nt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = nt * 8 + 2 * tig + h;
+            const int u = ch * P2_CB + c / 6, m = c % 6;
+            if (!ok || u >= U) continue;
+            const uint32_t word = amask[al * P2_UW + (u >> 5)];
+            if (!((word >> (u & 31)) & 1u)) continue;
+            const int g = apre[al * P2_UW + (u >> 5)] + __popc(word & ((1u << (u & 31)) - 1u));
+            p.Pbuf[(gbase + g) * 24 + a * 6 + m] = acc[mt][nt][h];
+          }
+      }
+      __syncthreads();
     }
   }
 }
@@ -626,12 +937,19 @@ void launch_fwd_warp(const TabParams& p, cudaStream_t st, int sms) {
 }
 
 template <int F>
-void launch_bwd_warp(const TabParams& p, cudaStream_t st, int sms) {
-  const size_t bytes = 2 * (4 * static_cast<size_t>(p.Mp) + 4 * p.mlt) * sizeof(double);
-  DPB_CUDA(cudaFuncSetAttribute(k_tab_bwd_P<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(bytes)));
-  const int blocks = std::max(1, std::min(ceil_div(p.n, 2), sms * 32));
-  k_tab_bwd_P<F><<<blocks, 64, bytes, st>>>(p);
+void launch_bwd_warp(const TabParams& p, const double* dTg, const int* fb_list, const int* fb_count, int na,
+                     cudaStream_t st, int sms) {
+  const int blocks = fb_list ? sms * 8 : std::max(1, std::min(ceil_div(p.n, 2), sms * 32));
+  k_tab_bwd_P<F><<<blocks, 64, 0, st>>>(p, dTg, fb_list, fb_count, na);
+  DPB_CUDA(cudaGetLastError());
+}
+
+template <int F>
+void launch_dT(const TabParams& p, double* dTg, cudaStream_t st, int sms) {
+  const size_t bytes = 8 * (4 * static_cast<size_t>(p.Mp) + 4 * p.mlt) * sizeof(double);
+  DPB_CUDA(cudaFuncSetAttribute(k_tab_dT<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+  const int blocks = std::max(1, std::min(ceil_div(p.n, 8), sms * 8));
+  k_tab_dT<F><<<blocks, 256, bytes, st>>>(p, dTg);
   DPB_CUDA(cudaGetLastError());
 }
 
@@ -704,15 +1022,36 @@ void Engine::grow_pbuf() {
 void Engine::launch_tab_bwd() {
   TabParams p = make_params(*this);
   const int sms = sm_count(device);
+  dTbuf.ensure(static_cast<size_t>(n) * 4 * Mp);
+  const int nblk = ceil_div(static_cast<int64_t>(n), P2_NA);
+  fb_list.ensure(nblk + 1);
   switch (Mp / 32) {
-    case 1: launch_bwd_warp<1>(p, stream, sms); break;
-    case 2: launch_bwd_warp<2>(p, stream, sms); break;
-    case 3: launch_bwd_warp<3>(p, stream, sms); break;
-    case 4: launch_bwd_warp<4>(p, stream, sms); break;
-    case 5: launch_bwd_warp<5>(p, stream, sms); break;
-    case 6: launch_bwd_warp<6>(p, stream, sms); break;
-    case 7: launch_bwd_warp<7>(p, stream, sms); break;
-    case 8: launch_bwd_warp<8>(p, stream, sms); break;
+#define DPB_DT(F) case F: launch_dT<F>(p, dTbuf.p, stream, sms); break;
+    DPB_DT(1) DPB_DT(2) DPB_DT(3) DPB_DT(4) DPB_DT(5) DPB_DT(6) DPB_DT(7) DPB_DT(8)
+#undef DPB_DT
+    default: throw InputErr("feature width 4*d1 must be at most 256");
+  }
+  ++launches;
+  const bool tensor = Mp <= 128;
+  const int* fl = nullptr;
+  const int* fc = nullptr;
+  if (tensor) {
+    // 32-centre blocks on the FP64 tensor pipe; blocks with a too wide interval union are listed
+    // and done by the per-warp kernel
+    DPB_CUDA(cudaMemsetAsync(fb_list.p + nblk, 0, sizeof(int), stream));
+    const size_t bytes = p2_smem_bytes(Mp);
+    DPB_CUDA(cudaFuncSetAttribute(k_tab_bwd_P2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+    static const int dbg = std::getenv("DPB_P2DBG") ? std::atoi(std::getenv("DPB_P2DBG")) : 0;
+    k_tab_bwd_P2<<<std::max(1, std::min(nblk, sms)), 256, bytes, stream>>>(p, dTbuf.p, fb_list.p, fb_list.p + nblk, dbg);
+    DPB_CUDA(cudaGetLastError());
+    ++launches;
+    fl = fb_list.p;
+    fc = fb_list.p + nblk;
+  }
+  switch (Mp / 32) {
+#define DPB_BW(F) case F: launch_bwd_warp<F>(p, dTbuf.p, fl, fc, P2_NA, stream, sms); break;
+    DPB_BW(1) DPB_BW(2) DPB_BW(3) DPB_BW(4) DPB_BW(5) DPB_BW(6) DPB_BW(7) DPB_BW(8)
+#undef DPB_BW
     default: throw InputErr("feature width 4*d1 must be at most 256");
   }
   ++launches;
