@@ -124,7 +124,7 @@ struct Engine {
   // ---- per-step buffers ----
   DevBuf<uint64_t> skeys;      // [E] reals sorted by (type, interval)
   DevBuf<int32_t> eown;         // [E] centre of each list entry
-  DevBuf<int32_t> ebin, egrp;   // [E] bin of real entries (-1 else), group index
+  DevBuf<int32_t> ebin, egrp, gbin;   // [E] bin of real entries (-1 else), group index
   DevBuf<double> erc;           // [5][E] per-entry R0..R3, u
   DevBuf<int32_t> n_grp;        // [n+1]
   DevBuf<int64_t> goff;         // [n+1]

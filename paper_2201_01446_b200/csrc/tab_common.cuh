@@ -18,6 +18,7 @@ struct TabParams {
   int32_t* ebin;        // [E] global bin t*tn + interval of a real entry, -1 otherwise
   double* erc;          // [5][E] SoA: R0..R3, u of real entries
   int32_t* egrp;        // [E] group index of a real entry inside its centre
+  int32_t* gbin;        // [E] per row: the centre's group bins, ascending (first n_grp entries)
   uint64_t* skeys;      // [E] per row: reals sorted by bin, (bin << 32 | entry)
   int32_t* n_real;      // [n]
   int32_t* n_grp;       // [n+1] groups per centre -> (scanned) offsets into Pbuf
@@ -200,6 +201,7 @@ inline TabParams make_params(Engine& E) {
   p.ebin = E.ebin.p;
   p.erc = E.erc.p;
   p.egrp = E.egrp.p;
+  p.gbin = E.gbin.p;
   p.skeys = E.skeys.p;
   p.n_real = E.n_real.p;
   p.n_grp = E.n_grp.p;

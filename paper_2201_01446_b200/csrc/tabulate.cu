@@ -293,8 +293,10 @@ __global__ void __launch_bounds__(64, 8) k_tab_fwd(TabParams p) {
       const int k = w.od[j];
       p.skeys[off + j] = (static_cast<uint64_t>(w.rk[k]) << 32) | w.ex[k];
     }
-    for (int g = lane; g < G; g += 32)
+    for (int g = lane; g < G; g += 32) {
+      p.gbin[off + g] = w.gb[g];
       for (int j = w.gs[g]; j < w.gs[g + 1]; ++j) p.egrp[off + w.ex[w.od[j]]] = g;
+    }
     // --- moments of each (type, interval) group, then T += W . C[interval] ---
     double tacc[4][F];
 #pragma unroll
@@ -620,7 +622,7 @@ constexpr int P2_NA = 32, P2_CB = 4, P2_UCAP = 128, P2_UW = P2_UCAP / 32, P2_BMW
 __host__ __device__ inline size_t p2_smem_bytes(int Mp) {
   const int pitch = Mp + 4;
   return static_cast<size_t>(4 * P2_NA + 2 * 6 * P2_CB) * pitch * sizeof(double) +
-         (2 * P2_BMW + P2_UCAP + 2 * P2_NA * P2_UW + 4) * sizeof(int);
+         (2 * P2_BMW + P2_UCAP + P2_NA / 2 * P2_UW + 4) * sizeof(int) + P2_NA * P2_UCAP * sizeof(int16_t);
 }
 
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
@@ -629,26 +631,37 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
                : "d"(a), "d"(b));
 }
 
+template <int F>
 __global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double* __restrict__ dTg,
-                                                       int* __restrict__ fb_list, int* __restrict__ fb_count, int dbg) {
+                                                       int* __restrict__ fb_list, int* __restrict__ fb_count) {
+  constexpr int Mp = 32 * F, pitch = Mp + 4, units = Mp / 2;
   extern __shared__ __align__(16) unsigned char smem[];
-  const int Mp = p.Mp, pitch = Mp + 4, units = Mp / 2;
-  double* dTs = reinterpret_cast<double*>(smem);              // [128][pitch]
-  double* Cs = dTs + 4 * P2_NA * pitch;                         // [2][24][pitch]
-  uint32_t* bm = reinterpret_cast<uint32_t*>(Cs + 2 * 6 * P2_CB * pitch); // [BMW]
-  int* wpre = reinterpret_cast<int*>(bm + P2_BMW);              // [BMW]
-  int* ubin = wpre + P2_BMW;                                    // [UCAP]
-  uint32_t* amask = reinterpret_cast<uint32_t*>(ubin + P2_UCAP); // [NA][UW]
-  int* apre = reinterpret_cast<int*>(amask + P2_NA * P2_UW);   // [NA][UW]
-  int* misc = apre + P2_NA * P2_UW;                             // bmin, bmax, U
+  double* dTs = reinterpret_cast<double*>(smem);                         // [128][pitch]
+  double* Cs = dTs + 4 * P2_NA * pitch;                                  // [2][24][pitch]
+  uint32_t* bm = reinterpret_cast<uint32_t*>(Cs + 2 * 6 * P2_CB * pitch); // [BMW] union bitmap
+  int* wpre = reinterpret_cast<int*>(bm + P2_BMW);                       // [BMW] popcount prefix
+  int* ubin = wpre + P2_BMW;                                             // [UCAP] union bins
+  uint32_t* mtmask = reinterpret_cast<uint32_t*>(ubin + P2_UCAP);        // [NA/2][UW] per m-tile union
+  int* misc = reinterpret_cast<int*>(mtmask + P2_NA / 2 * P2_UW);        // bmin, bmax, U
+  int16_t* gidx = reinterpret_cast<int16_t*>(misc + 4);                  // [NA][UCAP] group of slot or -1
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gid = lane >> 2, tig = lane & 3;
   const int nblk = (p.n + P2_NA - 1) / P2_NA;
+  // output columns of this thread inside a chunk: c = 8 nt + 2 tig + h -> (slot c / 6, m = c % 6)
+  int cslot[6], cm[6];
+#pragma unroll
+  for (int nt = 0; nt < 3; ++nt)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = nt * 8 + 2 * tig + h;
+      cslot[nt * 2 + h] = c / 6;
+      cm[nt * 2 + h] = c % 6;
+    }
   for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
     const int i0 = blk * P2_NA;
     // dT rows of the 32 centres (contiguous in dTg)
     for (int q = tid; q < 4 * P2_NA * units; q += 256) {
-      const int row = q / units, c2 = q - row * units;
+      const int row = q / units, c2 = q % units;
       double* dst = dTs + row * pitch + 2 * c2;
       if (i0 + (row >> 2) < p.n)
         tc::cp_async16(dst, dTg + (static_cast<size_t>(i0) * 4 + row) * Mp + 2 * c2);
@@ -660,48 +673,41 @@ __global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double
       misc[0] = 0x7fffffff;
       misc[1] = -1;
     }
+    for (int q = tid; q < P2_NA * P2_UCAP / 2; q += 256) reinterpret_cast<int32_t*>(gidx)[q] = -1;
+    for (int q = tid; q < P2_NA / 2 * P2_UW; q += 256) mtmask[q] = 0u;
     __syncthreads();
-    // interval range of the block (heads of each centre's sorted reals)
-    for (int al = warp * 4; al < warp * 4 + 4; ++al) {
-      const int i = i0 + al;
-      if (i >= p.n) break;
-      const int nreal = p.n_real[i];
-      const uint64_t* sk = p.skeys + p.row_off[i];
-      int lo = 0x7fffffff, hi = -1;
-      for (int k = lane; k < nreal; k += 32) {
-        const int b = static_cast<int>(sk[k] >> 32);
-        lo = min(lo, b);
-        hi = max(hi, b);
-      }
-      lo = warp_min(lo);
-      hi = warp_max(hi);
-      if (lane == 0 && hi >= 0) {
-        atomicMin(misc, lo);
-        atomicMax(misc + 1, hi);
+    // interval range of the block: each centre's group bins are sorted (gbin, written by k_tab_fwd)
+    if (tid < P2_NA && i0 + tid < p.n) {
+      const int i = i0 + tid;
+      const int G = p.n_grp[i];
+      if (G > 0) {
+        const int32_t* gb = p.gbin + p.row_off[i];
+        atomicMin(misc, gb[0]);
+        atomicMax(misc + 1, gb[G - 1]);
       }
     }
     __syncthreads();
     const int bmin = misc[0], bmax = misc[1];
     const int range = bmax < 0 ? 0 : bmax - bmin + 1;
     const int nw = (range + 31) >> 5;
-    bool fallback = nw > P2_BMW;
-    if (!fallback)
+    const bool wide = nw > P2_BMW;
+    if (!wide)
       for (int w = tid; w < nw; w += 256) bm[w] = 0u;
     __syncthreads();
-    if (!fallback) {
+    if (!wide) {
       for (int al = warp * 4; al < warp * 4 + 4; ++al) {
         const int i = i0 + al;
         if (i >= p.n) break;
-        const int nreal = p.n_real[i];
-        const uint64_t* sk = p.skeys + p.row_off[i];
-        for (int k = lane; k < nreal; k += 32) {
-          const int b = static_cast<int>(sk[k] >> 32) - bmin;
-          if (k == 0 || static_cast<int>(sk[k - 1] >> 32) - bmin != b) atomicOr(bm + (b >> 5), 1u << (b & 31));
+        const int G = p.n_grp[i];
+        const int32_t* gb = p.gbin + p.row_off[i];
+        for (int g = lane; g < G; g += 32) {
+          const int b = gb[g] - bmin;
+          atomicOr(bm + (b >> 5), 1u << (b & 31));
         }
       }
     }
     __syncthreads();
-    if (!fallback && warp == 0) {
+    if (!wide && warp == 0) {
       // exclusive prefix of the bitmap popcounts -> union list in ascending bin order
       constexpr int PER = P2_BMW / 32;
       int c[PER], s = 0;
@@ -733,41 +739,48 @@ __global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double
     }
     __syncthreads();
     const int U = range == 0 ? 0 : misc[2];
-    if (fallback || U > P2_UCAP) {
+    if (wide || U > P2_UCAP) {
       if (tid == 0) fb_list[atomicAdd(fb_count, 1)] = blk;
       tc::cp_wait<0>();
       __syncthreads();
       continue;
     }
-    // membership of each centre in the union (bit u of amask[al]) and per-word prefix counts
-    for (int w = tid; w < P2_NA * P2_UW; w += 256) amask[w] = 0u;
-    __syncthreads();
+    // slot -> group of each centre, and the union each m-tile (2 centres) really needs
     for (int al = warp * 4; al < warp * 4 + 4; ++al) {
       const int i = i0 + al;
       if (i >= p.n) break;
-      const int nreal = p.n_real[i];
-      const uint64_t* sk = p.skeys + p.row_off[i];
-      for (int k = lane; k < nreal; k += 32) {
-        const int b = static_cast<int>(sk[k] >> 32) - bmin;
-        if (k == 0 || static_cast<int>(sk[k - 1] >> 32) - bmin != b) {
-          const int u = wpre[b >> 5] + __popc(bm[b >> 5] & ((1u << (b & 31)) - 1u));
-          atomicOr(amask + al * P2_UW + (u >> 5), 1u << (u & 31));
-        }
+      const int G = p.n_grp[i];
+      const int32_t* gb = p.gbin + p.row_off[i];
+      for (int g = lane; g < G; g += 32) {
+        const int b = gb[g] - bmin;
+        const int u = wpre[b >> 5] + __popc(bm[b >> 5] & ((1u << (b & 31)) - 1u));
+        gidx[al * P2_UCAP + u] = static_cast<int16_t>(g);
+        atomicOr(mtmask + (al >> 1) * P2_UW + (u >> 5), 1u << (u & 31));
       }
     }
-    __syncthreads();
-    for (int q = tid; q < P2_NA * P2_UW; q += 256) {
-      const int al = q / P2_UW, w = q - al * P2_UW;
-      int s = 0;
-      for (int x = 0; x < w; ++x) s += __popc(amask[al * P2_UW + x]);
-      apre[q] = s;
+    // this thread's two output rows (one per m-tile): centre, component, group base
+    int r_al[2], r_a[2];
+    int64_t r_base[2];
+    bool r_ok[2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int r = warp * 16 + mt * 8 + gid;
+      r_al[mt] = r >> 2;
+      r_a[mt] = r & 3;
+      const int i = i0 + r_al[mt];
+      r_ok[mt] = i < p.n;
+      r_base[mt] = r_ok[mt] ? p.goff[i] : 0;
+      if (r_ok[mt] && r_base[mt] + p.n_grp[i] > p.pcap) {
+        if (r_a[mt] == 0 && tig == 0) raise_err(p.err, DEV_PBUF);
+        r_ok[mt] = false;
+      }
     }
     // coefficient chunks: CB intervals x 6 rows, double-buffered
     const int nch = (U + P2_CB - 1) / P2_CB;
     auto stage = [&](int ch, int buf) {
       double* dst0 = Cs + buf * 6 * P2_CB * pitch;
       for (int q = tid; q < 6 * P2_CB * units; q += 256) {
-        const int row = q / units, c2 = q - row * units;
+        const int row = q / units, c2 = q % units;
         const int u = ch * P2_CB + row / 6, m = row % 6;
         double* dst = dst0 + row * pitch + 2 * c2;
         if (u < U)
@@ -794,23 +807,13 @@ __global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double
         for (int nt = 0; nt < 3; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
       const double* a0 = dTs + (warp * 16 + gid) * pitch + tig;
       const double* b0 = cs + gid * pitch + tig;
-      // n-tile nt of this chunk covers union slots [ch*CB + (8 nt)/6, ch*CB + (8 nt + 7)/6]; an m-tile
-      // (2 centres) needs it only if one of its centres touches one of those intervals
-      unsigned use = 0u;
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-        const int al0 = warp * 4 + mt * 2;
-#pragma unroll
-        for (int nt = 0; nt < 3; ++nt) {
-          bool any = false;
-          for (int u = ch * P2_CB + (8 * nt) / 6; u <= ch * P2_CB + (8 * nt + 7) / 6 && u < U; ++u) {
-            const uint32_t bit = 1u << (u & 31);
-            any |= (amask[al0 * P2_UW + (u >> 5)] & bit) || (amask[(al0 + 1) * P2_UW + (u >> 5)] & bit);
-          }
-          if (any) use |= 1u << (mt * 3 + nt);
-        }
-      }
-      if (dbg & 1) use = 0u;
+      // n-tile nt covers chunk slots {nt, nt+1} (columns 8 nt .. 8 nt + 7 of 6 per slot); an m-tile
+      // needs it only if one of its two centres has one of those intervals
+      const int sh = (ch * P2_CB) & 31, wd = (ch * P2_CB) >> 5;
+      const unsigned n0 = (mtmask[(2 * warp) * P2_UW + wd] >> sh) & 15u;
+      const unsigned n1 = (mtmask[(2 * warp + 1) * P2_UW + wd] >> sh) & 15u;
+      const unsigned use = ((n0 & 3u) ? 1u : 0u) | ((n0 & 6u) ? 2u : 0u) | ((n0 & 12u) ? 4u : 0u) |
+                           ((n1 & 3u) ? 8u : 0u) | ((n1 & 6u) ? 16u : 0u) | ((n1 & 12u) ? 32u : 0u);
       if (use == 0x3fu) {
 #pragma unroll 4
         for (int k = 0; k < Mp; k += 4) {
@@ -839,25 +842,15 @@ __global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double
       // scatter the (centre, interval) pairs that exist into Pbuf
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
-        const int r = warp * 16 + mt * 8 + gid;
-        const int al = r >> 2, a = r & 3;
-        const int i = i0 + al;
-        if (i >= p.n) continue;
-        const int64_t gbase = p.goff[i];
-        const bool ok = gbase + p.n_grp[i] <= p.pcap;
-        if (!ok && a == 0 && tig == 0) raise_err(p.err, DEV_PBUF);
+        if (!r_ok[mt]) continue;
+        const int16_t* gi = gidx + r_al[mt] * P2_UCAP + ch * P2_CB;
+        double* pb = p.Pbuf + r_base[mt] * 24 + r_a[mt] * 6;
 #pragma unroll
-        for (int nt = 0; nt < 3; ++nt)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int c = nt * 8 + 2 * tig + h;
-            const int u = ch * P2_CB + c / 6, m = c % 6;
-            if (!ok || u >= U) continue;
-            const uint32_t word = amask[al * P2_UW + (u >> 5)];
-            if (!((word >> (u & 31)) & 1u)) continue;
-            const int g = apre[al * P2_UW + (u >> 5)] + __popc(word & ((1u << (u & 31)) - 1u));
-            p.Pbuf[(gbase + g) * 24 + a * 6 + m] = acc[mt][nt][h];
-          }
+        for (int k = 0; k < 6; ++k) {
+          const int u = ch * P2_CB + cslot[k];
+          const int g = u < U ? gi[cslot[k]] : -1;
+          if (g >= 0) pb[static_cast<int64_t>(g) * 24 + cm[k]] = acc[mt][k >> 1][k & 1];
+        }
       }
       __syncthreads();
     }
@@ -1040,9 +1033,17 @@ void Engine::launch_tab_bwd() {
     // and done by the per-warp kernel
     DPB_CUDA(cudaMemsetAsync(fb_list.p + nblk, 0, sizeof(int), stream));
     const size_t bytes = p2_smem_bytes(Mp);
-    DPB_CUDA(cudaFuncSetAttribute(k_tab_bwd_P2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
-    static const int dbg = std::getenv("DPB_P2DBG") ? std::atoi(std::getenv("DPB_P2DBG")) : 0;
-    k_tab_bwd_P2<<<std::max(1, std::min(nblk, sms)), 256, bytes, stream>>>(p, dTbuf.p, fb_list.p, fb_list.p + nblk, dbg);
+    switch (Mp / 32) {
+#define DPB_P2(F)                                                                                             \
+  case F:                                                                                                     \
+    DPB_CUDA(cudaFuncSetAttribute(k_tab_bwd_P2<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
+                                  static_cast<int>(bytes)));                                                  \
+    k_tab_bwd_P2<F><<<std::max(1, std::min(nblk, sms)), 256, bytes, stream>>>(p, dTbuf.p, fb_list.p,         \
+                                                                              fb_list.p + nblk);              \
+    break;
+      DPB_P2(1) DPB_P2(2) DPB_P2(3) DPB_P2(4)
+#undef DPB_P2
+    }
     DPB_CUDA(cudaGetLastError());
     ++launches;
     fl = fb_list.p;
