@@ -12,13 +12,15 @@
 // SASS DMMA.8x8x4), measured at 37.1 TFLOP/s on this B200 (profiles/r01_fp64_peak_microbench.log).
 // Tiles: CTA 64x64, BK 16, 4 warps of 32x32 (4x4 DMMA tiles), 3-stage cp.async pipeline; both
 // operands K-contiguous in shared memory with a 20-double row pitch (bank-conflict free).
+#include <cstdlib>
+
 #include "engine.hpp"
 
 namespace dpb {
 
 namespace {
 
-constexpr int BM = 64, BK = 16, PITCH = BK + 4, STAGES = 3;
+constexpr int BM = 64, BK = 16, PITCH = BK + 4;
 
 enum Epi : int { EPI_FWD = 0, EPI_BWD = 1 };
 
@@ -56,7 +58,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 }
 
 // BN = 64 (4 DMMA column tiles per warp) or 80 (5): 240-wide layers tile exactly with 80.
-template <int EPI, int BN>
+template <int EPI, int BN, int STAGES>
 __global__ void __launch_bounds__(128) k_gemm(GemmArgs g) {
   constexpr int NT = BN / 16; // 8-wide column tiles per warp (2 warps across BN)
   extern __shared__ __align__(16) double sm[];
@@ -192,28 +194,31 @@ __global__ void k_scatter_energy(int64_t slots, const int32_t* __restrict__ atom
   if (a >= 0) e_atom[a] = e_slot[s];
 }
 
-template <int EPI, int BN>
+template <int EPI, int BN, int STAGES>
 void launch_gemm(const GemmArgs& a, int rows, int N, cudaStream_t st) {
   const size_t bytes = static_cast<size_t>(STAGES) * (BM + BN) * PITCH * sizeof(double);
   static bool init = false;
   if (!init) {
-    DPB_CUDA(cudaFuncSetAttribute(k_gemm<EPI, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    DPB_CUDA(cudaFuncSetAttribute(k_gemm<EPI, BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(bytes)));
     init = true;
   }
-  k_gemm<EPI, BN><<<dim3(N / BN, rows / BM), 128, bytes, st>>>(a);
+  k_gemm<EPI, BN, STAGES><<<dim3(N / BN, rows / BM), 128, bytes, st>>>(a);
   DPB_CUDA(cudaGetLastError());
 }
 
 // N is a multiple of 80 or 64 (widths are padded by pad_width()).
+// Short K (hidden layers): 2 stages -> 4 CTAs/SM to hide the epilogue's global latency.
 void run_gemm(int epi, const GemmArgs& a, int rows, int N, cudaStream_t st) {
   const bool b80 = N % 80 == 0;
+  static const int kshort = std::getenv("DPB_GEMM_KSHORT") ? std::atoi(std::getenv("DPB_GEMM_KSHORT")) : 256;
+  const bool s2 = a.K <= kshort;
   if (epi == EPI_FWD) {
-    if (b80) launch_gemm<EPI_FWD, 80>(a, rows, N, st);
-    else launch_gemm<EPI_FWD, 64>(a, rows, N, st);
+    if (b80) s2 ? launch_gemm<EPI_FWD, 80, 2>(a, rows, N, st) : launch_gemm<EPI_FWD, 80, 3>(a, rows, N, st);
+    else s2 ? launch_gemm<EPI_FWD, 64, 2>(a, rows, N, st) : launch_gemm<EPI_FWD, 64, 3>(a, rows, N, st);
   } else {
-    if (b80) launch_gemm<EPI_BWD, 80>(a, rows, N, st);
-    else launch_gemm<EPI_BWD, 64>(a, rows, N, st);
+    if (b80) s2 ? launch_gemm<EPI_BWD, 80, 2>(a, rows, N, st) : launch_gemm<EPI_BWD, 80, 3>(a, rows, N, st);
+    else s2 ? launch_gemm<EPI_BWD, 64, 2>(a, rows, N, st) : launch_gemm<EPI_BWD, 64, 3>(a, rows, N, st);
   }
 }
 
