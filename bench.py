@@ -57,52 +57,79 @@ def algorithmic_flops_per_atom(m, n_real: float) -> float:
     return fitting_flops_per_atom(m) + 16384 + 32768 + 7060.0 * n_real
 
 
+_SAMPLER = r"""
+import sys, time, pynvml
+pynvml.nvmlInit()
+bus, period = sys.argv[1], float(sys.argv[2])
+try:
+    h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+except Exception:
+    h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[3]))
+mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+fn = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+print("ready", flush=True)
+import select
+while True:
+    r, _, _ = select.select([sys.stdin], [], [], period)
+    print(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM), mx, int(fn(h)), flush=True)
+    if r:
+        break
+"""
+
+
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region by a separate NVML process
+    (started with the sampler, not forked from a thread mid-run). In-process NVML or nvidia-smi
+    queries from a thread of this CUDA process stalled the timed region at random; the sampling
+    period is 100 ms."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap"}
 
-    def __init__(self, gpu: int):
-        self.gpu = gpu
+    def __init__(self, gpu: int, period: float = float(os.environ.get("BENCH_CLK_PERIOD", "0.1"))):
+        self.gpu, self.period = gpu, period
         self.samples = []
-        self._stop = threading.Event()
-        self._t = None
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        self._p = None
+        try:
+            import torch
+            pr = torch.cuda.get_device_properties(gpu)
+            self.bus = "%08X:%02X:%02X.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id)
+        except Exception:
+            self.bus = ""
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        if os.environ.get("BENCH_NO_CLOCKS"):
+            return self
+        try:
+            self._p = subprocess.Popen([sys.executable, "-c", _SAMPLER, self.bus, str(self.period), str(self.gpu)],
+                                       stdin=subprocess.PIPE, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                       text=True)
+            line = self._p.stdout.readline()
+            if not line.startswith("ready"):
+                self._p = None
+        except Exception:
+            self._p = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        if self._t:
-            self._t.join(timeout=6)
+        if self._p is None:
+            return
+        try:
+            out, _ = self._p.communicate("stop\n", timeout=10)
+            for line in out.splitlines():
+                f = line.split()
+                if len(f) == 3:
+                    self.samples.append((float(f[0]), float(f[1]), int(f[2])))
+        except Exception:
+            self._p.kill()
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for s in self.samples for k in range(4)
-                          if len(s) > 2 + k and s[2 + k].lower().startswith("active")})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+        sm = [s[0] for s in self.samples]
+        reasons = sorted({name for s in self.samples for bit, name in self.REASONS.items() if s[2] & bit})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": reasons, "samples": len(self.samples), "source": "NVML (sampler process, 100 ms)"}
 
 
 def dist_setup():

@@ -174,6 +174,7 @@ int dp_neighbor_list_build(dp_handle* h, int64_t n, const double* pos, const int
     E.set_config(n, pos, types, box, pbc);
     E.build_list(cutoff);
     E.check_err();
+    E.sync_entry_count();
     if (total) *total = E.n_entries;
   });
 }

@@ -28,6 +28,7 @@ enum DevErr : int {
   DEV_STALE = 6,       // list stale in MD (md.cpp:211-217)
   DEV_PBUF = 7,        // tabulate group buffer too small (grows at the next list rebuild)
   DEV_TABLE_VERIFY = 8, // GPU-built table does not reproduce the net at a node (table.cpp:133-147)
+  DEV_LIST_CAP = 9,    // asynchronous MD rebuild produced more entries than the list capacity
 };
 
 // Cell as the kernels see it (geom.hpp:14-44).

@@ -35,6 +35,7 @@ void raise_device_error(int code) {
     case DEV_ROW_CAP: throw NumErr("neighbour row exceeds the kernel capacity");
     case DEV_PBUF: throw NumErr("tabulate group buffer overflow (retry: it grows at the next rebuild)");
     case DEV_TABLE_VERIFY: throw NumErr("table verification failed at a node");
+    case DEV_LIST_CAP: throw NumErr("neighbour list grew past its capacity (+25 %) between MD rebuilds");
     case DEV_STALE: throw NumErr("neighbor list stale: an atom moved more than half the buffer since the last rebuild");
     default: throw CudaErr("unknown device error " + std::to_string(code));
   }
@@ -162,6 +163,17 @@ void Engine::create(const dp_model_desc* md, const dp_table_desc* td, int dev, i
   if (precision == 1) prepare_mixed();
   d_max_nbr.ensure(n_types);
   DPB_CUDA(cudaMemcpy(d_max_nbr.p, max_nbr.data(), n_types * sizeof(int), cudaMemcpyHostToDevice));
+  // Buffers that may grow inside the MD loop are stream-ordered: growing them must not
+  // synchronise the device (a cudaFree would drain the whole queued trajectory). Keep freed
+  // pool memory cached so regrowth is cheap.
+  {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    Pbuf.ord = stream;
+  }
   err.ensure(1);
   counters.ensure(3);
   exact_ctr.ensure(3);
@@ -243,6 +255,7 @@ void Engine::set_config(int64_t nn, const double* pos, const int32_t* ty, const 
     n = nn;
     list_valid = false;
     pbuf_cap = 0; // resize the group buffer from the next evaluation's exact total
+    row_cap = 0;  // and the row capacity from the next (synchronous) list build
     h_types.assign(ty, ty + nn);
     types.ensure(n);
     DPB_CUDA(cudaMemcpyAsync(types.p, ty, n * sizeof(int32_t), cudaMemcpyHostToDevice, stream));
@@ -326,17 +339,17 @@ void Engine::upload_positions(const double* pos) {
   launch_pos4(*this);
 }
 
-void Engine::build_list(double cutoff) {
+void Engine::build_list(double cutoff, bool async) {
   phase_begin(0);
-  launch_nlist(cutoff); // synchronises: the last evaluation's group total is final here
+  launch_nlist(cutoff, async);
   phase_end();
   if (pbuf_cap > 0) grow_pbuf();
-  skeys.ensure(n_entries + 1);
-  ebin.ensure(n_entries + 1);
-  egrp.ensure(n_entries + 1);
-  gbin.ensure(n_entries + 1);
-  erc.ensure(5 * n_entries + 5);
-  g.ensure(3 * n_entries + 3);
+  skeys.ensure(e_cap + 1);
+  ebin.ensure(e_cap + 1);
+  egrp.ensure(e_cap + 1);
+  gbin.ensure(e_cap + 1);
+  erc.ensure(5 * e_cap + 5);
+  g.ensure(3 * e_cap + 3);
 }
 
 void Engine::evaluate() {
@@ -484,6 +497,14 @@ void Engine::md_begin(const double* pos, const double* vel, const dp_md_config* 
   md_step = 0;
   md_active = true;
   check_err();
+  // The group count grows while a lattice start thermalises; Pbuf then regrows inside the loop.
+  // Pre-warm the stream-ordered pool (kept, release threshold = max) so that regrowth is a
+  // sub-allocation instead of a physical allocation stalling the host for tens of ms.
+  if (Pbuf.n) {
+    void* tmp = nullptr;
+    if (cudaMallocAsync(&tmp, Pbuf.n * sizeof(double) * 3, stream) == cudaSuccess) cudaFreeAsync(tmp, stream);
+    else cudaGetLastError();
+  }
 }
 
 void Engine::md_steps(int64_t k) {
@@ -499,7 +520,7 @@ void Engine::md_steps(int64_t k) {
       if (dist)
         dist_rebuild(*this);
       else
-        build_list(r_cut + md.buffer);
+        build_list(r_cut + md.buffer, true); // no host sync: capacities are checked on the device
     } else if (dist) {
       phase_begin(6);
       dist_halo_forward(*this);

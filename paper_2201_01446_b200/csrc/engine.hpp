@@ -13,6 +13,10 @@
 //   vpart[n][9]        per-centre virial partials, reduced in a fixed order
 #pragma once
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -33,15 +37,29 @@ template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  cudaStream_t ord = nullptr; // set: stream-ordered (cudaMallocAsync / cudaFreeAsync) buffer
   void ensure(size_t count) {
     if (count <= n) return;
+    static const bool trace = std::getenv("DPB_TRACE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     release();
     size_t want = count + count / 8 + 64;
-    DPB_CUDA(cudaMalloc(&p, want * sizeof(T)));
+    if (ord)
+      DPB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), want * sizeof(T), ord));
+    else
+      DPB_CUDA(cudaMalloc(&p, want * sizeof(T)));
     n = want;
+    if (trace)
+      std::fprintf(stderr, "[dpb] %salloc %zu B: %.2f ms\n", ord ? "stream-ordered " : "", want * sizeof(T),
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (ord)
+        cudaFreeAsync(p, ord);
+      else
+        cudaFree(p);
+    }
     p = nullptr;
     n = 0;
   }
@@ -109,8 +127,10 @@ struct Engine {
   // ---- neighbour list ----
   double list_cutoff = 0;
   bool list_valid = false;
-  int64_t n_entries = 0;
+  int64_t n_entries = 0; // -1 after an asynchronous rebuild (see sync_entry_count)
   int max_row = 0;
+  int64_t e_cap = 0;      // per-entry buffer capacity (SoA stride of the step buffers)
+  int row_cap = 0;        // row length capacity (power of two)
   DevBuf<int64_t> row_off;
   DevBuf<uint64_t> keys;
   DevBuf<int32_t> rev;
@@ -188,7 +208,8 @@ struct Engine {
                   const uint8_t* pbc, const uint8_t* center_mask = nullptr);
   void upload_positions(const double* pos);
   // neighbour list at `cutoff`, device resident
-  void build_list(double cutoff);
+  void build_list(double cutoff, bool async = false);
+  void sync_entry_count();
   void download_list(int64_t* offsets, int32_t* j, int32_t* shift);
   // one evaluation on the current positions/list; results stay on device
   void evaluate();
@@ -198,7 +219,7 @@ struct Engine {
   void reset_counters();
   void read_counters();
   // kernels (defined in the .cu files)
-  void launch_nlist(double cutoff);
+  void launch_nlist(double cutoff, bool async);
   void launch_tab_fwd();
   void launch_fitting();
   void launch_fitting_mixed();

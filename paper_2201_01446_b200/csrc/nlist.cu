@@ -70,9 +70,13 @@ __global__ void k_nlist_pass(NlParams p, const double4* __restrict__ pos,
                              const int* __restrict__ bin_of, const int* __restrict__ bin_start,
                              const int* __restrict__ bin_atoms, int64_t* __restrict__ row_len,
                              const int64_t* __restrict__ row_off, uint64_t* __restrict__ keys,
-                             int32_t* __restrict__ eown, int* err) {
+                             int32_t* __restrict__ eown, int* err, int64_t e_cap) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= p.n) return;
+  if (WRITE && row_off[i + 1] > e_cap) { // asynchronous rebuild past the list capacity
+    raise_err(err, DEV_LIST_CAP);
+    return;
+  }
   const int bi = bin_of[i];
   const int bc[3] = {bi / (p.nb[1] * p.nb[2]), (bi / p.nb[2]) % p.nb[1], bi % p.nb[2]};
   int cnt[3], first[3];
@@ -225,7 +229,7 @@ double host_spacing(const DevCell& c, int k) {
 
 } // namespace
 
-void Engine::launch_nlist(double cutoff) {
+void Engine::launch_nlist(double cutoff, bool async) {
   if (!(cutoff > 0.0)) throw InputErr("neighbor cutoff must be positive");
   if (n >= (1ll << 28)) throw InputErr("too many atoms for the packed neighbour key (2^28)");
   NlParams p;
@@ -270,7 +274,7 @@ void Engine::launch_nlist(double cutoff) {
   ++launches;
   k_nlist_pass<false><<<ceil_div(N, 128), 128, 0, stream>>>(p, pos4.p, frac.p, types.p, bin_of.p,
                                                             bin_start.p, bin_atoms.p, lens.p,
-                                                            nullptr, nullptr, nullptr, err.p);
+                                                            nullptr, nullptr, nullptr, err.p, 0);
   ++launches;
   DPB_CUDA(cudaMemsetAsync(lens.p + n, 0, sizeof(int64_t), stream));
   size_t tmp2 = 0;
@@ -281,22 +285,32 @@ void Engine::launch_nlist(double cutoff) {
   DPB_CUDA(cudaMemsetAsync(row_len.p, 0, sizeof(int), stream));
   k_max_len<<<std::min(ceil_div(N, 256), 1024), 256, 0, stream>>>(N, lens.p, row_len.p);
   ++launches;
-  int64_t total = 0;
-  int mx = 0;
-  DPB_CUDA(cudaMemcpyAsync(&total, row_off.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
-  DPB_CUDA(cudaMemcpyAsync(&mx, row_len.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
-  DPB_CUDA(cudaStreamSynchronize(stream));
-  n_entries = total;
-  max_row = mx;
-  keys.ensure(total + 1);
-  rev.ensure(total + 1);
-  eown.ensure(total + 1);
+  // Sizing. A synchronous build reads the total and the longest row back and sizes every
+  // per-entry buffer with slack; an asynchronous rebuild (MD) keeps the capacities and lets the
+  // kernels check them on the device (DEV_LIST_CAP / DEV_ROW_CAP), so the host never waits.
+  if (!async || e_cap == 0 || row_cap == 0) {
+    int64_t total = 0;
+    int mx = 0;
+    DPB_CUDA(cudaMemcpyAsync(&total, row_off.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+    DPB_CUDA(cudaMemcpyAsync(&mx, row_len.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    DPB_CUDA(cudaStreamSynchronize(stream));
+    n_entries = total;
+    max_row = mx;
+    if (total + 1 > e_cap) e_cap = total + total / 4 + 1024;
+    int rc = 2;
+    while (rc < mx + mx / 8) rc <<= 1;
+    if (rc > row_cap) row_cap = rc;
+  } else {
+    n_entries = -1; // known on the device only (row_off[n])
+  }
+  keys.ensure(e_cap + 1);
+  rev.ensure(e_cap + 1);
+  eown.ensure(e_cap + 1);
   k_nlist_pass<true><<<ceil_div(N, 128), 128, 0, stream>>>(p, pos4.p, frac.p, types.p, bin_of.p,
                                                            bin_start.p, bin_atoms.p, nullptr,
-                                                           row_off.p, keys.p, eown.p, err.p);
+                                                           row_off.p, keys.p, eown.p, err.p, e_cap);
   ++launches;
-  int cap = 2;
-  while (cap < mx) cap <<= 1;
+  const int cap = row_cap;
   if (cap > 8192) throw NumErr("neighbour row longer than 8192 entries");
   k_sort_rows<<<N, 256, cap * sizeof(uint64_t), stream>>>(N, row_off.p, keys.p, cap, err.p);
   ++launches;
@@ -309,6 +323,7 @@ void Engine::launch_nlist(double cutoff) {
 }
 
 void Engine::download_list(int64_t* offsets, int32_t* jout, int32_t* shift) {
+  sync_entry_count();
   std::vector<int64_t> off(n + 1);
   std::vector<uint64_t> k(n_entries);
   DPB_CUDA(cudaMemcpyAsync(off.data(), row_off.p, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
@@ -327,6 +342,12 @@ void Engine::download_list(int64_t* offsets, int32_t* jout, int32_t* shift) {
     }
   }
   offsets[n] = off[n];
+}
+
+void Engine::sync_entry_count() {
+  if (n_entries >= 0) return;
+  DPB_CUDA(cudaMemcpyAsync(&n_entries, row_off.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+  DPB_CUDA(cudaStreamSynchronize(stream));
 }
 
 } // namespace dpb

@@ -224,7 +224,7 @@ inline TabParams make_params(Engine& E) {
   p.Mp = E.Mp;
   p.mlt = E.mlt;
   p.K0p = E.K0p;
-  p.E = E.n_entries;
+  p.E = E.e_cap;   // SoA stride and grid bound; the live count is row_off[n]
   p.slot_of = E.slot_of.p;
   p.T = E.T.p;
   p.D = E.precision == 1 ? nullptr : E.D.p;
@@ -234,7 +234,7 @@ inline TabParams make_params(Engine& E) {
   p.counters = E.counters.p;
   p.err = E.err.p;
   int scap = 32;
-  while (scap < E.max_row) scap <<= 1;
+  while (scap < E.row_cap) scap <<= 1;
   p.scap = scap;
   return p;
 }

@@ -41,8 +41,9 @@ namespace {
 __global__ void __launch_bounds__(256) k_env_fwd(TabParams p) {
   const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   bool ext = false;
-  if (e < p.E && !p.center[p.eown[e]]) p.ebin[e] = -1;
-  if (e < p.E && p.center[p.eown[e]]) {
+  const bool live = e < p.E && e < p.row_off[p.n];
+  if (live && !p.center[p.eown[e]]) p.ebin[e] = -1;
+  if (live && p.center[p.eown[e]]) {
     const int i = p.eown[e];
     const uint64_t key = p.keys[e];
     int sh[3];
@@ -860,7 +861,7 @@ __global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double
 // ---------------------------------------------------------------- k_tab_bwd_g (thread per entry)
 __global__ void __launch_bounds__(256) k_tab_bwd_g(TabParams p) {
   const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (e >= p.E) return;
+  if (e >= p.E || e >= p.row_off[p.n]) return;
   const int bin = p.ebin[e];
   double* ge = p.g + 3 * e;
   if (bin < 0) {
@@ -1005,7 +1006,7 @@ void Engine::launch_env_exact() {
 }
 
 void Engine::grow_pbuf() {
-  const int64_t want = *h_gtotal + *h_gtotal / 4 + 1024;
+  const int64_t want = *h_gtotal + *h_gtotal / 2 + 1024;
   if (want > pbuf_cap) {
     Pbuf.ensure(static_cast<size_t>(want) * 24);
     pbuf_cap = want;
