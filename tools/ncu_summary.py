@@ -1,0 +1,21 @@
+"""Per-kernel summary of an ncu --set full report (tools helper): time, DRAM bytes, pipes, occupancy."""
+import csv, subprocess, sys
+rep, out = sys.argv[1], sys.argv[2]
+title = sys.argv[3] if len(sys.argv) > 3 else rep
+cols = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum',
+        'sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active',
+        'sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active',
+        'sm__warps_active.avg.pct_of_peak_sustained_active', 'smsp__issue_active.avg.pct_of_peak_sustained_active',
+        'launch__registers_per_thread', 'launch__grid_size', 'gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed']
+short = ['time_ms', 'dram_rd_MB', 'dram_wr_MB', 'fp64pipe%', 'tensor%', 'warps%', 'issue%', 'regs', 'grid', 'memthru%']
+txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(cols)],
+                     capture_output=True, text=True).stdout
+r = list(csv.reader(txt.splitlines()))
+h = r[0]
+lines = [f"# {title}", "%-34s " % "kernel" + " ".join("%11s" % s for s in short)]
+for x in r[2:]:
+    k = x[h.index('Kernel Name')].split('(')[0].replace('void ', '').replace('dpb::', '').replace('<unnamed>::', '')
+    k = k.replace('(anonymous namespace)::', '')[-34:]
+    lines.append("%-34s " % k + " ".join("%11s" % x[h.index(c)][:10] for c in cols))
+open(out, "w").write("\n".join(lines) + "\n")
+print("\n".join(lines))
