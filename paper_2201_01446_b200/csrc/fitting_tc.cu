@@ -196,10 +196,26 @@ __global__ void __launch_bounds__(192, 2) k_tc_gemm(const __grid_constant__ CUte
       tmem_wait_ld();
       if (staged) epi_bar();
       if (EPI == T_FWD) {
+        // gather phase first (all 16 table rows in flight), then the arithmetic: a per-element
+        // branchy lookup serialised the L1/L2 latency of every gather
+        double z[CW], c0v[CW], c1v[CW], c2v[CW];
 #pragma unroll
         for (int j = 0; j < CW; ++j) {
-          const double z = static_cast<double>(__uint_as_float(v[j])) + static_cast<double>(g.bias[col0 + j]);
-          const double td = tanh_tab(g.tanh_c, z);
+          z[j] = static_cast<double>(__uint_as_float(v[j])) + static_cast<double>(__ldg(g.bias + col0 + j));
+          const int k = min(static_cast<int>(fabs(z[j]) * 1024.0), 8191);
+          const double* qq = g.tanh_c + 3 * k;
+          c0v[j] = __ldg(qq);
+          c1v[j] = __ldg(qq + 1);
+          c2v[j] = __ldg(qq + 2);
+        }
+#pragma unroll
+        for (int j = 0; j < CW; ++j) {
+          // TanhTable::operator() (tanh_table.hpp:18-30)
+          const double ax = fabs(z[j]);
+          const int k = min(static_cast<int>(ax * 1024.0), 8191);
+          const double u = ax - k * (1.0 / 1024.0);
+          double td = ax > 8.0 ? 1.0 : c0v[j] + u * (c1v[j] + u * c2v[j]);
+          td = signbit(z[j]) ? -td : td;
           double y = td;
           if (g.xin2) y += static_cast<double>(sin0[r * SP + j]) + static_cast<double>(sin1[r * SP + j]);
           const float yf = static_cast<float>(y);
