@@ -63,18 +63,33 @@ __global__ void k_bin_fill(int n, const int* __restrict__ bin_of, const int* __r
   bin_atoms[bin_start[b] + atomicAdd(bin_fill + b, 1)] = i;
 }
 
-// One thread per centre. WRITE=false counts entries, WRITE=true emits unsorted keys.
+__device__ __forceinline__ int warp_excl_scan_nl(int v, int lane, int* total) {
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  *total = __shfl_sync(0xffffffffu, x, 31);
+  return x - v;
+}
+
+// Warp per centre (lanes over the candidates of each neighbouring bin): same acceptance rule,
+// image range and arithmetic as the reference's scan (one evaluation per pair from min(i, j)). Row order before the sort is
+// (bin, candidate, image) with lanes interleaved; rows are sorted afterwards, so the list is
+// identical. WRITE=false counts, WRITE=true emits keys at warp-scanned positions.
 template <bool WRITE>
-__global__ void k_nlist_pass(NlParams p, const double4* __restrict__ pos,
-                             const double* __restrict__ frac, const int32_t* __restrict__ types,
-                             const int* __restrict__ bin_of, const int* __restrict__ bin_start,
-                             const int* __restrict__ bin_atoms, int64_t* __restrict__ row_len,
-                             const int64_t* __restrict__ row_off, uint64_t* __restrict__ keys,
-                             int32_t* __restrict__ eown, int* err, int64_t e_cap) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(256) k_nlist_warp(NlParams p, const double4* __restrict__ pos,
+                                                    const double* __restrict__ frac, const int32_t* __restrict__ types,
+                                                    const int* __restrict__ bin_of, const int* __restrict__ bin_start,
+                                                    const int* __restrict__ bin_atoms, int64_t* __restrict__ row_len,
+                                                    const int64_t* __restrict__ row_off, uint64_t* __restrict__ keys,
+                                                    int32_t* __restrict__ eown, int* err, int64_t e_cap) {
+  const int lane = threadIdx.x & 31;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (i >= p.n) return;
-  if (WRITE && row_off[i + 1] > e_cap) { // asynchronous rebuild past the list capacity
-    raise_err(err, DEV_LIST_CAP);
+  if (WRITE && row_off[i + 1] > e_cap) {
+    if (lane == 0) raise_err(err, DEV_LIST_CAP);
     return;
   }
   const int bi = bin_of[i];
@@ -101,51 +116,96 @@ __global__ void k_nlist_pass(NlParams p, const double4* __restrict__ pos,
       for (int o2 = 0; o2 < cnt[2]; ++o2) {
         const int q2 = (first[2] + o2 + p.nb[2]) % p.nb[2];
         const int q = (q0 * p.nb[1] + q1) * p.nb[2] + q2;
-        const int qe = bin_start[q + 1];
-        for (int idx = bin_start[q]; idx < qe; ++idx) {
-          const int j = bin_atoms[idx];
-          const bool i_low = i <= j;
-          const int a = i_low ? i : j;
-          const int b = i_low ? j : i;
-          const double3 rj = ld_pos(pos, j);
-          const double3 ra = i_low ? ri : rj;
-          const double3 rb = i_low ? rj : ri;
-          int lo[3], hi[3];
+        const int qs = bin_start[q], qe = bin_start[q + 1];
+        for (int idx0 = qs; idx0 < qe; idx0 += 32) {
+          const int idx = idx0 + lane;
+          int mine = 0;
+          int j = 0, a = 0, b = 0, lo[3] = {0, 0, 0}, hi[3] = {-1, -1, -1};
+          bool i_low = true;
+          double3 ra, rb;
+          if (idx < qe) {
+            j = bin_atoms[idx];
+            i_low = i <= j;
+            a = i_low ? i : j;
+            b = i_low ? j : i;
+            const double3 rj = ld_pos(pos, j);
+            ra = i_low ? ri : rj;
+            rb = i_low ? rj : ri;
 #pragma unroll
-          for (int k = 0; k < 3; ++k) {
-            if (p.c.per[k]) {
-              const double fa = i_low ? fi[k] : frac[3 * a + k];
-              const double fb = i_low ? frac[3 * b + k] : fi[k];
-              const double df = __dsub_rn(fb, fa);
-              lo[k] = static_cast<int>(ceil(__dsub_rn(__dsub_rn(-df, p.margin[k]), 1e-12)));
-              hi[k] = static_cast<int>(floor(__dadd_rn(__dadd_rn(-df, p.margin[k]), 1e-12)));
-            } else {
-              lo[k] = hi[k] = 0;
+            for (int k = 0; k < 3; ++k) {
+              if (p.c.per[k]) {
+                const double fa = i_low ? fi[k] : frac[3 * a + k];
+                const double fb = i_low ? frac[3 * b + k] : fi[k];
+                const double df = __dsub_rn(fb, fa);
+                lo[k] = static_cast<int>(ceil(__dsub_rn(__dsub_rn(-df, p.margin[k]), 1e-12)));
+                hi[k] = static_cast<int>(floor(__dadd_rn(__dadd_rn(-df, p.margin[k]), 1e-12)));
+              } else {
+                lo[k] = hi[k] = 0;
+              }
             }
+            for (int s0 = lo[0]; s0 <= hi[0]; ++s0)
+              for (int s1 = lo[1]; s1 <= hi[1]; ++s1)
+                for (int s2 = lo[2]; s2 <= hi[2]; ++s2) {
+                  if (a == b && s0 == 0 && s1 == 0 && s2 == 0) continue;
+                  double d[3];
+                  disp_exact(p.c, ra, rb, s0, s1, s2, d);
+                  if (norm2_exact(d) <= p.cut2) ++mine;
+                }
           }
-          for (int s0 = lo[0]; s0 <= hi[0]; ++s0)
-            for (int s1 = lo[1]; s1 <= hi[1]; ++s1)
-              for (int s2 = lo[2]; s2 <= hi[2]; ++s2) {
-                if (a == b && s0 == 0 && s1 == 0 && s2 == 0) continue;
-                double d[3];
-                disp_exact(p.c, ra, rb, s0, s1, s2, d);
-                if (norm2_exact(d) <= p.cut2) {
-                  if (WRITE) {
-                    const int e0 = i_low ? s0 : -s0, e1 = i_low ? s1 : -s1,
-                              e2 = i_low ? s2 : -s2;
+          int tot;
+          const int ex = warp_excl_scan_nl(mine, lane, &tot);
+          if (WRITE && mine) {
+            int w = 0;
+            for (int s0 = lo[0]; s0 <= hi[0]; ++s0)
+              for (int s1 = lo[1]; s1 <= hi[1]; ++s1)
+                for (int s2 = lo[2]; s2 <= hi[2]; ++s2) {
+                  if (a == b && s0 == 0 && s1 == 0 && s2 == 0) continue;
+                  double d[3];
+                  disp_exact(p.c, ra, rb, s0, s1, s2, d);
+                  if (norm2_exact(d) <= p.cut2) {
+                    const int e0 = i_low ? s0 : -s0, e1 = i_low ? s1 : -s1, e2 = i_low ? s2 : -s2;
                     if (e0 < -511 || e0 > 511 || e1 < -511 || e1 > 511 || e2 < -511 || e2 > 511)
                       raise_err(err, DEV_SHIFT_RANGE);
-                    keys[base + count] = make_key(types[j], j, e0, e1, e2);
-                    eown[base + count] = i;
+                    const int64_t at = base + count + ex + w;
+                    keys[at] = make_key(types[j], j, e0, e1, e2);
+                    eown[at] = i;
+                    ++w;
                   }
-                  ++count;
                 }
-              }
+          }
+          count += tot;
         }
       }
     }
   }
-  if (!WRITE) row_len[i] = count;
+  if (!WRITE && lane == 0) row_len[i] = count;
+}
+
+// Reverse entry of every list entry (thread per entry): position of (j -> i, -s) in row j.
+__global__ void k_reverse_e(const int64_t* __restrict__ row_off, int n, const uint64_t* __restrict__ keys,
+                            const int32_t* __restrict__ eown, const int32_t* __restrict__ types,
+                            int32_t* __restrict__ rev, int* err, int64_t e_cap) {
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (e >= e_cap || e >= row_off[n]) return;
+  const int i = eown[e];
+  const uint64_t k = keys[e];
+  const int j = key_j(k);
+  const uint64_t want = reverse_key(k, types[i], i);
+  const int64_t r0 = row_off[j], r1 = row_off[j + 1];
+  int64_t lo = r0, hi = r1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (keys[mid] < want)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  if (lo >= r1 || keys[lo] != want) {
+    raise_err(err, DEV_ROW_CAP);
+    rev[e] = 0;
+  } else {
+    rev[e] = static_cast<int32_t>(lo - r0);
+  }
 }
 
 // One block per row: bitonic sort of the row's keys in shared memory.
@@ -182,33 +242,6 @@ __global__ void k_sort_rows(int n, const int64_t* __restrict__ row_off, uint64_t
     }
   }
   for (int t = threadIdx.x; t < len; t += blockDim.x) keys[off + t] = sk[t];
-}
-
-// Position of the reverse entry (j -> i, -s) in row j, by binary search in the sorted row.
-__global__ void k_reverse(int n, const int64_t* __restrict__ row_off, const uint64_t* __restrict__ keys,
-                          const int32_t* __restrict__ types, int32_t* __restrict__ rev, int* err) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int ti = types[i];
-  for (int64_t e = row_off[i]; e < row_off[i + 1]; ++e) {
-    const uint64_t k = keys[e];
-    const int j = key_j(k);
-    const uint64_t want = reverse_key(k, ti, i);
-    int64_t lo = row_off[j], hi = row_off[j + 1];
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (keys[mid] < want)
-        lo = mid + 1;
-      else
-        hi = mid;
-    }
-    if (lo >= row_off[j + 1] || keys[lo] != want) {
-      raise_err(err, DEV_ROW_CAP);
-      rev[e] = 0;
-    } else {
-      rev[e] = static_cast<int32_t>(lo - row_off[j]);
-    }
-  }
 }
 
 __global__ void k_max_len(int n, const int64_t* __restrict__ row_len, int* out) {
@@ -272,9 +305,8 @@ void Engine::launch_nlist(double cutoff, bool async) {
   DPB_CUDA(cudaMemsetAsync(bin_fill.p, 0, (nbins + 1) * sizeof(int), stream));
   k_bin_fill<<<ceil_div(N, 256), 256, 0, stream>>>(N, bin_of.p, bin_start.p, bin_fill.p, bin_atoms.p);
   ++launches;
-  k_nlist_pass<false><<<ceil_div(N, 128), 128, 0, stream>>>(p, pos4.p, frac.p, types.p, bin_of.p,
-                                                            bin_start.p, bin_atoms.p, lens.p,
-                                                            nullptr, nullptr, nullptr, err.p, 0);
+  k_nlist_warp<false><<<ceil_div(static_cast<int64_t>(N) * 32, 256), 256, 0, stream>>>(
+      p, pos4.p, frac.p, types.p, bin_of.p, bin_start.p, bin_atoms.p, lens.p, nullptr, nullptr, nullptr, err.p, 0);
   ++launches;
   DPB_CUDA(cudaMemsetAsync(lens.p + n, 0, sizeof(int64_t), stream));
   size_t tmp2 = 0;
@@ -306,15 +338,15 @@ void Engine::launch_nlist(double cutoff, bool async) {
   keys.ensure(e_cap + 1);
   rev.ensure(e_cap + 1);
   eown.ensure(e_cap + 1);
-  k_nlist_pass<true><<<ceil_div(N, 128), 128, 0, stream>>>(p, pos4.p, frac.p, types.p, bin_of.p,
-                                                           bin_start.p, bin_atoms.p, nullptr,
-                                                           row_off.p, keys.p, eown.p, err.p, e_cap);
+  k_nlist_warp<true><<<ceil_div(static_cast<int64_t>(N) * 32, 256), 256, 0, stream>>>(
+      p, pos4.p, frac.p, types.p, bin_of.p, bin_start.p, bin_atoms.p, nullptr, row_off.p, keys.p, eown.p, err.p,
+      e_cap);
   ++launches;
   const int cap = row_cap;
   if (cap > 8192) throw NumErr("neighbour row longer than 8192 entries");
   k_sort_rows<<<N, 256, cap * sizeof(uint64_t), stream>>>(N, row_off.p, keys.p, cap, err.p);
   ++launches;
-  k_reverse<<<ceil_div(N, 128), 128, 0, stream>>>(N, row_off.p, keys.p, types.p, rev.p, err.p);
+  k_reverse_e<<<ceil_div(e_cap, 256), 256, 0, stream>>>(row_off.p, N, keys.p, eown.p, types.p, rev.p, err.p, e_cap);
   ++launches;
   ref_pos.ensure(3 * n);
   DPB_CUDA(cudaMemcpyAsync(ref_pos.p, pos3.p, 3 * n * sizeof(double), cudaMemcpyDeviceToDevice, stream));
