@@ -19,6 +19,8 @@
 #include <cstdlib>
 #include <nccl.h>
 
+#include <cub/cub.cuh>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -54,6 +56,14 @@ struct Dist {
   std::vector<int64_t> soff, roff;
   DevBuf<int32_t> sidx, ridx;
   DevBuf<double> sbuf, rbuf, gbuf_send, gbuf_all;
+  // device-side repartition (every rebuild): global state, sort keys, owners, plans
+  DevBuf<double> d_gpos, d_gvel, d_fw, d_lohi, d_lpos, d_lvel;
+  DevBuf<int32_t> d_gtypes, d_owner, d_ids, d_ids2, d_flag, d_scan, d_lidx, d_lgid, d_slot, d_ltypes;
+  DevBuf<uint64_t> d_keys, d_keys2;
+  DevBuf<uint8_t> d_smask, d_lcenter;
+  DevBuf<int64_t> d_counts; // [0] n_local, [1 .. W] send counts, [W+1 .. 2W] recv counts
+  DevBuf<unsigned char> d_tmp;
+  bool host_global_valid = true; // gpos/gvel (host) reflect the last gather
 };
 
 namespace {
@@ -189,6 +199,266 @@ __global__ void k_pack_state(int64_t n, const uint8_t* __restrict__ center, cons
   }
 }
 
+
+__device__ __forceinline__ double circ_dist_d(double x, double lo, double hi, bool periodic) {
+  if (x >= lo && x <= hi) return 0.0;
+  const double d1 = (x < lo) ? lo - x : x - hi;
+  if (!periodic) return d1;
+  const double d2 = (x < lo) ? x + 1.0 - hi : lo + 1.0 - x;
+  return fmin(d1, d2);
+}
+
+__global__ void k_unpack_global(int64_t nrec, const double* __restrict__ all, double* __restrict__ gpos,
+                                double* __restrict__ gvel) {
+  const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (q >= nrec) return;
+  const double* o = all + 7 * q;
+  if (!(o[0] >= 0.0)) return;
+  const int64_t j = static_cast<int64_t>(o[0]);
+  for (int c = 0; c < 3; ++c) {
+    gpos[3 * j + c] = o[1 + c];
+    gvel[3 * j + c] = o[4 + c];
+  }
+}
+
+// Wrapped fractional coordinate along the slab axis (domain.cpp:38-45) and an order-preserving
+// integer key (stable radix sort over ids 0..N-1 = the reference's (fw, id) ordering).
+__global__ void k_fw_keys(int64_t N, const double* __restrict__ gpos, double h0, double h1, double h2, int per,
+                          double* __restrict__ fw, uint64_t* __restrict__ keys, int32_t* __restrict__ ids) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= N) return;
+  const double* r = gpos + 3 * i;
+  const double f = __dadd_rn(__dadd_rn(__dmul_rn(r[0], h0), __dmul_rn(r[1], h1)), __dmul_rn(r[2], h2));
+  const double w = per ? __dsub_rn(f, floor(f)) : f;
+  fw[i] = w;
+  uint64_t b = static_cast<uint64_t>(__double_as_longlong(w));
+  keys[i] = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+  ids[i] = static_cast<int32_t>(i);
+}
+
+// Equal-count chunks of the sorted order (domain.cpp:49-63): owner and [lo, hi] per worker.
+__global__ void k_owner(int64_t N, int W, const int32_t* __restrict__ sorted_ids, const double* __restrict__ fw,
+                        int32_t* __restrict__ owner, double* __restrict__ lohi) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (k >= N) return;
+  const int64_t base = N / W, extra = N % W;
+  const int64_t big = extra * (base + 1);
+  const int w = k < big ? static_cast<int>(k / (base + 1)) : static_cast<int>(extra + (k - big) / base);
+  const int64_t start = w < extra ? w * (base + 1) : big + (w - extra) * base;
+  const int64_t cnt = base + (w < extra ? 1 : 0);
+  const int id = sorted_ids[k];
+  owner[id] = w;
+  if (k == start) lohi[2 * w] = fw[id];
+  if (k == start + cnt - 1) lohi[2 * w + 1] = fw[id];
+}
+
+// Local membership (owned or ghost of rank r) and, per peer p, "I own it and p holds it as a
+// ghost" as a bit mask (domain.cpp:64-80 ghost rule).
+__global__ void k_flags(int64_t N, int r, int W, const int32_t* __restrict__ owner, const double* __restrict__ fw,
+                        const double* __restrict__ lohi, double mf, int per, int32_t* __restrict__ local,
+                        uint8_t* __restrict__ smask) {
+  const int64_t id = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (id >= N) return;
+  const int o = owner[id];
+  const double x = fw[id];
+  const bool own = o == r;
+  const bool ghost = !own && circ_dist_d(x, lohi[2 * r], lohi[2 * r + 1], per) <= mf;
+  local[id] = (own || ghost) ? 1 : 0;
+  uint8_t m = 0;
+  if (own)
+    for (int p = 0; p < W; ++p)
+      if (p != r && circ_dist_d(x, lohi[2 * p], lohi[2 * p + 1], per) <= mf) m |= static_cast<uint8_t>(1u << p);
+  smask[id] = m;
+}
+
+__global__ void k_local_index(int64_t N, const int32_t* __restrict__ local, const int32_t* __restrict__ scan,
+                              int32_t* __restrict__ lidx, int32_t* __restrict__ lgid, int64_t* __restrict__ counts) {
+  const int64_t id = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (id >= N) return;
+  if (local[id]) {
+    lidx[id] = scan[id];
+    lgid[scan[id]] = static_cast<int32_t>(id);
+  } else {
+    lidx[id] = -1;
+  }
+  if (id == N - 1) counts[0] = scan[id] + local[id];
+}
+
+// Flag of peer p: send (mode 0: owned, p holds it as a ghost) or recv (mode 1: my ghost owned by p).
+__global__ void k_peer_flag(int64_t N, int r, int p, int mode, const uint8_t* __restrict__ smask,
+                            const int32_t* __restrict__ local, const int32_t* __restrict__ owner,
+                            int32_t* __restrict__ flag) {
+  const int64_t id = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (id >= N) return;
+  flag[id] = mode == 0 ? ((smask[id] >> p) & 1) : ((local[id] && owner[id] == p && owner[id] != r) ? 1 : 0);
+}
+
+// Ascending-id compaction of the flagged local indices into dst (+ count into counts[slot]).
+__global__ void k_peer_scatter(int64_t N, const int32_t* __restrict__ flag, const int32_t* __restrict__ scan,
+                               const int32_t* __restrict__ lidx, int32_t* __restrict__ dst,
+                               int64_t* __restrict__ counts, int slot) {
+  const int64_t id = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (id >= N) return;
+  if (flag[id]) dst[scan[id]] = lidx[id];
+  if (id == N - 1) counts[slot] = scan[id] + flag[id];
+}
+
+__global__ void k_local_arrays(int64_t nl, int r, const int32_t* __restrict__ lgid, const double* __restrict__ gpos,
+                               const double* __restrict__ gvel, const int32_t* __restrict__ gtypes,
+                               const int32_t* __restrict__ owner, double* __restrict__ lp, double* __restrict__ lv,
+                               int32_t* __restrict__ lt, uint8_t* __restrict__ lc) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (k >= nl) return;
+  const int64_t j = lgid[k];
+  for (int c = 0; c < 3; ++c) {
+    lp[3 * k + c] = gpos[3 * j + c];
+    lv[3 * k + c] = gvel[3 * j + c];
+  }
+  lt[k] = gtypes[j];
+  lc[k] = owner[j] == r ? 1 : 0;
+}
+
+__global__ void k_slot_of_center(int64_t nl, const uint8_t* __restrict__ center, const int32_t* __restrict__ scan,
+                                 int32_t* __restrict__ slot) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (k < nl) slot[k] = center[k] ? scan[k] : -1;
+}
+
+__global__ void k_pack_state_d(int64_t n, const int32_t* __restrict__ slot, const int32_t* __restrict__ gid,
+                               const double* __restrict__ x, const double* __restrict__ v, double* __restrict__ out) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n || slot[i] < 0) return;
+  double* o = out + 7 * static_cast<int64_t>(slot[i]);
+  o[0] = static_cast<double>(gid[i]);
+  for (int c = 0; c < 3; ++c) {
+    o[1 + c] = x[3 * i + c];
+    o[4 + c] = v[3 * i + c];
+  }
+}
+
+__global__ void k_u8_to_i32(int64_t n, const uint8_t* __restrict__ a, int32_t* __restrict__ b) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (k < n) b[k] = a[k];
+}
+
+template <class T>
+void excl_scan(Dist& D, const T* in, T* out, int64_t n, cudaStream_t st) {
+  size_t b = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, b, in, out, n, st);
+  D.d_tmp.ensure(b + 1);
+  cub::DeviceScan::ExclusiveSum(D.d_tmp.p, b, in, out, n, st);
+}
+
+// The partition and exchange plan of this rank, computed on the device from d_gpos (identical
+// on every rank after the all-gather). Produces D.sidx / D.ridx (device), D.soff / D.roff and the
+// local arrays (host copies for set_config), with one small read-back of the counts.
+void device_plan(Engine& E, std::vector<double>& lp, std::vector<double>& lv, std::vector<int32_t>& lt,
+                 std::vector<uint8_t>& lc) {
+  Dist& D = *E.dist;
+  cudaStream_t st = E.stream;
+  const int64_t N = D.N;
+  const int W = static_cast<int>(std::min<int64_t>(D.world, N));
+  if (D.world > 8) throw InputErr("the device partition supports up to 8 ranks");
+  double hinv[9], vol;
+  host_cell(D.box, hinv, vol);
+  int ax = 0;
+  double best = -1.0;
+  for (int k = 0; k < 3; ++k) {
+    const double sp = spacing(D.box, vol, k);
+    if (sp > best) {
+      best = sp;
+      ax = k;
+    }
+  }
+  const int per = D.pbc[ax] != 0;
+  const double mf = D.margin / spacing(D.box, vol, ax);
+  D.d_fw.ensure(N);
+  D.d_keys.ensure(N);
+  D.d_keys2.ensure(N);
+  D.d_ids.ensure(N);
+  D.d_ids2.ensure(N);
+  D.d_owner.ensure(N);
+  D.d_lohi.ensure(2 * D.world);
+  D.d_flag.ensure(N);
+  D.d_scan.ensure(N);
+  D.d_lidx.ensure(N);
+  D.d_lgid.ensure(N);
+  D.d_smask.ensure(N);
+  D.d_counts.ensure(2 * D.world + 2);
+  const int nb = static_cast<int>(ceil_div(N, 256));
+  k_fw_keys<<<nb, 256, 0, st>>>(N, D.d_gpos.p, hinv[ax], hinv[3 + ax], hinv[6 + ax], per, D.d_fw.p, D.d_keys.p,
+                                D.d_ids.p);
+  size_t b = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, b, D.d_keys.p, D.d_keys2.p, D.d_ids.p, D.d_ids2.p, static_cast<int>(N), 0, 64,
+                                  st);
+  D.d_tmp.ensure(b + 1);
+  cub::DeviceRadixSort::SortPairs(D.d_tmp.p, b, D.d_keys.p, D.d_keys2.p, D.d_ids.p, D.d_ids2.p, static_cast<int>(N), 0,
+                                  64, st);
+  k_owner<<<nb, 256, 0, st>>>(N, W, D.d_ids2.p, D.d_fw.p, D.d_owner.p, D.d_lohi.p);
+  k_flags<<<nb, 256, 0, st>>>(N, D.rank, W, D.d_owner.p, D.d_fw.p, D.d_lohi.p, mf, per, D.d_flag.p, D.d_smask.p);
+  excl_scan(D, D.d_flag.p, D.d_scan.p, N, st);
+  k_local_index<<<nb, 256, 0, st>>>(N, D.d_flag.p, D.d_scan.p, D.d_lidx.p, D.d_lgid.p, D.d_counts.p);
+  // exchange lists per peer, ascending global id; staged at offset p * N, packed after the counts
+  D.sidx.ensure(static_cast<size_t>(N) * D.world + 1);
+  D.ridx.ensure(static_cast<size_t>(N) * D.world + 1);
+  DevBuf<int32_t>& pf = D.d_ids;  // reuse (free after the sort) as the per-peer flag
+  DevBuf<int32_t>& ps = D.d_ids2; // scan of the peer flag (the sorted ids are no longer needed)
+  for (int mode = 0; mode < 2; ++mode)
+    for (int p = 0; p < D.world; ++p) {
+      if (p == D.rank) {
+        DPB_CUDA(cudaMemsetAsync(D.d_counts.p + 1 + mode * D.world + p, 0, sizeof(int64_t), st));
+        continue;
+      }
+      k_peer_flag<<<nb, 256, 0, st>>>(N, D.rank, p, mode, D.d_smask.p, D.d_flag.p, D.d_owner.p, pf.p);
+      excl_scan(D, pf.p, ps.p, N, st);
+      int32_t* dst = (mode == 0 ? D.sidx.p : D.ridx.p) + static_cast<size_t>(p) * N;
+      k_peer_scatter<<<nb, 256, 0, st>>>(N, pf.p, ps.p, D.d_lidx.p, dst, D.d_counts.p, 1 + mode * D.world + p);
+    }
+  std::vector<int64_t> cnt(2 * D.world + 1);
+  DPB_CUDA(cudaMemcpyAsync(cnt.data(), D.d_counts.p, cnt.size() * 8, cudaMemcpyDeviceToHost, st));
+  DPB_CUDA(cudaStreamSynchronize(st));
+  const int64_t nl = cnt[0];
+  D.soff.assign(D.world + 1, 0);
+  D.roff.assign(D.world + 1, 0);
+  for (int p = 0; p < D.world; ++p) {
+    D.soff[p + 1] = D.soff[p] + cnt[1 + p];
+    D.roff[p + 1] = D.roff[p] + cnt[1 + D.world + p];
+  }
+  // pack the per-peer lists contiguously (device to device)
+  for (int mode = 0; mode < 2; ++mode) {
+    DevBuf<int32_t>& L = mode == 0 ? D.sidx : D.ridx;
+    const std::vector<int64_t>& off = mode == 0 ? D.soff : D.roff;
+    for (int p = 0; p < D.world; ++p) {
+      const int64_t c = off[p + 1] - off[p];
+      if (c && p > 0)
+        DPB_CUDA(cudaMemcpyAsync(L.p + off[p], L.p + static_cast<size_t>(p) * N, c * sizeof(int32_t),
+                                 cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  const size_t mx = std::max(D.soff[D.world], D.roff[D.world]) + 1;
+  D.sbuf.ensure(3 * mx);
+  D.rbuf.ensure(3 * mx);
+  // local arrays (owned + ghosts, ascending global id)
+  D.d_lpos.ensure(3 * nl + 3);
+  D.d_lvel.ensure(3 * nl + 3);
+  D.d_ltypes.ensure(nl + 1);
+  D.d_lcenter.ensure(nl + 1);
+  k_local_arrays<<<ceil_div(nl, 256), 256, 0, st>>>(nl, D.rank, D.d_lgid.p, D.d_gpos.p, D.d_gvel.p, D.d_gtypes.p,
+                                                    D.d_owner.p, D.d_lpos.p, D.d_lvel.p, D.d_ltypes.p, D.d_lcenter.p);
+  lp.resize(3 * nl);
+  lv.resize(3 * nl);
+  lt.resize(nl);
+  lc.resize(nl);
+  DPB_CUDA(cudaMemcpyAsync(lp.data(), D.d_lpos.p, 3 * nl * 8, cudaMemcpyDeviceToHost, st));
+  DPB_CUDA(cudaMemcpyAsync(lv.data(), D.d_lvel.p, 3 * nl * 8, cudaMemcpyDeviceToHost, st));
+  DPB_CUDA(cudaMemcpyAsync(lt.data(), D.d_ltypes.p, nl * 4, cudaMemcpyDeviceToHost, st));
+  DPB_CUDA(cudaMemcpyAsync(lc.data(), D.d_lcenter.p, nl, cudaMemcpyDeviceToHost, st));
+  DPB_CUDA(cudaStreamSynchronize(st));
+  D.lcenter.assign(lc.begin(), lc.end());
+  D.n_own = 0;
+  for (auto c : lc) D.n_own += c;
+}
+
 // Host plan of one rank: local atoms (owned + ghosts, ascending global id), centre mask and the
 // exchange lists (local indices) per peer: s = my owned atoms that peer p holds as ghosts,
 // rv = my ghosts owned by p, both ascending in global id.
@@ -236,53 +506,45 @@ void make_plan(const Dist& D, int r, Plan& P) {
 // Build the local system for this rank from the global state and upload it.
 void build_local(Engine& E) {
   static const bool trace = std::getenv("DPB_TRACE") != nullptr;
+  static const bool check = std::getenv("DPB_CHECK_PLAN") != nullptr;
   auto now = [&] {
     if (trace) cudaStreamSynchronize(E.stream);
     return std::chrono::steady_clock::now();
   };
   const auto t0 = now();
   Dist& D = *E.dist;
-  Plan P;
-  make_plan(D, D.rank, P);
-  const auto t1 = now();
-  D.lgid.swap(P.lgid);
-  D.lcenter.swap(P.lcenter);
-  D.soff = P.soff;
-  D.roff = P.roff;
-  const std::vector<int32_t>& s = P.s;
-  const std::vector<int32_t>& rv = P.rv;
-  const int64_t nl = static_cast<int64_t>(D.lgid.size());
-  D.n_own = 0;
-  for (auto c : D.lcenter) D.n_own += c;
-  D.sidx.ensure(s.size() + 1);
-  D.ridx.ensure(rv.size() + 1);
-  const size_t mx = std::max(s.size(), rv.size()) + 1;
-  D.sbuf.ensure(3 * mx);
-  D.rbuf.ensure(3 * mx);
-  if (!s.empty()) DPB_CUDA(cudaMemcpyAsync(D.sidx.p, s.data(), s.size() * 4, cudaMemcpyHostToDevice, E.stream));
-  if (!rv.empty()) DPB_CUDA(cudaMemcpyAsync(D.ridx.p, rv.data(), rv.size() * 4, cudaMemcpyHostToDevice, E.stream));
-  // local arrays
-  std::vector<double> lp(3 * nl), lv(3 * nl);
-  std::vector<int32_t> lt(nl);
-  for (int64_t k = 0; k < nl; ++k) {
-    const int64_t j = D.lgid[k];
-    for (int c = 0; c < 3; ++c) {
-      lp[3 * k + c] = D.gpos[3 * j + c];
-      lv[3 * k + c] = D.gvel[3 * j + c];
+  std::vector<double> lp, lv;
+  std::vector<int32_t> lt;
+  std::vector<uint8_t> lc;
+  device_plan(E, lp, lv, lt, lc);
+  const int64_t nl = static_cast<int64_t>(lt.size());
+  if (check) {
+    // the host restatement of partition_domain must agree entry by entry
+    if (!D.host_global_valid) {
+      D.gpos.resize(3 * D.N);
+      D.gvel.resize(3 * D.N);
+      DPB_CUDA(cudaMemcpy(D.gpos.data(), D.d_gpos.p, 3 * D.N * 8, cudaMemcpyDeviceToHost));
+      DPB_CUDA(cudaMemcpy(D.gvel.data(), D.d_gvel.p, 3 * D.N * 8, cudaMemcpyDeviceToHost));
+      D.host_global_valid = true;
     }
-    lt[k] = D.gtypes[j];
+    Plan P;
+    make_plan(D, D.rank, P);
+    std::vector<int32_t> s(D.soff[D.world]), rv(D.roff[D.world]);
+    if (!s.empty()) DPB_CUDA(cudaMemcpy(s.data(), D.sidx.p, s.size() * 4, cudaMemcpyDeviceToHost));
+    if (!rv.empty()) DPB_CUDA(cudaMemcpy(rv.data(), D.ridx.p, rv.size() * 4, cudaMemcpyDeviceToHost));
+    if (P.lcenter != lc || P.soff != D.soff || P.roff != D.roff || P.s != s || P.rv != rv)
+      throw CudaErr("device partition differs from the host restatement of partition_domain");
   }
+  const auto t1 = now();
+  E.set_config(nl, lp.data(), lt.data(), D.box, D.pbc, lc.data());
   const auto t2 = now();
-  E.set_config(nl, lp.data(), lt.data(), D.box, D.pbc, D.lcenter.data());
-  const auto t3 = now();
   E.md_upload_atoms(lv.data());
-  const auto t4 = now();
   E.build_list(E.r_cut + E.md.buffer);
-  const auto t5 = now();
+  const auto t3 = now();
   if (trace) {
     auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
-    std::fprintf(stderr, "[dpb rank %d] local: plan %.2f, arrays %.2f, set_config %.2f, upload %.2f, list %.2f ms\n",
-                 D.rank, ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4), ms(t4, t5));
+    std::fprintf(stderr, "[dpb rank %d] local: device plan %.2f, set_config %.2f, upload+list %.2f ms\n", D.rank,
+                 ms(t0, t1), ms(t1, t2), ms(t2, t3));
   }
 }
 
@@ -321,6 +583,17 @@ void dist_destroy(Engine& E) {
   E.dist->rbuf.release();
   E.dist->gbuf_send.release();
   E.dist->gbuf_all.release();
+  Dist& D = *E.dist;
+  for (auto* b : {&D.d_gpos, &D.d_gvel, &D.d_fw, &D.d_lohi, &D.d_lpos, &D.d_lvel}) b->release();
+  for (auto* b : {&D.d_gtypes, &D.d_owner, &D.d_ids, &D.d_ids2, &D.d_flag, &D.d_scan, &D.d_lidx, &D.d_lgid,
+                  &D.d_slot, &D.d_ltypes})
+    b->release();
+  D.d_keys.release();
+  D.d_keys2.release();
+  D.d_smask.release();
+  D.d_lcenter.release();
+  D.d_counts.release();
+  D.d_tmp.release();
   delete E.dist;
   E.dist = nullptr;
 }
@@ -345,6 +618,13 @@ void dist_md_begin(Engine& E, int64_t N, const double* pos, const double* vel, c
   std::memcpy(D.pbc, pbc, sizeof(D.pbc));
   D.margin = E.r_cut + cfg->buffer;
   D.max_own = N / std::min<int64_t>(D.world, N) + 1;
+  D.d_gpos.ensure(3 * N);
+  D.d_gvel.ensure(3 * N);
+  D.d_gtypes.ensure(N);
+  DPB_CUDA(cudaMemcpyAsync(D.d_gpos.p, pos, 3 * N * 8, cudaMemcpyHostToDevice, E.stream));
+  DPB_CUDA(cudaMemcpyAsync(D.d_gvel.p, vel, 3 * N * 8, cudaMemcpyHostToDevice, E.stream));
+  DPB_CUDA(cudaMemcpyAsync(D.d_gtypes.p, types, N * 4, cudaMemcpyHostToDevice, E.stream));
+  D.host_global_valid = true;
   E.md = *cfg;
   build_local(E);
 }
@@ -372,39 +652,28 @@ void dist_halo_reverse(Engine& E) {
   E.launches += 1 + D.world;
 }
 
-// All-gather of the owned (id, x, v) into the global arrays on every rank.
+// All-gather of the owned (id, x, v) into the global arrays on every rank (device resident).
 static void gather_global(Engine& E) {
   Dist& D = *E.dist;
   const int64_t nl = E.n;
-  std::vector<int64_t> slot(nl, 0);
-  int64_t k = 0;
-  for (int64_t i = 0; i < nl; ++i)
-    if (D.lcenter[i]) slot[i] = k++;
-  DevBuf<int64_t> dgid, dslot;
-  dgid.ensure(nl);
-  dslot.ensure(nl);
-  DPB_CUDA(cudaMemcpyAsync(dgid.p, D.lgid.data(), nl * 8, cudaMemcpyHostToDevice, E.stream));
-  DPB_CUDA(cudaMemcpyAsync(dslot.p, slot.data(), nl * 8, cudaMemcpyHostToDevice, E.stream));
+  D.d_slot.ensure(nl + 1);
+  D.d_flag.ensure(nl + 1);
+  // slot of each owned atom = its rank among the local centres (ascending global id)
+  DevBuf<int32_t>& cflag = D.d_ids;
+  cflag.ensure(nl + 1);
+  k_u8_to_i32<<<ceil_div(nl, 256), 256, 0, E.stream>>>(nl, E.center.p, cflag.p);
+  excl_scan(D, cflag.p, D.d_flag.p, nl, E.stream);
+  k_slot_of_center<<<ceil_div(nl, 256), 256, 0, E.stream>>>(nl, E.center.p, D.d_flag.p, D.d_slot.p);
   D.gbuf_send.ensure(7 * D.max_own);
   D.gbuf_all.ensure(7 * D.max_own * D.world);
   DPB_CUDA(cudaMemsetAsync(D.gbuf_send.p, 0xff, 7 * D.max_own * sizeof(double), E.stream)); // NaN ids
-  k_pack_state<<<ceil_div(nl, 256), 256, 0, E.stream>>>(nl, E.center.p, dgid.p, dslot.p, E.pos3.p,
-                                                        E.vel3.p, D.gbuf_send.p);
+  k_pack_state_d<<<ceil_div(nl, 256), 256, 0, E.stream>>>(nl, D.d_slot.p, D.d_lgid.p, E.pos3.p, E.vel3.p,
+                                                          D.gbuf_send.p);
   DPB_NCCL(ncclAllGather(D.gbuf_send.p, D.gbuf_all.p, 7 * D.max_own, ncclDouble, D.comm, E.stream));
-  std::vector<double> all(7 * D.max_own * D.world);
-  DPB_CUDA(cudaMemcpyAsync(all.data(), D.gbuf_all.p, all.size() * 8, cudaMemcpyDeviceToHost, E.stream));
-  DPB_CUDA(cudaStreamSynchronize(E.stream));
-  dgid.release();
-  dslot.release();
-  for (int64_t q = 0; q < D.max_own * D.world; ++q) {
-    const double* o = &all[7 * q];
-    if (!(o[0] >= 0.0)) continue;
-    const int64_t j = static_cast<int64_t>(o[0]);
-    for (int c = 0; c < 3; ++c) {
-      D.gpos[3 * j + c] = o[1 + c];
-      D.gvel[3 * j + c] = o[4 + c];
-    }
-  }
+  const int64_t nrec = D.max_own * D.world;
+  k_unpack_global<<<ceil_div(nrec, 256), 256, 0, E.stream>>>(nrec, D.gbuf_all.p, D.d_gpos.p, D.d_gvel.p);
+  E.launches += 5;
+  D.host_global_valid = false;
 }
 
 void dist_rebuild(Engine& E) {
@@ -427,8 +696,9 @@ void dist_rebuild(Engine& E) {
 void dist_md_end(Engine& E, double* gpos, double* gvel) {
   Dist& D = *E.dist;
   gather_global(E);
-  if (gpos) std::memcpy(gpos, D.gpos.data(), 3 * D.N * 8);
-  if (gvel) std::memcpy(gvel, D.gvel.data(), 3 * D.N * 8);
+  if (gpos) DPB_CUDA(cudaMemcpyAsync(gpos, D.d_gpos.p, 3 * D.N * 8, cudaMemcpyDeviceToHost, E.stream));
+  if (gvel) DPB_CUDA(cudaMemcpyAsync(gvel, D.d_gvel.p, 3 * D.N * 8, cudaMemcpyDeviceToHost, E.stream));
+  DPB_CUDA(cudaStreamSynchronize(E.stream));
   // counters summed over ranks, largest drift over ranks
   DPB_NCCL(ncclAllReduce(E.counters.p, E.counters.p, 3, ncclUint64, ncclSum, D.comm, E.stream));
   DPB_NCCL(ncclAllReduce(E.red.p + 11, E.red.p + 11, 1, ncclDouble, ncclMax, D.comm, E.stream));
