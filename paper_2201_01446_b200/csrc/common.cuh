@@ -93,6 +93,15 @@ __device__ __forceinline__ double3 ld_pos(const double4* p, int j) {
 
 __device__ __forceinline__ void raise_err(int* err, int code) { atomicCAS(err, 0, code); }
 
+// FP64 tanh without the branchy library path: t = (1 - e) / (1 + e), e = exp(-2|x|) in (0, 1],
+// sign restored. Absolute error <= ~2.5e-16 everywhere (the value is only ever used next to O(1)
+// terms: y = x + t, 1 - t^2), which keeps the FP64 path far inside its 1e-10 parity bar against
+// glibc's tanh; ~2x fewer instructions and no divergence between the |x| regimes.
+__device__ __forceinline__ double tanh_fp64(double x) {
+  const double e = exp(-2.0 * fabs(x));
+  return copysign(__ddiv_rn(1.0 - e, 1.0 + e), x);
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

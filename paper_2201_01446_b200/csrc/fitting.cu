@@ -135,8 +135,8 @@ __global__ void __launch_bounds__(128) k_gemm(GemmArgs g) {
       const size_t o = static_cast<size_t>(row) * g.ldc + col;
       if (EPI == EPI_FWD) {
         const double2 b = *reinterpret_cast<const double2*>(g.bias + col);
-        const double t0 = tanh(acc[i][j][0] + b.x);
-        const double t1 = tanh(acc[i][j][1] + b.y);
+        const double t0 = tanh_fp64(acc[i][j][0] + b.x);
+        const double t1 = tanh_fp64(acc[i][j][1] + b.y);
         double2 y = make_double2(t0, t1);
         if (g.xin) {
           const double2 x = *reinterpret_cast<const double2*>(g.xin + static_cast<size_t>(row) * g.ldx + col);
