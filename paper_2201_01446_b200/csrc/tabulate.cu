@@ -864,12 +864,7 @@ __global__ void __launch_bounds__(256) k_tab_bwd_g(TabParams p) {
   if (e >= p.E || e >= p.row_off[p.n]) return;
   const int bin = p.ebin[e];
   double* ge = p.g + 3 * e;
-  if (bin < 0) {
-    ge[0] = 0.0;
-    ge[1] = 0.0;
-    ge[2] = 0.0;
-    return;
-  }
+  if (bin < 0) return; // never read: k_forces gathers only real entries (own and reverse)
   const int i = p.eown[e];
   Env ev;
   env_of(p, ld_pos(p.pos, i), p.keys[e], ev);
