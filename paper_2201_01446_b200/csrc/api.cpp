@@ -67,8 +67,7 @@ int dp_compute(dp_handle* h, int64_t n, const double* pos, const int32_t* types,
     if (h->skin == 0.0) rebuild = true;
     if (rebuild) E.build_list(cutoff);
     E.reset_counters();
-    E.evaluate();
-    E.check_err();
+    E.evaluate_retry();
     E.fetch_results(energy, forces, virial, atom_energy);
     E.read_counters();
   });
@@ -139,8 +138,7 @@ int dp_rmse_sweep(dp_handle* h, int n_configs, const int64_t* n_atoms, const dou
         E.set_config(na, pos + 3 * at, types + at, boxes + 9 * c, pbcs + 3 * c);
         E.build_list(E.r_cut);
         E.reset_counters();
-        E.evaluate();
-        E.check_err();
+        E.evaluate_retry();
         E.fetch_results(&e, f.data(), vir.data(), nullptr);
         E.read_counters();
         const double de = ref_e[c] - e;

@@ -150,7 +150,13 @@ struct Engine {
   DevBuf<int64_t> goff;         // [n+1]
   DevBuf<double> Pbuf;          // [groups][24]
   int64_t pbuf_cap = 0;
-  int64_t* h_gtotal = nullptr;  // pinned: total groups of the last evaluation
+  int64_t* h_gtotal = nullptr;  // pinned: total groups per half of the last evaluation
+  int n_halves = 1;
+  DevBuf<int64_t> gtot;
+  DevBuf<unsigned char> scan_tmp2;
+  cudaStream_t st2 = nullptr; // second half of a pipelined evaluation
+  cudaEvent_t ev_split = nullptr, ev_join = nullptr;
+  bool pipeline = std::getenv("DPB_NO_PIPELINE") == nullptr;
   void grow_pbuf();
   DevBuf<int32_t> n_real;
   DevBuf<double> T;
@@ -221,6 +227,18 @@ struct Engine {
   // kernels (defined in the .cu files)
   void launch_nlist(double cutoff, bool async);
   void launch_tab_fwd();
+  void launch_env(cudaStream_t st);
+  void tab_fwd_range(int c, int64_t i0, int64_t i1, cudaStream_t st);
+  void tab_bwd_range(int c, int64_t i0, int64_t i1, cudaStream_t st);
+  void size_pbuf_if_needed();
+  void fitting_rows(int64_t r0, int64_t rows, cudaStream_t st); // FP64, single centre type
+  void fitting_type_rows(int t, int64_t r0, int64_t rows, cudaStream_t st);
+  void fitting_type_rows_mixed(int t, int64_t r0, int64_t rows, cudaStream_t st);
+  void finish_energy();
+  void fitting_rows_mixed(int64_t r0, int64_t rows, cudaStream_t st);
+  void evaluate_pipelined();
+  void evaluate_retry();
+  bool pipeline_ok() const;
   void launch_fitting();
   void launch_fitting_mixed();
   void set_embedding(const dp_embedding_desc* nets);

@@ -229,73 +229,81 @@ void scatter_energy(Engine& E) {
   ++E.launches;
 }
 
-void Engine::launch_fitting() {
+void Engine::fitting_type_rows(int t, int64_t r0_, int64_t rows_, cudaStream_t st) {
   const int L = static_cast<int>(layers.size());
   const int wpm = widthp_max;
-  for (int t = 0; t < n_types; ++t) {
-    const int rows = seg_rows[t];
-    if (rows == 0) continue;
-    const size_t r0 = static_cast<size_t>(seg_start[t]);
-    // forward
-    const double* x = D.p + r0 * K0p;
-    int ldx = K0p;
-    for (int k = 0; k < L; ++k) {
-      const FitLayer& fl = layers[k];
-      GemmArgs a{};
-      a.A = x;
-      a.lda = ldx;
-      a.Bt = fit_wt[t * L + k].p;
-      a.ldb = fl.inp;
-      a.K = fl.inp;
-      a.bias = fit_b[t * L + k].p;
-      a.xin = fl.shortcut ? x : nullptr;
-      a.ldx = ldx;
-      a.tout = act_t[k].p + r0 * wpm;
-      a.yout = act_y[k].p + r0 * wpm;
-      a.ldc = wpm;
-      run_gemm(EPI_FWD, a, rows, fl.outp, stream);
-      ++launches;
-      x = a.yout;
-      ldx = wpm;
-    }
-    // readout
-    const FitLayer& last = layers[L - 1];
-    double* dzc = dz.p + r0 * wpm;
-    double* dyc = dy.p + r0 * wpm;
-    double* dzn = dz2.p + r0 * wpm;
-    double* dyn = dy2.p + r0 * wpm;
-    k_readout<<<ceil_div(rows, 4), 128, 0, stream>>>(rows, wpm, last.out, act_y[L - 1].p + r0 * wpm,
-                                                     act_t[L - 1].p + r0 * wpm, fit_wout[t].p,
-                                                     b_out[t], e_slot.p + r0, dzc, dyc);
+  const int rows = static_cast<int>(rows_);
+  const size_t r0 = static_cast<size_t>(r0_);
+  // forward
+  const double* x = D.p + r0 * K0p;
+  int ldx = K0p;
+  for (int k = 0; k < L; ++k) {
+    const FitLayer& fl = layers[k];
+    GemmArgs a{};
+    a.A = x;
+    a.lda = ldx;
+    a.Bt = fit_wt[t * L + k].p;
+    a.ldb = fl.inp;
+    a.K = fl.inp;
+    a.bias = fit_b[t * L + k].p;
+    a.xin = fl.shortcut ? x : nullptr;
+    a.ldx = ldx;
+    a.tout = act_t[k].p + r0 * wpm;
+    a.yout = act_y[k].p + r0 * wpm;
+    a.ldc = wpm;
+    run_gemm(EPI_FWD, a, rows, fl.outp, st);
     ++launches;
-    // backward
-    for (int k = L - 1; k >= 0; --k) {
-      const FitLayer& fl = layers[k];
-      GemmArgs a{};
-      a.A = dzc;
-      a.lda = wpm;
-      a.Bt = fit_w[t * L + k].p; // W [inp][outp]: K = outp contiguous
-      a.ldb = fl.outp;
-      a.K = fl.outp;
-      a.dyin = fl.shortcut ? dyc : nullptr;
-      a.ldd = wpm;
-      if (k > 0) {
-        a.tprev = act_t[k - 1].p + r0 * wpm;
-        a.dyout = dyn;
-        a.dzout = dzn;
-        a.ldc = wpm;
-      } else {
-        a.tprev = nullptr;
-        a.dyout = dD.p + r0 * K0p;
-        a.dzout = nullptr;
-        a.ldc = K0p;
-      }
-      run_gemm(EPI_BWD, a, rows, fl.inp, stream);
-      ++launches;
-      std::swap(dzc, dzn);
-      std::swap(dyc, dyn);
-    }
+    x = a.yout;
+    ldx = wpm;
   }
+  // readout
+  const FitLayer& last = layers[L - 1];
+  double* dzc = dz.p + r0 * wpm;
+  double* dyc = dy.p + r0 * wpm;
+  double* dzn = dz2.p + r0 * wpm;
+  double* dyn = dy2.p + r0 * wpm;
+  k_readout<<<ceil_div(rows, 4), 128, 0, st>>>(rows, wpm, last.out, act_y[L - 1].p + r0 * wpm,
+                                                   act_t[L - 1].p + r0 * wpm, fit_wout[t].p,
+                                                   b_out[t], e_slot.p + r0, dzc, dyc);
+  ++launches;
+  // backward
+  for (int k = L - 1; k >= 0; --k) {
+    const FitLayer& fl = layers[k];
+    GemmArgs a{};
+    a.A = dzc;
+    a.lda = wpm;
+    a.Bt = fit_w[t * L + k].p; // W [inp][outp]: K = outp contiguous
+    a.ldb = fl.outp;
+    a.K = fl.outp;
+    a.dyin = fl.shortcut ? dyc : nullptr;
+    a.ldd = wpm;
+    if (k > 0) {
+      a.tprev = act_t[k - 1].p + r0 * wpm;
+      a.dyout = dyn;
+      a.dzout = dzn;
+      a.ldc = wpm;
+    } else {
+      a.tprev = nullptr;
+      a.dyout = dD.p + r0 * K0p;
+      a.dzout = nullptr;
+      a.ldc = K0p;
+    }
+    run_gemm(EPI_BWD, a, rows, fl.inp, st);
+    ++launches;
+    std::swap(dzc, dzn);
+    std::swap(dyc, dyn);
+  }
+}
+
+void Engine::fitting_rows(int64_t r0, int64_t rows, cudaStream_t st) { fitting_type_rows(0, r0, rows, st); }
+
+void Engine::launch_fitting() {
+  for (int t = 0; t < n_types; ++t)
+    if (seg_rows[t] > 0) fitting_type_rows(t, seg_start[t], seg_rows[t], stream);
+  finish_energy();
+}
+
+void Engine::finish_energy() {
   if (n_centers < n) DPB_CUDA(cudaMemsetAsync(e_atom.p, 0, n * sizeof(double), stream));
   scatter_energy(*this);
 }

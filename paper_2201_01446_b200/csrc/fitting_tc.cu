@@ -455,73 +455,76 @@ void Engine::ensure_mixed_buffers() {
   tc_dyb.ensure(static_cast<size_t>(n_slots) * wpm);
 }
 
-void Engine::launch_fitting_mixed() {
+void Engine::fitting_type_rows_mixed(int t, int64_t r0_, int64_t rows_, cudaStream_t st) {
   const int L = static_cast<int>(layers.size());
   const int wpm = widthp_max, s2 = seg32(wpm);
-  for (int t = 0; t < n_types; ++t) {
-    const int rows = seg_rows[t];
-    if (rows == 0) continue;
-    const size_t r0 = static_cast<size_t>(seg_start[t]);
-    // forward: layer 0 reads the split D (written by the tabulate kernel), layer k > 0 the split
-    // y_{k-1} (ping-pong), which is also the shortcut source
-    const float* A2 = tc_d2.p + r0 * 2 * K0p;
-    const float* yprev = nullptr;
-    for (int k = 0; k < L; ++k) {
-      const FitLayer& fl = layers[k];
-      TArgs g{};
-      g.kseg = k == 0 ? K0p : s2;
-      g.bias = tc_bias[t * L + k].p;
-      g.xin2 = fl.shortcut ? yprev : nullptr;
-      g.ldx = s2;
-      g.tout = tc_t[k].p + r0 * wpm;
-      g.ldc = wpm;
-      float* y2 = (k & 1 ? tc_y2b.p : tc_y2a.p) + r0 * 2 * s2;
-      g.y2 = y2;
-      g.ld2 = s2;
-      g.tanh_c = tc_tanh.p;
-      run_tc(T_FWD, A2, tc_wf[t * L + k].p, rows, fl.outp, g, stream);
-      ++launches;
-      yprev = y2;
-      A2 = y2;
-    }
-    // readout
-    const FitLayer& last = layers[L - 1];
-    float* dzc = tc_dz2a.p + r0 * 2 * s2;
-    float* dzn = tc_dz2b.p + r0 * 2 * s2;
-    float* dyc = tc_dya.p + r0 * wpm;
-    float* dyn = tc_dyb.p + r0 * wpm;
-    k_readout_tc<<<ceil_div(rows, 4), 128, 0, stream>>>(rows, wpm, s2, last.out, yprev, tc_t[L - 1].p + r0 * wpm,
-                                                        tc_wout[t].p, b_out[t], e_slot.p + r0, dzc);
+  const int rows = static_cast<int>(rows_);
+  const size_t r0 = static_cast<size_t>(r0_);
+  // forward: layer 0 reads the split D (written by the tabulate kernel), layer k > 0 the split
+  // y_{k-1} (ping-pong), which is also the shortcut source
+  const float* A2 = tc_d2.p + r0 * 2 * K0p;
+  const float* yprev = nullptr;
+  for (int k = 0; k < L; ++k) {
+    const FitLayer& fl = layers[k];
+    TArgs g{};
+    g.kseg = k == 0 ? K0p : s2;
+    g.bias = tc_bias[t * L + k].p;
+    g.xin2 = fl.shortcut ? yprev : nullptr;
+    g.ldx = s2;
+    g.tout = tc_t[k].p + r0 * wpm;
+    g.ldc = wpm;
+    float* y2 = (k & 1 ? tc_y2b.p : tc_y2a.p) + r0 * 2 * s2;
+    g.y2 = y2;
+    g.ld2 = s2;
+    g.tanh_c = tc_tanh.p;
+    run_tc(T_FWD, A2, tc_wf[t * L + k].p, rows, fl.outp, g, st);
     ++launches;
-    const float* dy_mat = nullptr;     // dy of the layer above (matrix), null at the top
-    const float* dy_vec = tc_wout[t].p; // dy_L = w_out for every row
-    for (int k = L - 1; k >= 0; --k) {
-      const FitLayer& fl = layers[k];
-      TArgs g{};
-      g.kseg = s2;
-      g.ldc = wpm;
-      g.ld2 = s2;
-      if (fl.shortcut) {
-        g.dyin = dy_mat;
-        g.dyvec = dy_mat ? nullptr : dy_vec;
-      }
-      if (k > 0) {
-        g.tprev = tc_t[k - 1].p + r0 * wpm;
-        g.dyout = dyn;
-        g.dz2 = dzn;
-      } else {
-        g.dD = dD.p + r0 * K0p;
-        g.ldD = K0p;
-      }
-      run_tc(T_BWD, dzc, tc_wb[t * L + k].p, rows, fl.inp, g, stream);
-      ++launches;
-      std::swap(dzc, dzn);
-      std::swap(dyc, dyn);
-      dy_mat = dyc;
-    }
+    yprev = y2;
+    A2 = y2;
   }
-  if (n_centers < n) DPB_CUDA(cudaMemsetAsync(e_atom.p, 0, n * sizeof(double), stream));
-  scatter_energy(*this);
+  // readout
+  const FitLayer& last = layers[L - 1];
+  float* dzc = tc_dz2a.p + r0 * 2 * s2;
+  float* dzn = tc_dz2b.p + r0 * 2 * s2;
+  float* dyc = tc_dya.p + r0 * wpm;
+  float* dyn = tc_dyb.p + r0 * wpm;
+  k_readout_tc<<<ceil_div(rows, 4), 128, 0, st>>>(rows, wpm, s2, last.out, yprev, tc_t[L - 1].p + r0 * wpm,
+                                                      tc_wout[t].p, b_out[t], e_slot.p + r0, dzc);
+  ++launches;
+  const float* dy_mat = nullptr;     // dy of the layer above (matrix), null at the top
+  const float* dy_vec = tc_wout[t].p; // dy_L = w_out for every row
+  for (int k = L - 1; k >= 0; --k) {
+    const FitLayer& fl = layers[k];
+    TArgs g{};
+    g.kseg = s2;
+    g.ldc = wpm;
+    g.ld2 = s2;
+    if (fl.shortcut) {
+      g.dyin = dy_mat;
+      g.dyvec = dy_mat ? nullptr : dy_vec;
+    }
+    if (k > 0) {
+      g.tprev = tc_t[k - 1].p + r0 * wpm;
+      g.dyout = dyn;
+      g.dz2 = dzn;
+    } else {
+      g.dD = dD.p + r0 * K0p;
+      g.ldD = K0p;
+    }
+    run_tc(T_BWD, dzc, tc_wb[t * L + k].p, rows, fl.inp, g, st);
+    ++launches;
+    std::swap(dzc, dzn);
+    std::swap(dyc, dyn);
+    dy_mat = dyc;
+  }
+}
+
+void Engine::fitting_rows_mixed(int64_t r0, int64_t rows, cudaStream_t st) { fitting_type_rows_mixed(0, r0, rows, st); }
+
+void Engine::launch_fitting_mixed() {
+  for (int t = 0; t < n_types; ++t)
+    if (seg_rows[t] > 0) fitting_type_rows_mixed(t, seg_start[t], seg_rows[t], stream);
+  finish_energy();
 }
 
 } // namespace dpb

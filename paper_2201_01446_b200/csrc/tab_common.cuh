@@ -32,6 +32,7 @@ struct TabParams {
   double x0, h, x_end;
   int tn;
   int n, n_types, M, Mp, mlt, K0p;
+  int i0, i1;           // centre range of this launch (pipelined halves); [0, n) otherwise
   int64_t E;
   const int32_t* slot_of;
   double* T;            // [n][4][Mp]
@@ -219,6 +220,8 @@ inline TabParams make_params(Engine& E) {
   p.x_end = E.tab_x0 + E.tab_h * static_cast<double>(E.tab_n);
   p.tn = static_cast<int>(E.tab_n);
   p.n = static_cast<int>(E.n);
+  p.i0 = 0;
+  p.i1 = static_cast<int>(E.n);
   p.n_types = E.n_types;
   p.M = E.M;
   p.Mp = E.Mp;

@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(64, 8) k_tab_fwd(TabParams p) {
   const FwdSmem w = carve_fwd(smem + wid * fwd_smem_bytes(p.scap, p.Mp), p.scap, p.Mp);
   const size_t istride = static_cast<size_t>(6) * p.Mp;
   const int f0 = F * lane;
-  for (int i = blockIdx.x * wpb + wid; i < p.n; i += gridDim.x * wpb) {
+  for (int i = p.i0 + blockIdx.x * wpb + wid; i < p.i1; i += gridDim.x * wpb) {
     const int64_t off = p.row_off[i];
     const int len = static_cast<int>(p.row_off[i + 1] - off);
     for (int t = lane; t < 64; t += 32) w.tc[t] = 0;
@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(256, 2) k_tab_dT(TabParams p, double* __restri
   double* ts = reinterpret_cast<double*>(smem) + wid * (4 * p.Mp + 4 * p.mlt);
   double* S = ts + 4 * p.Mp;
   const int f0 = F * lane;
-  for (int i = blockIdx.x * wpb + wid; i < p.n; i += gridDim.x * wpb) {
+  for (int i = p.i0 + blockIdx.x * wpb + wid; i < p.i1; i += gridDim.x * wpb) {
     double* out = dTg + static_cast<size_t>(i) * 4 * p.Mp;
     if (!p.center[i]) {
 #pragma unroll
@@ -538,10 +538,10 @@ __global__ void __launch_bounds__(64, 6) k_tab_bwd_P(TabParams p, const double* 
   const int wpb = blockDim.x >> 5;
   const size_t istride = static_cast<size_t>(6) * p.Mp;
   const int f0 = F * lane;
-  const int total = fb_list ? *fb_count * na : p.n;
+  const int total = fb_list ? *fb_count * na : p.i1 - p.i0;
   for (int idx = blockIdx.x * wpb + wid; idx < total; idx += gridDim.x * wpb) {
-    const int i = fb_list ? fb_list[idx / na] * na + idx % na : idx;
-    if (i >= p.n) continue;
+    const int i = fb_list ? fb_list[idx / na] + idx % na : p.i0 + idx; // fb_list holds block starts
+    if (i >= p.i1) continue;
     const int64_t off = p.row_off[i];
     const int nreal = p.n_real[i];
     int G = p.n_grp[i];
@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double
   int16_t* gidx = reinterpret_cast<int16_t*>(misc + 4);                  // [NA][UCAP] group of slot or -1
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gid = lane >> 2, tig = lane & 3;
-  const int nblk = (p.n + P2_NA - 1) / P2_NA;
+  const int nblk = (p.i1 - p.i0 + P2_NA - 1) / P2_NA;
   // output columns of this thread inside a chunk: c = 8 nt + 2 tig + h -> (slot c / 6, m = c % 6)
   int cslot[6], cm[6];
 #pragma unroll
@@ -659,12 +659,12 @@ __global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double
       cm[nt * 2 + h] = c % 6;
     }
   for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
-    const int i0 = blk * P2_NA;
+    const int i0 = p.i0 + blk * P2_NA;
     // dT rows of the 32 centres (contiguous in dTg)
     for (int q = tid; q < 4 * P2_NA * units; q += 256) {
       const int row = q / units, c2 = q % units;
       double* dst = dTs + row * pitch + 2 * c2;
-      if (i0 + (row >> 2) < p.n)
+      if (i0 + (row >> 2) < p.i1)
         tc::cp_async16(dst, dTg + (static_cast<size_t>(i0) * 4 + row) * Mp + 2 * c2);
       else
         dst[0] = dst[1] = 0.0;
@@ -678,7 +678,7 @@ __global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double
     for (int q = tid; q < P2_NA / 2 * P2_UW; q += 256) mtmask[q] = 0u;
     __syncthreads();
     // interval range of the block: each centre's group bins are sorted (gbin, written by k_tab_fwd)
-    if (tid < P2_NA && i0 + tid < p.n) {
+    if (tid < P2_NA && i0 + tid < p.i1) {
       const int i = i0 + tid;
       const int G = p.n_grp[i];
       if (G > 0) {
@@ -698,7 +698,7 @@ __global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double
     if (!wide) {
       for (int al = warp * 4; al < warp * 4 + 4; ++al) {
         const int i = i0 + al;
-        if (i >= p.n) break;
+        if (i >= p.i1) break;
         const int G = p.n_grp[i];
         const int32_t* gb = p.gbin + p.row_off[i];
         for (int g = lane; g < G; g += 32) {
@@ -741,7 +741,7 @@ __global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double
     __syncthreads();
     const int U = range == 0 ? 0 : misc[2];
     if (wide || U > P2_UCAP) {
-      if (tid == 0) fb_list[atomicAdd(fb_count, 1)] = blk;
+      if (tid == 0) fb_list[atomicAdd(fb_count, 1)] = i0;
       tc::cp_wait<0>();
       __syncthreads();
       continue;
@@ -749,7 +749,7 @@ __global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double
     // slot -> group of each centre, and the union each m-tile (2 centres) really needs
     for (int al = warp * 4; al < warp * 4 + 4; ++al) {
       const int i = i0 + al;
-      if (i >= p.n) break;
+      if (i >= p.i1) break;
       const int G = p.n_grp[i];
       const int32_t* gb = p.gbin + p.row_off[i];
       for (int g = lane; g < G; g += 32) {
@@ -769,7 +769,7 @@ __global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double
       r_al[mt] = r >> 2;
       r_a[mt] = r & 3;
       const int i = i0 + r_al[mt];
-      r_ok[mt] = i < p.n;
+      r_ok[mt] = i < p.i1;
       r_base[mt] = r_ok[mt] ? p.goff[i] : 0;
       if (r_ok[mt] && r_base[mt] + p.n_grp[i] > p.pcap) {
         if (r_a[mt] == 0 && tig == 0) raise_err(p.err, DEV_PBUF);
@@ -860,8 +860,10 @@ __global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double
 
 // ---------------------------------------------------------------- k_tab_bwd_g (thread per entry)
 __global__ void __launch_bounds__(256) k_tab_bwd_g(TabParams p) {
-  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (e >= p.E || e >= p.row_off[p.n]) return;
+  const int64_t eo = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t eb = p.row_off[p.i0];
+  const int64_t e = eb + eo;
+  if (e >= p.E || e >= p.row_off[p.i1]) return;
   const int bin = p.ebin[e];
   double* ge = p.g + 3 * e;
   if (bin < 0) return; // never read: k_forces gathers only real entries (own and reverse)
@@ -920,7 +922,7 @@ void launch_fwd_warp(const TabParams& p, cudaStream_t st, int sms) {
   if (bytes > 227 * 1024) throw NumErr("neighbour rows too long for the tabulate kernel");
   DPB_CUDA(cudaFuncSetAttribute(k_tab_fwd<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(bytes)));
-  const int blocks = std::max(1, std::min(ceil_div(p.n, 2), sms * 32));
+  const int blocks = std::max(1, std::min(ceil_div(p.i1 - p.i0, 2), sms * 32));
   k_tab_fwd<F><<<blocks, 64, bytes, st>>>(p);
   DPB_CUDA(cudaGetLastError());
 }
@@ -928,7 +930,7 @@ void launch_fwd_warp(const TabParams& p, cudaStream_t st, int sms) {
 template <int F>
 void launch_bwd_warp(const TabParams& p, const double* dTg, const int* fb_list, const int* fb_count, int na,
                      cudaStream_t st, int sms) {
-  const int blocks = fb_list ? sms * 8 : std::max(1, std::min(ceil_div(p.n, 2), sms * 32));
+  const int blocks = fb_list ? sms * 8 : std::max(1, std::min(ceil_div(p.i1 - p.i0, 2), sms * 32));
   k_tab_bwd_P<F><<<blocks, 64, 0, st>>>(p, dTg, fb_list, fb_count, na);
   DPB_CUDA(cudaGetLastError());
 }
@@ -937,57 +939,80 @@ template <int F>
 void launch_dT(const TabParams& p, double* dTg, cudaStream_t st, int sms) {
   const size_t bytes = 8 * (4 * static_cast<size_t>(p.Mp) + 4 * p.mlt) * sizeof(double);
   DPB_CUDA(cudaFuncSetAttribute(k_tab_dT<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
-  const int blocks = std::max(1, std::min(ceil_div(p.n, 8), sms * 8));
+  const int blocks = std::max(1, std::min(ceil_div(p.i1 - p.i0, 8), sms * 8));
   k_tab_dT<F><<<blocks, 256, bytes, st>>>(p, dTg);
   DPB_CUDA(cudaGetLastError());
 }
 
 } // namespace
 
-void Engine::launch_tab_fwd() {
+// Parameters of the centre range [i0, i1) of pipelined half c.
+TabParams chunk_params(Engine& E, int c, int64_t i0, int64_t i1) {
+  TabParams p = make_params(E);
+  p.i0 = static_cast<int>(i0);
+  p.i1 = static_cast<int>(i1);
+  p.Pbuf = E.Pbuf.p + static_cast<size_t>(c) * E.pbuf_cap * 24;
+  return p;
+}
+
+// Total groups of a centre range (for the Pbuf capacity of its half).
+__global__ void k_group_total(const int32_t* __restrict__ n_grp, const int64_t* __restrict__ goff, int i0, int i1,
+                              int64_t* __restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *out = i1 > i0 ? goff[i1 - 1] + n_grp[i1 - 1] : 0;
+}
+
+void Engine::launch_env(cudaStream_t st) {
   TabParams p = make_params(*this);
-  const int sms = sm_count(device);
   if (p.E > 0) {
-    k_env_fwd<<<ceil_div(p.E, 256), 256, 0, stream>>>(p);
+    k_env_fwd<<<ceil_div(p.E, 256), 256, 0, st>>>(p);
     ++launches;
   }
+}
+
+// k_tab_fwd over centres [i0, i1) of half c, then the group offsets of that half (goff[i0..i1)
+// start at 0; half c owns Pbuf[c * pbuf_cap ...]).
+void Engine::tab_fwd_range(int c, int64_t i0, int64_t i1, cudaStream_t st) {
+  TabParams p = chunk_params(*this, c, i0, i1);
+  const int sms = sm_count(device);
   switch (Mp / 32) {
-    case 1: launch_fwd_warp<1>(p, stream, sms); break;
-    case 2: launch_fwd_warp<2>(p, stream, sms); break;
-    case 3: launch_fwd_warp<3>(p, stream, sms); break;
-    case 4: launch_fwd_warp<4>(p, stream, sms); break;
-    case 5: launch_fwd_warp<5>(p, stream, sms); break;
-    case 6: launch_fwd_warp<6>(p, stream, sms); break;
-    case 7: launch_fwd_warp<7>(p, stream, sms); break;
-    case 8: launch_fwd_warp<8>(p, stream, sms); break;
+    case 1: launch_fwd_warp<1>(p, st, sms); break;
+    case 2: launch_fwd_warp<2>(p, st, sms); break;
+    case 3: launch_fwd_warp<3>(p, st, sms); break;
+    case 4: launch_fwd_warp<4>(p, st, sms); break;
+    case 5: launch_fwd_warp<5>(p, st, sms); break;
+    case 6: launch_fwd_warp<6>(p, st, sms); break;
+    case 7: launch_fwd_warp<7>(p, st, sms); break;
+    case 8: launch_fwd_warp<8>(p, st, sms); break;
     default: throw InputErr("feature width 4*d1 must be at most 256");
   }
   ++launches;
-  // group offsets for the backward projections; the total sizes Pbuf (one small sync per step)
-  DPB_CUDA(cudaMemsetAsync(n_grp.p + n, 0, sizeof(int32_t), stream));
+  DevBuf<unsigned char>& tmp = c == 0 ? scan_tmp : scan_tmp2;
+  const int cnt = static_cast<int>(i1 - i0);
   size_t tb = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tb, n_grp.p, goff.p, n + 1, stream);
-  scan_tmp.ensure(tb + 1);
-  cub::DeviceScan::ExclusiveSum(scan_tmp.p, tb, n_grp.p, goff.p, n + 1, stream);
-  ++launches;
-  // Pbuf capacity: sized with one sync on first use, re-checked at every list rebuild (which
-  // synchronises anyway); the backward kernel refuses to write past it (DEV_PBUF).
-  if (!h_gtotal) DPB_CUDA(cudaMallocHost(&h_gtotal, sizeof(int64_t)));
-  DPB_CUDA(cudaMemcpyAsync(h_gtotal, goff.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
-  if (pbuf_cap == 0 || !md_active) { // single evaluations size it exactly (they sync anyway)
-    static const bool trace = std::getenv("DPB_TRACE") != nullptr;
-    const auto t0 = std::chrono::steady_clock::now();
-    DPB_CUDA(cudaStreamSynchronize(stream));
-    const auto t1 = std::chrono::steady_clock::now();
-    grow_pbuf();
-    if (trace) {
-      DPB_CUDA(cudaStreamSynchronize(stream));
-      const auto t2 = std::chrono::steady_clock::now();
-      std::fprintf(stderr, "[dpb] pbuf sizing: wait %.2f ms, grow %.2f ms (cap %lld)\n",
-                   std::chrono::duration<double, std::milli>(t1 - t0).count(),
-                   std::chrono::duration<double, std::milli>(t2 - t1).count(), static_cast<long long>(pbuf_cap));
-    }
-  }
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, n_grp.p + i0, goff.p + i0, cnt, st);
+  tmp.ensure(tb + 1);
+  cub::DeviceScan::ExclusiveSum(tmp.p, tb, n_grp.p + i0, goff.p + i0, cnt, st);
+  gtot.ensure(4);
+  k_group_total<<<1, 32, 0, st>>>(n_grp.p, goff.p, static_cast<int>(i0), static_cast<int>(i1), gtot.p + c);
+  if (!h_gtotal) DPB_CUDA(cudaMallocHost(&h_gtotal, 4 * sizeof(int64_t)));
+  DPB_CUDA(cudaMemcpyAsync(h_gtotal + c, gtot.p + c, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  launches += 2;
+}
+
+void Engine::launch_tab_fwd() {
+  launch_env(stream);
+  tab_fwd_range(0, 0, n, stream);
+  n_halves = 1;
+  size_pbuf_if_needed();
+}
+
+// Pbuf capacity: exact (one sync) on the first evaluation of a system; afterwards the previous
+// totals + 50 % slack, grown at list rebuilds (MD) or by the retry of a single evaluation; the
+// backward kernels refuse to write past it (DEV_PBUF).
+void Engine::size_pbuf_if_needed() {
+  if (pbuf_cap != 0) return;
+  DPB_CUDA(cudaDeviceSynchronize());
+  grow_pbuf();
 }
 
 void Engine::launch_env_exact() {
@@ -1001,21 +1026,26 @@ void Engine::launch_env_exact() {
 }
 
 void Engine::grow_pbuf() {
-  const int64_t want = *h_gtotal + *h_gtotal / 2 + 1024;
+  if (!h_gtotal) return;
+  int64_t mx = 0;
+  for (int c = 0; c < n_halves; ++c) mx = std::max(mx, h_gtotal[c]);
+  const int64_t want = mx + mx / 2 + 1024;
   if (want > pbuf_cap) {
-    Pbuf.ensure(static_cast<size_t>(want) * 24);
+    Pbuf.ensure(static_cast<size_t>(want) * 24 * 2); // one region per pipelined half
     pbuf_cap = want;
   }
 }
 
-void Engine::launch_tab_bwd() {
-  TabParams p = make_params(*this);
+void Engine::tab_bwd_range(int c, int64_t i0, int64_t i1, cudaStream_t st) {
+  TabParams p = chunk_params(*this, c, i0, i1);
   const int sms = sm_count(device);
   dTbuf.ensure(static_cast<size_t>(n) * 4 * Mp);
-  const int nblk = ceil_div(static_cast<int64_t>(n), P2_NA);
-  fb_list.ensure(nblk + 1);
+  const int nblk_all = ceil_div(static_cast<int64_t>(n), P2_NA);
+  fb_list.ensure(2 * (nblk_all + 1));
+  int* fbl = fb_list.p + c * (nblk_all + 1);
+  const int nblk = ceil_div(i1 - i0, P2_NA);
   switch (Mp / 32) {
-#define DPB_DT(F) case F: launch_dT<F>(p, dTbuf.p, stream, sms); break;
+#define DPB_DT(F) case F: launch_dT<F>(p, dTbuf.p, st, sms); break;
     DPB_DT(1) DPB_DT(2) DPB_DT(3) DPB_DT(4) DPB_DT(5) DPB_DT(6) DPB_DT(7) DPB_DT(8)
 #undef DPB_DT
     default: throw InputErr("feature width 4*d1 must be at most 256");
@@ -1027,35 +1057,37 @@ void Engine::launch_tab_bwd() {
   if (tensor) {
     // 32-centre blocks on the FP64 tensor pipe; blocks with a too wide interval union are listed
     // and done by the per-warp kernel
-    DPB_CUDA(cudaMemsetAsync(fb_list.p + nblk, 0, sizeof(int), stream));
+    DPB_CUDA(cudaMemsetAsync(fbl + nblk_all, 0, sizeof(int), st));
     const size_t bytes = p2_smem_bytes(Mp);
     switch (Mp / 32) {
 #define DPB_P2(F)                                                                                             \
   case F:                                                                                                     \
     DPB_CUDA(cudaFuncSetAttribute(k_tab_bwd_P2<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
                                   static_cast<int>(bytes)));                                                  \
-    k_tab_bwd_P2<F><<<std::max(1, std::min(nblk, sms)), 256, bytes, stream>>>(p, dTbuf.p, fb_list.p,         \
-                                                                              fb_list.p + nblk);              \
+    k_tab_bwd_P2<F><<<std::max(1, std::min(nblk, sms)), 256, bytes, st>>>(p, dTbuf.p, fbl, fbl + nblk_all);   \
     break;
       DPB_P2(1) DPB_P2(2) DPB_P2(3) DPB_P2(4)
 #undef DPB_P2
     }
     DPB_CUDA(cudaGetLastError());
     ++launches;
-    fl = fb_list.p;
-    fc = fb_list.p + nblk;
+    fl = fbl;
+    fc = fbl + nblk_all;
   }
   switch (Mp / 32) {
-#define DPB_BW(F) case F: launch_bwd_warp<F>(p, dTbuf.p, fl, fc, P2_NA, stream, sms); break;
+#define DPB_BW(F) case F: launch_bwd_warp<F>(p, dTbuf.p, fl, fc, P2_NA, st, sms); break;
     DPB_BW(1) DPB_BW(2) DPB_BW(3) DPB_BW(4) DPB_BW(5) DPB_BW(6) DPB_BW(7) DPB_BW(8)
 #undef DPB_BW
     default: throw InputErr("feature width 4*d1 must be at most 256");
   }
   ++launches;
   if (p.E > 0) {
-    k_tab_bwd_g<<<ceil_div(p.E, 256), 256, 0, stream>>>(p);
+    k_tab_bwd_g<<<ceil_div(p.E, 256), 256, 0, st>>>(p);
     ++launches;
   }
 }
+
+void Engine::launch_tab_bwd() { tab_bwd_range(0, 0, n, stream); }
+
 
 } // namespace dpb
