@@ -202,6 +202,10 @@ int dp_dist_plan(int64_t n, const double* pos, const double* box, const uint8_t*
                  int64_t* send_off, int64_t* send_gid, int64_t* recv_off, int64_t* recv_gid);
 int dp_dist_init(dp_handle* h, int rank, int world, const void* nccl_id);
 
+/* Two-stream pipelined evaluation (FP64, one centre type; on by default). Phase times are only
+ * per-kernel-group meaningful with it off, which is how bench.py measures its roofline. */
+int dp_set_pipeline(dp_handle* h, int enable);
+
 /* cudaStream_t of the handle (for CUDA-event timing on the launching stream). */
 void* dp_stream(dp_handle* h);
 /* Number of kernels this handle has launched since creation. */

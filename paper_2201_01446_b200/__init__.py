@@ -162,6 +162,7 @@ def _lib():
         "dp_read_tables": ([C.c_char_p, D], I),
         "dp_tanh_table": ([D], I),
         "dp_set_embedding": ([P, C.POINTER(_EmbDesc)], I),
+        "dp_set_pipeline": ([P, I], I),
         "dp_write_model_json": ([C.c_char_p, C.POINTER(_Preset), D, C.c_char_p, C.c_char_p, U64], I),
         "dp_read_model_json": ([C.c_char_p, C.POINTER(_Preset), D, I64, C.c_char_p, I, C.c_char_p, I,
                                 C.POINTER(U64)], I),
@@ -641,6 +642,10 @@ class DeepPot:
         """Join a domain-decomposed run (one handle per GPU process)."""
         _check(_lib().dp_dist_init(self._h, rank, world, nccl_id), self._h)
         self._dist = True
+
+    def set_pipeline(self, enable: bool) -> None:
+        """Two-stream pipelined evaluation (on by default; FP64 single-type systems)."""
+        _check(_lib().dp_set_pipeline(self._h, 1 if enable else 0), self._h)
 
     def set_timing(self, enable: bool) -> None:
         _check(_lib().dp_set_timing(self._h, int(enable)), self._h)

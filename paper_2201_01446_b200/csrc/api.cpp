@@ -73,6 +73,12 @@ int dp_compute(dp_handle* h, int64_t n, const double* pos, const int32_t* types,
   });
 }
 
+int dp_set_pipeline(dp_handle* h, int enable) {
+  if (!h) return DP_INPUT_ERROR;
+  h->eng.pipeline = enable != 0;
+  return DP_OK;
+}
+
 int dp_set_embedding(dp_handle* h, const dp_embedding_desc* nets) {
   if (!h) return DP_INPUT_ERROR;
   return guard_call(&h->eng.last_error, [&] { h->eng.set_embedding(nets); });

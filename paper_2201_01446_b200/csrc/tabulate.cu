@@ -1027,9 +1027,11 @@ void Engine::launch_env_exact() {
 
 void Engine::grow_pbuf() {
   if (!h_gtotal) return;
-  int64_t mx = 0;
-  for (int c = 0; c < n_halves; ++c) mx = std::max(mx, h_gtotal[c]);
-  const int64_t want = mx + mx / 2 + 1024;
+  // every region is sized for the whole system's total, so switching between the pipelined
+  // halves and a single range never overflows
+  int64_t tot = 0;
+  for (int c = 0; c < n_halves; ++c) tot += h_gtotal[c];
+  const int64_t want = tot + tot / 2 + 1024;
   if (want > pbuf_cap) {
     Pbuf.ensure(static_cast<size_t>(want) * 24 * 2); // one region per pipelined half
     pbuf_cap = want;
