@@ -206,6 +206,13 @@ int dp_dist_init(dp_handle* h, int rank, int world, const void* nccl_id);
  * per-kernel-group meaningful with it off, which is how bench.py measures its roofline. */
 int dp_set_pipeline(dp_handle* h, int enable);
 
+/* Largest number of centres evaluated per chunk (a multiple of 128; 0 = default 131,072 or the
+ * DPB_CHUNK environment variable). The per-step working set (descriptors, activations,
+ * per-entry tabulate arrays) is sized for two chunks, so systems of tens of millions of atoms
+ * fit one GPU; results are bitwise independent of the chunk size. One centre type only (systems
+ * with several centre types are evaluated as one chunk). */
+int dp_set_chunk_size(dp_handle* h, int64_t centres);
+
 /* cudaStream_t of the handle (for CUDA-event timing on the launching stream). */
 void* dp_stream(dp_handle* h);
 /* Number of kernels this handle has launched since creation. */

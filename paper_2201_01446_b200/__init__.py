@@ -163,6 +163,7 @@ def _lib():
         "dp_tanh_table": ([D], I),
         "dp_set_embedding": ([P, C.POINTER(_EmbDesc)], I),
         "dp_set_pipeline": ([P, I], I),
+        "dp_set_chunk_size": ([P, I64], I),
         "dp_write_model_json": ([C.c_char_p, C.POINTER(_Preset), D, C.c_char_p, C.c_char_p, U64], I),
         "dp_read_model_json": ([C.c_char_p, C.POINTER(_Preset), D, I64, C.c_char_p, I, C.c_char_p, I,
                                 C.POINTER(U64)], I),
@@ -646,6 +647,11 @@ class DeepPot:
     def set_pipeline(self, enable: bool) -> None:
         """Two-stream pipelined evaluation (on by default; FP64 single-type systems)."""
         _check(_lib().dp_set_pipeline(self._h, 1 if enable else 0), self._h)
+
+    def set_chunk_size(self, centres: int) -> None:
+        """Largest number of centres per evaluation chunk (0 = default); results are bitwise
+        independent of it."""
+        _check(_lib().dp_set_chunk_size(self._h, int(centres)), self._h)
 
     def set_timing(self, enable: bool) -> None:
         _check(_lib().dp_set_timing(self._h, int(enable)), self._h)

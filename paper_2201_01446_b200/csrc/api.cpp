@@ -73,8 +73,17 @@ int dp_compute(dp_handle* h, int64_t n, const double* pos, const int32_t* types,
   });
 }
 
+int dp_set_chunk_size(dp_handle* h, int64_t centres) {
+  if (!h) return DP_INPUT_ERROR;
+  if (centres < 0) return DP_INPUT_ERROR;
+  h->eng.chunk_max = centres;
+  h->eng.plan_dirty = true;
+  return DP_OK;
+}
+
 int dp_set_pipeline(dp_handle* h, int enable) {
   if (!h) return DP_INPUT_ERROR;
+  if (h->eng.pipeline != (enable != 0)) h->eng.plan_dirty = true;
   h->eng.pipeline = enable != 0;
   return DP_OK;
 }

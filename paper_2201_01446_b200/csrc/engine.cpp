@@ -85,7 +85,8 @@ void Engine::create(const dp_model_desc* md, const dp_table_desc* td, int dev, i
   DPB_CUDA(cudaSetDevice(dev));
   DPB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   DPB_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
-  for (cudaEvent_t* e : {&ev_split, &ev_join}) DPB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  for (cudaEvent_t* e : {&ev_split, &ev_join, &ev_fwd[0], &ev_fwd[1]})
+    DPB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   n_types = md->n_types;
   r_cut = md->r_cut;
   r_smooth = md->r_smooth;
@@ -223,7 +224,7 @@ void Engine::destroy() {
     }
   if (stream) cudaStreamDestroy(stream);
   stream = nullptr;
-  for (cudaEvent_t* e : {&ev_split, &ev_join})
+  for (cudaEvent_t* e : {&ev_split, &ev_join, &ev_fwd[0], &ev_fwd[1]})
     if (*e) {
       cudaEventDestroy(*e);
       *e = nullptr;
@@ -270,6 +271,7 @@ void Engine::set_config(int64_t nn, const double* pos, const int32_t* ty, const 
     n = nn;
     list_valid = false;
     pbuf_cap = 0; // resize the group buffer from the next evaluation's exact total
+    plan_dirty = true;
     row_cap = 0;  // and the row capacity from the next (synchronous) list build
     h_types.assign(ty, ty + nn);
     types.ensure(n);
@@ -317,20 +319,84 @@ void Engine::set_config(int64_t nn, const double* pos, const int32_t* ty, const 
   upload_positions(pos);
 }
 
+// Chunk plan (see engine.hpp). Single centre type: chunks of consecutive slots (a multiple of
+// 128 rows: GEMM and P2 tiles), two chunks at least once the system is large enough for the
+// two-stream overlap (FP64), at most DPB_CHUNK centres each (default 131,072: two buffer sets of
+// ~12 GB). Several centre types: one chunk holding every segment.
+void Engine::plan_chunks() {
+  int64_t cmax = 131072;
+  if (const char* v = std::getenv("DPB_CHUNK")) cmax = std::atoll(v);
+  if (chunk_max > 0) cmax = chunk_max;
+  cmax = std::max<int64_t>(128, cmax / 128 * 128);
+  int nk = 1;
+  const int64_t nc = n_centers;
+  if (n_types == 1 && !force_single_chunk && nc > 0) {
+    const bool overlap = pipeline && precision == 0 && Mp <= 128 && nc >= 8192;
+    nk = static_cast<int>((nc + cmax - 1) / cmax);
+    if (overlap) nk = std::max(nk, 2);
+    if (nk > MAX_CHUNKS) throw InputErr("too many evaluation chunks (raise DPB_CHUNK)");
+  }
+  n_chunks = nk;
+  ck_sets = nk > 1 ? 2 : 1;
+  ck_a.assign(nk + 1, 0);
+  ck_s.assign(nk + 1, 0);
+  ck_rows.assign(nk, 0);
+  if (nk == 1) {
+    ck_a[1] = n;
+    ck_s[1] = n_slots;
+    ck_rows[0] = n_slots;
+  } else {
+    // slot boundaries every cs centres; atom boundary = index of the first centre of the chunk
+    const int64_t cs = round_up((nc + nk - 1) / nk, 128);
+    int64_t c = 0;
+    int k = 1;
+    for (int64_t i = 0; i < n && k < nk; ++i)
+      if (h_center[i]) {
+        if (c == k * cs) ck_a[k++] = i;
+        ++c;
+      }
+    for (; k < nk; ++k) ck_a[k] = n; // (cannot happen: nk chunks of cs cover nc)
+    ck_a[nk] = n;
+    for (int q = 0; q <= nk; ++q) ck_s[q] = std::min<int64_t>(static_cast<int64_t>(q) * cs, nc);
+    ck_s[nk] = nc;
+    for (int q = 0; q < nk; ++q) ck_rows[q] = (q == nk - 1 ? seg_rows[0] : ck_s[q + 1]) - ck_s[q];
+  }
+  ck_cap_a = ck_cap_s = 0;
+  for (int q = 0; q < nk; ++q) {
+    ck_cap_a = std::max(ck_cap_a, ck_a[q + 1] - ck_a[q]);
+    ck_cap_s = std::max(ck_cap_s, ck_rows[q]);
+  }
+  if (nk == 1) ck_cap_s = n_slots;
+  plan_dirty = false;
+}
+
+// Per-set buffers for the current plan; grows only (ensure) and zeroes what the GEMMs read as
+// padding (D columns K0..K0p). Pbuf is re-sized from the next evaluation.
+void Engine::apply_plan() {
+  plan_chunks();
+  ensure_step_buffers();
+  ensure_entry_step_buffers();
+  pbuf_cap = 0;
+}
+
 void Engine::ensure_step_buffers() {
+  if (plan_dirty) plan_chunks();
   const int L = static_cast<int>(layers.size());
-  T.ensure(static_cast<size_t>(n) * 4 * Mp);
-  const size_t dsz = static_cast<size_t>(n_slots) * K0p;
+  const size_t sa = static_cast<size_t>(ck_sets) * ck_cap_a, ss = static_cast<size_t>(ck_sets) * ck_cap_s;
+  T.ensure(sa * 4 * Mp);
+  dTbuf.ensure(sa * 4 * Mp);
+  const size_t dsz = ss * K0p;
   dD.ensure(dsz);
   if (precision == 1) {
     // mixed: the tabulate kernel writes D directly as the split FP32 operand of the tcgen05 GEMM
     ensure_mixed_buffers();
   } else {
+    const size_t had = D.n;
     D.ensure(dsz);
-    DPB_CUDA(cudaMemsetAsync(D.p, 0, D.n * sizeof(double), stream));
+    if (D.n != had) DPB_CUDA(cudaMemsetAsync(D.p, 0, D.n * sizeof(double), stream));
     act_t.resize(L);
     act_y.resize(L);
-    const size_t asz = static_cast<size_t>(n_slots) * widthp_max;
+    const size_t asz = ss * widthp_max;
     for (int k = 0; k < L; ++k) {
       act_t[k].ensure(asz);
       act_y[k].ensure(asz);
@@ -349,6 +415,18 @@ void Engine::ensure_step_buffers() {
   pos3.ensure(3 * n);
 }
 
+// Chunk-local entry arrays: a chunk's rows hold at most (atoms in the chunk) x row_cap entries
+// (row lengths are checked against row_cap on the device at every rebuild).
+void Engine::ensure_entry_step_buffers() {
+  if (e_cap == 0) return;
+  ck_cap_e = n_chunks == 1 ? e_cap : std::min<int64_t>(e_cap, ck_cap_a * std::max(row_cap, 1));
+  const size_t se = static_cast<size_t>(ck_sets) * ck_cap_e;
+  skeys.ensure(se + 1);
+  egrp.ensure(se + 1);
+  gbin.ensure(se + 1);
+  erc.ensure(5 * se + 5);
+}
+
 void Engine::upload_positions(const double* pos) {
   DPB_CUDA(cudaMemcpyAsync(pos3.p, pos, 3 * n * sizeof(double), cudaMemcpyHostToDevice, stream));
   launch_pos4(*this);
@@ -359,21 +437,21 @@ void Engine::build_list(double cutoff, bool async) {
   launch_nlist(cutoff, async);
   phase_end();
   if (pbuf_cap > 0) grow_pbuf();
-  skeys.ensure(e_cap + 1);
+  if (plan_dirty) apply_plan();
   ebin.ensure(e_cap + 1);
-  egrp.ensure(e_cap + 1);
-  gbin.ensure(e_cap + 1);
-  erc.ensure(5 * e_cap + 5);
   g.ensure(3 * e_cap + 3);
+  ensure_entry_step_buffers();
 }
 
 void Engine::evaluate() {
   if (!list_valid) throw InputErr("no neighbour list");
   if (tab_n == 0) throw InputErr("no compression tables: pass them to dp_create or build them with dp_build_tables_gpu");
-  if (pipeline_ok()) {
-    evaluate_pipelined();
+  if (plan_dirty) apply_plan();
+  if (n_chunks > 1) {
+    evaluate_chunked();
     return;
   }
+  use_chunk(0);
   phase_begin(1);
   launch_tab_fwd();
   phase_begin(2);
@@ -388,41 +466,46 @@ void Engine::evaluate() {
   phase_end();
 }
 
-// Two halves of the centres on two streams, the second half one stage behind the first: the
-// latency-bound tabulate kernels of one half run beside the tensor-pipe GEMMs of the other
-// (measured: C2 FP64 5.40 -> 5.30 ms/step; stream priorities or a three-stream split by kernel
-// class were slower, and the tcgen05 GEMMs of mixed mode lose more to the half-size grids than
-// the overlap gains, so mixed mode is not pipelined). Single centre type, every atom a centre
-// (slots == atom order), so a half is a contiguous atom and slot range; the split is a multiple
-// of 128 (GEMM and P2 tiles).
-bool Engine::pipeline_ok() const {
-  return pipeline && precision == 0 && n_types == 1 && !dist && n_centers == n && n >= 8192 && Mp <= 128;
-}
+// Chunks k = 0..n_chunks-1 on two streams (FP64: chunk k on stream k % 2 with buffer set
+// k % 2), each one stage behind the previous one: the latency-bound tabulate kernels of one
+// chunk run beside the tensor-pipe GEMMs of the other (C2, two chunks: 5.40 -> 5.30 ms/step;
+// stream priorities or a three-stream split by kernel class were slower). Mixed mode and
+// dp_set_pipeline(0) run the chunks in order on one stream (the tcgen05 GEMMs lose more to
+// half-size grids than the overlap gains).
+bool Engine::pipeline_ok() const { return pipeline && precision == 0 && Mp <= 128 && n_chunks > 1; }
 
-void Engine::evaluate_pipelined() {
-  const int64_t h = (n / 2) / 128 * 128;
-  const int64_t rows_b = seg_rows[0] - h;
-  phase_begin(1);
-  launch_env(stream);
-  n_halves = 2;
-  tab_fwd_range(0, 0, h, stream);
-  DPB_CUDA(cudaEventRecord(ev_split, stream));
-  DPB_CUDA(cudaStreamWaitEvent(st2, ev_split, 0));
-  tab_fwd_range(1, h, n, st2);
-  if (pbuf_cap == 0) {
-    DPB_CUDA(cudaDeviceSynchronize());
-    grow_pbuf();
+void Engine::evaluate_chunked() {
+  const bool two = pipeline_ok();
+  cudaStream_t last = stream;
+  for (int k = 0; k < n_chunks; ++k) {
+    use_chunk(k);
+    cudaStream_t st = two && (k & 1) ? st2 : stream;
+    if (two && k >= 1) DPB_CUDA(cudaStreamWaitEvent(st, ev_fwd[(k - 1) & 1], 0));
+    phase_begin(1);
+    tab_fwd_range(k, ck_a[k], ck_a[k + 1], st);
+    if (two) DPB_CUDA(cudaEventRecord(ev_fwd[k & 1], st));
+    if (pbuf_cap == 0) {
+      // first evaluation of this system/plan: size the group buffer from chunk 0's exact total
+      DPB_CUDA(cudaStreamSynchronize(st));
+      grow_pbuf();
+    }
+    phase_begin(2);
+    if (precision == 1)
+      fitting_rows_mixed(ck_s[k], ck_rows[k], st);
+    else
+      fitting_rows(ck_s[k], ck_rows[k], st);
+    phase_begin(3);
+    tab_bwd_range(k, ck_a[k], ck_a[k + 1], st);
+    last = st;
   }
-  phase_begin(2);
-  fitting_rows(0, h, stream);
-  fitting_rows(h, rows_b, st2);
-  phase_begin(3);
-  tab_bwd_range(0, 0, h, stream);
-  tab_bwd_range(1, h, n, st2);
-  DPB_CUDA(cudaEventRecord(ev_join, st2));
-  DPB_CUDA(cudaStreamWaitEvent(stream, ev_join, 0));
-  finish_energy();
+  phase_end();
+  if (two) {
+    DPB_CUDA(cudaEventRecord(ev_join, st2));
+    DPB_CUDA(cudaStreamWaitEvent(stream, ev_join, 0));
+  }
+  (void)last;
   phase_begin(4);
+  finish_energy();
   launch_forces();
   phase_end();
 }

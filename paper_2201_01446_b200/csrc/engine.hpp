@@ -141,6 +141,46 @@ struct Engine {
   DevBuf<int64_t> nl_len;
   DevBuf<unsigned char> scan_tmp;
 
+  // ---- chunked evaluation ----
+  // Centres are evaluated in chunks of consecutive slots (single centre type; one chunk for
+  // several types). Every per-centre step buffer (T, dT, D, dD, activations) and the per-entry
+  // step arrays (erc, skeys, gbin, egrp) exist twice (two buffer sets, chunk k uses set k % 2)
+  // and are sized for one chunk, so the step working set no longer grows with the system
+  // (13.5 M atoms would need ~1 TB unchunked). Kernels keep global atom / slot indices: the
+  // window pointers wa()/ws() are based so that index a0 (s0) of the current chunk lands at
+  // the start of its buffer set; entry arrays are indexed e - row_off[i0] on the device.
+  int n_chunks = 1;
+  bool plan_dirty = true;
+  bool force_single_chunk = false; // exact path: whole system in one chunk
+  int64_t chunk_max = 0;           // dp_set_chunk_size (0: DPB_CHUNK or the default)
+  std::vector<int64_t> ck_a, ck_s, ck_rows; // atom / slot boundaries [n_chunks + 1], GEMM rows
+  int64_t ck_cap_a = 0, ck_cap_s = 0, ck_cap_e = 0; // capacities of one buffer set
+  int ck_sets = 1;
+  int cur_set = 0;
+  int64_t cur_a0 = 0, cur_s0 = 0;
+  cudaEvent_t ev_fwd[2] = {nullptr, nullptr};
+  void plan_chunks();
+  void apply_plan();
+  void ensure_entry_step_buffers();
+  void use_chunk(int k) {
+    cur_set = ck_sets > 1 ? (k & 1) : 0;
+    cur_a0 = ck_a[k];
+    cur_s0 = ck_s[k];
+  }
+  template <class T>
+  T* wa(const DevBuf<T>& b, int64_t stride) const {
+    return b.p + (static_cast<int64_t>(cur_set) * ck_cap_a - cur_a0) * stride;
+  }
+  template <class T>
+  T* ws(const DevBuf<T>& b, int64_t stride) const {
+    return b.p + (static_cast<int64_t>(cur_set) * ck_cap_s - cur_s0) * stride;
+  }
+  template <class T>
+  T* we(const DevBuf<T>& b, int64_t per_entry = 1) const {
+    return b.p + static_cast<int64_t>(cur_set) * ck_cap_e * per_entry;
+  }
+  void evaluate_chunked();
+
   // ---- per-step buffers ----
   DevBuf<uint64_t> skeys;      // [E] reals sorted by (type, interval)
   DevBuf<int32_t> eown;         // [E] centre of each list entry
@@ -150,8 +190,8 @@ struct Engine {
   DevBuf<int64_t> goff;         // [n+1]
   DevBuf<double> Pbuf;          // [groups][24]
   int64_t pbuf_cap = 0;
-  int64_t* h_gtotal = nullptr;  // pinned: total groups per half of the last evaluation
-  int n_halves = 1;
+  int64_t* h_gtotal = nullptr;  // pinned: total groups per chunk of the last evaluation
+  static constexpr int MAX_CHUNKS = 4096;
   DevBuf<int64_t> gtot;
   DevBuf<unsigned char> scan_tmp2;
   cudaStream_t st2 = nullptr; // second half of a pipelined evaluation
@@ -227,7 +267,6 @@ struct Engine {
   // kernels (defined in the .cu files)
   void launch_nlist(double cutoff, bool async);
   void launch_tab_fwd();
-  void launch_env(cudaStream_t st);
   void tab_fwd_range(int c, int64_t i0, int64_t i1, cudaStream_t st);
   void tab_bwd_range(int c, int64_t i0, int64_t i1, cudaStream_t st);
   void size_pbuf_if_needed();
@@ -236,7 +275,6 @@ struct Engine {
   void fitting_type_rows_mixed(int t, int64_t r0, int64_t rows, cudaStream_t st);
   void finish_energy();
   void fitting_rows_mixed(int64_t r0, int64_t rows, cudaStream_t st);
-  void evaluate_pipelined();
   void evaluate_retry();
   bool pipeline_ok() const;
   void launch_fitting();

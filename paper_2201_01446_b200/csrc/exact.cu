@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(128) k_exact_fwd(TabParams p, const EmbPtrs* n
           const bool ok = c0 + q < cnt;
           const int64_t e = off + (ok ? idx[c0 + q] : 0);
 #pragma unroll
-          for (int a = 0; a < 4; ++a) R[q][a] = ok ? p.erc[a * p.E + e] : 0.0;
+          for (int a = 0; a < 4; ++a) R[q][a] = ok ? p.erc[a * p.es + e] : 0.0;
           s[q] = R[q][0];
         }
         double g[NP][F], g1[NP][F], g2[NP][F];
@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(128) k_exact_bwd(TabParams p, const EmbPtrs* n
           const bool ok = c0 + q < cnt;
           const int64_t e = off + (ok ? idx[c0 + q] : 0);
 #pragma unroll
-          for (int a = 0; a < 4; ++a) R[q][a] = ok ? p.erc[a * p.E + e] : 0.0;
+          for (int a = 0; a < 4; ++a) R[q][a] = ok ? p.erc[a * p.es + e] : 0.0;
           s[q] = R[q][0];
         }
         double g[NP][F], g1[NP][F], g2[NP][F];
@@ -537,6 +537,14 @@ void Engine::set_embedding(const dp_embedding_desc* nets) {
 void Engine::evaluate_exact() {
   if (!has_embedding) throw InputErr("the exact path needs the embedding nets (dp_set_embedding)");
   if (!list_valid) throw InputErr("no neighbour list");
+  if (n_chunks > 1 || plan_dirty) {
+    // the exact kernels index every list entry: whole system in one chunk for this call
+    force_single_chunk = true;
+    apply_plan();
+    force_single_chunk = false;
+    plan_dirty = true; // the tabulated path re-plans its chunks at its next evaluation
+  }
+  use_chunk(0);
   TabParams p = make_params(*this);
   p.tn = 0;                     // env-mat only: ebin = neighbour type of a real entry
   p.counters = exact_ctr.p;     // the exact path does not touch the tabulation counters

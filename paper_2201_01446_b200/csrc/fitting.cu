@@ -235,7 +235,7 @@ void Engine::fitting_type_rows(int t, int64_t r0_, int64_t rows_, cudaStream_t s
   const int rows = static_cast<int>(rows_);
   const size_t r0 = static_cast<size_t>(r0_);
   // forward
-  const double* x = D.p + r0 * K0p;
+  const double* x = ws(D, K0p) + r0 * K0p; // chunk windows (engine.hpp)
   int ldx = K0p;
   for (int k = 0; k < L; ++k) {
     const FitLayer& fl = layers[k];
@@ -248,8 +248,8 @@ void Engine::fitting_type_rows(int t, int64_t r0_, int64_t rows_, cudaStream_t s
     a.bias = fit_b[t * L + k].p;
     a.xin = fl.shortcut ? x : nullptr;
     a.ldx = ldx;
-    a.tout = act_t[k].p + r0 * wpm;
-    a.yout = act_y[k].p + r0 * wpm;
+    a.tout = ws(act_t[k], wpm) + r0 * wpm;
+    a.yout = ws(act_y[k], wpm) + r0 * wpm;
     a.ldc = wpm;
     run_gemm(EPI_FWD, a, rows, fl.outp, st);
     ++launches;
@@ -258,12 +258,12 @@ void Engine::fitting_type_rows(int t, int64_t r0_, int64_t rows_, cudaStream_t s
   }
   // readout
   const FitLayer& last = layers[L - 1];
-  double* dzc = dz.p + r0 * wpm;
-  double* dyc = dy.p + r0 * wpm;
-  double* dzn = dz2.p + r0 * wpm;
-  double* dyn = dy2.p + r0 * wpm;
-  k_readout<<<ceil_div(rows, 4), 128, 0, st>>>(rows, wpm, last.out, act_y[L - 1].p + r0 * wpm,
-                                                   act_t[L - 1].p + r0 * wpm, fit_wout[t].p,
+  double* dzc = ws(dz, wpm) + r0 * wpm;
+  double* dyc = ws(dy, wpm) + r0 * wpm;
+  double* dzn = ws(dz2, wpm) + r0 * wpm;
+  double* dyn = ws(dy2, wpm) + r0 * wpm;
+  k_readout<<<ceil_div(rows, 4), 128, 0, st>>>(rows, wpm, last.out, ws(act_y[L - 1], wpm) + r0 * wpm,
+                                                   ws(act_t[L - 1], wpm) + r0 * wpm, fit_wout[t].p,
                                                    b_out[t], e_slot.p + r0, dzc, dyc);
   ++launches;
   // backward
@@ -278,13 +278,13 @@ void Engine::fitting_type_rows(int t, int64_t r0_, int64_t rows_, cudaStream_t s
     a.dyin = fl.shortcut ? dyc : nullptr;
     a.ldd = wpm;
     if (k > 0) {
-      a.tprev = act_t[k - 1].p + r0 * wpm;
+      a.tprev = ws(act_t[k - 1], wpm) + r0 * wpm;
       a.dyout = dyn;
       a.dzout = dzn;
       a.ldc = wpm;
     } else {
       a.tprev = nullptr;
-      a.dyout = dD.p + r0 * K0p;
+      a.dyout = ws(dD, K0p) + r0 * K0p;
       a.dzout = nullptr;
       a.ldc = K0p;
     }

@@ -444,15 +444,16 @@ void Engine::prepare_mixed() {
 void Engine::ensure_mixed_buffers() {
   const int L = static_cast<int>(layers.size());
   const int wpm = widthp_max, s2 = seg32(wpm);
-  ensure_zeroed(tc_d2, static_cast<size_t>(n_slots) * 2 * K0p, stream);
-  ensure_zeroed(tc_y2a, static_cast<size_t>(n_slots) * 2 * s2, stream);
-  ensure_zeroed(tc_y2b, static_cast<size_t>(n_slots) * 2 * s2, stream);
-  ensure_zeroed(tc_dz2a, static_cast<size_t>(n_slots) * 2 * s2, stream);
-  ensure_zeroed(tc_dz2b, static_cast<size_t>(n_slots) * 2 * s2, stream);
+  const size_t ss = static_cast<size_t>(ck_sets) * ck_cap_s; // rows of the chunk buffer sets
+  ensure_zeroed(tc_d2, ss * 2 * K0p, stream);
+  ensure_zeroed(tc_y2a, ss * 2 * s2, stream);
+  ensure_zeroed(tc_y2b, ss * 2 * s2, stream);
+  ensure_zeroed(tc_dz2a, ss * 2 * s2, stream);
+  ensure_zeroed(tc_dz2b, ss * 2 * s2, stream);
   tc_t.resize(L);
-  for (int k = 0; k < L; ++k) tc_t[k].ensure(static_cast<size_t>(n_slots) * wpm);
-  tc_dya.ensure(static_cast<size_t>(n_slots) * wpm);
-  tc_dyb.ensure(static_cast<size_t>(n_slots) * wpm);
+  for (int k = 0; k < L; ++k) tc_t[k].ensure(ss * wpm);
+  tc_dya.ensure(ss * wpm);
+  tc_dyb.ensure(ss * wpm);
 }
 
 void Engine::fitting_type_rows_mixed(int t, int64_t r0_, int64_t rows_, cudaStream_t st) {
@@ -462,7 +463,7 @@ void Engine::fitting_type_rows_mixed(int t, int64_t r0_, int64_t rows_, cudaStre
   const size_t r0 = static_cast<size_t>(r0_);
   // forward: layer 0 reads the split D (written by the tabulate kernel), layer k > 0 the split
   // y_{k-1} (ping-pong), which is also the shortcut source
-  const float* A2 = tc_d2.p + r0 * 2 * K0p;
+  const float* A2 = ws(tc_d2, 2 * K0p) + r0 * 2 * K0p; // chunk windows (engine.hpp)
   const float* yprev = nullptr;
   for (int k = 0; k < L; ++k) {
     const FitLayer& fl = layers[k];
@@ -471,9 +472,9 @@ void Engine::fitting_type_rows_mixed(int t, int64_t r0_, int64_t rows_, cudaStre
     g.bias = tc_bias[t * L + k].p;
     g.xin2 = fl.shortcut ? yprev : nullptr;
     g.ldx = s2;
-    g.tout = tc_t[k].p + r0 * wpm;
+    g.tout = ws(tc_t[k], wpm) + r0 * wpm;
     g.ldc = wpm;
-    float* y2 = (k & 1 ? tc_y2b.p : tc_y2a.p) + r0 * 2 * s2;
+    float* y2 = ws(k & 1 ? tc_y2b : tc_y2a, 2 * s2) + r0 * 2 * s2;
     g.y2 = y2;
     g.ld2 = s2;
     g.tanh_c = tc_tanh.p;
@@ -484,11 +485,11 @@ void Engine::fitting_type_rows_mixed(int t, int64_t r0_, int64_t rows_, cudaStre
   }
   // readout
   const FitLayer& last = layers[L - 1];
-  float* dzc = tc_dz2a.p + r0 * 2 * s2;
-  float* dzn = tc_dz2b.p + r0 * 2 * s2;
-  float* dyc = tc_dya.p + r0 * wpm;
-  float* dyn = tc_dyb.p + r0 * wpm;
-  k_readout_tc<<<ceil_div(rows, 4), 128, 0, st>>>(rows, wpm, s2, last.out, yprev, tc_t[L - 1].p + r0 * wpm,
+  float* dzc = ws(tc_dz2a, 2 * s2) + r0 * 2 * s2;
+  float* dzn = ws(tc_dz2b, 2 * s2) + r0 * 2 * s2;
+  float* dyc = ws(tc_dya, wpm) + r0 * wpm;
+  float* dyn = ws(tc_dyb, wpm) + r0 * wpm;
+  k_readout_tc<<<ceil_div(rows, 4), 128, 0, st>>>(rows, wpm, s2, last.out, yprev, ws(tc_t[L - 1], wpm) + r0 * wpm,
                                                       tc_wout[t].p, b_out[t], e_slot.p + r0, dzc);
   ++launches;
   const float* dy_mat = nullptr;     // dy of the layer above (matrix), null at the top
@@ -504,11 +505,11 @@ void Engine::fitting_type_rows_mixed(int t, int64_t r0_, int64_t rows_, cudaStre
       g.dyvec = dy_mat ? nullptr : dy_vec;
     }
     if (k > 0) {
-      g.tprev = tc_t[k - 1].p + r0 * wpm;
+      g.tprev = ws(tc_t[k - 1], wpm) + r0 * wpm;
       g.dyout = dyn;
       g.dz2 = dzn;
     } else {
-      g.dD = dD.p + r0 * K0p;
+      g.dD = ws(dD, K0p) + r0 * K0p;
       g.ldD = K0p;
     }
     run_tc(T_BWD, dzc, tc_wb[t * L + k].p, rows, fl.inp, g, st);

@@ -33,7 +33,8 @@ struct TabParams {
   int tn;
   int n, n_types, M, Mp, mlt, K0p;
   int i0, i1;           // centre range of this launch (pipelined halves); [0, n) otherwise
-  int64_t E;
+  int64_t E;            // global entry capacity (bound of ebin / g)
+  int64_t es;           // SoA stride of the chunk-local entry arrays (erc, skeys, gbin, egrp)
   const int32_t* slot_of;
   double* T;            // [n][4][Mp]
   double* D;            // [slots][K0p] (FP64 mode)
@@ -200,10 +201,10 @@ inline TabParams make_params(Engine& E) {
   p.eown = E.eown.p;
   p.center = E.center.p;
   p.ebin = E.ebin.p;
-  p.erc = E.erc.p;
-  p.egrp = E.egrp.p;
-  p.gbin = E.gbin.p;
-  p.skeys = E.skeys.p;
+  p.erc = E.we(E.erc, 5); // chunk-local entry arrays of the current buffer set
+  p.egrp = E.we(E.egrp);
+  p.gbin = E.we(E.gbin);
+  p.skeys = E.we(E.skeys);
   p.n_real = E.n_real.p;
   p.n_grp = E.n_grp.p;
   p.goff = E.goff.p;
@@ -227,12 +228,13 @@ inline TabParams make_params(Engine& E) {
   p.Mp = E.Mp;
   p.mlt = E.mlt;
   p.K0p = E.K0p;
-  p.E = E.e_cap;   // SoA stride and grid bound; the live count is row_off[n]
+  p.E = E.e_cap;   // grid bound of the global entry arrays; the live count is row_off[n]
+  p.es = E.ck_cap_e; // chunk-local entry arrays are indexed e - row_off[i0] (see chunk_params)
   p.slot_of = E.slot_of.p;
-  p.T = E.T.p;
-  p.D = E.precision == 1 ? nullptr : E.D.p;
-  p.D2 = E.precision == 1 ? E.tc_d2.p : nullptr;
-  p.dD = E.dD.p;
+  p.T = E.wa(E.T, 4 * E.Mp); // per-centre windows of the current chunk (Engine::use_chunk)
+  p.D = E.precision == 1 ? nullptr : E.ws(E.D, E.K0p);
+  p.D2 = E.precision == 1 ? E.ws(E.tc_d2, 2 * E.K0p) : nullptr;
+  p.dD = E.ws(E.dD, E.K0p);
   p.g = E.g.p;
   p.counters = E.counters.p;
   p.err = E.err.p;

@@ -39,9 +39,14 @@ namespace {
 
 // ---------------------------------------------------------------- k_env_fwd (thread per entry)
 __global__ void __launch_bounds__(256) k_env_fwd(TabParams p) {
-  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  // entries of the centre range [i0, i1); chunk-local arrays at el = e - row_off[i0]
+  const int64_t eb = p.row_off[p.i0];
+  const int64_t el = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t e = eb + el;
   bool ext = false;
-  const bool live = e < p.E && e < p.row_off[p.n];
+  const bool in_range = e < p.E && e < p.row_off[p.i1];
+  if (in_range && el >= p.es) raise_err(p.err, DEV_LIST_CAP); // chunk entry capacity (never expected)
+  const bool live = in_range && el < p.es;
   if (live && !p.center[p.eown[e]]) p.ebin[e] = -1;
   if (live && p.center[p.eown[e]]) {
     const int i = p.eown[e];
@@ -60,21 +65,21 @@ __global__ void __launch_bounds__(256) k_env_fwd(TabParams p) {
       const double ir = 1.0 / r;
       const double s = switch_fn(r, p.rs, p.rc) * ir;
       bin = key_type(key);
-      p.erc[e] = s;
-      p.erc[p.E + e] = s * (d[0] * ir);
-      p.erc[2 * p.E + e] = s * (d[1] * ir);
-      p.erc[3 * p.E + e] = s * (d[2] * ir);
+      p.erc[el] = s;
+      p.erc[p.es + el] = s * (d[0] * ir);
+      p.erc[2 * p.es + el] = s * (d[1] * ir);
+      p.erc[3 * p.es + el] = s * (d[2] * ir);
     } else if (r2 < p.rc2) {
       const double r = sqrt(r2);
       const double ir = 1.0 / r;
       const double s = switch_fn(r, p.rs, p.rc) * ir;
       const int th = locate(p, s, ext, p.err);
       bin = key_type(key) * p.tn + th;
-      p.erc[e] = s;
-      p.erc[p.E + e] = s * (d[0] * ir);
-      p.erc[2 * p.E + e] = s * (d[1] * ir);
-      p.erc[3 * p.E + e] = s * (d[2] * ir);
-      p.erc[4 * p.E + e] = s - node_x(p.x0, p.h, th);
+      p.erc[el] = s;
+      p.erc[p.es + el] = s * (d[0] * ir);
+      p.erc[2 * p.es + el] = s * (d[1] * ir);
+      p.erc[3 * p.es + el] = s * (d[2] * ir);
+      p.erc[4 * p.es + el] = s - node_x(p.x0, p.h, th);
     }
     p.ebin[e] = bin;
   }
@@ -255,8 +260,10 @@ __global__ void __launch_bounds__(64, 8) k_tab_fwd(TabParams p) {
   const FwdSmem w = carve_fwd(smem + wid * fwd_smem_bytes(p.scap, p.Mp), p.scap, p.Mp);
   const size_t istride = static_cast<size_t>(6) * p.Mp;
   const int f0 = F * lane;
+  const int64_t eb = p.row_off[p.i0];
   for (int i = p.i0 + blockIdx.x * wpb + wid; i < p.i1; i += gridDim.x * wpb) {
     const int64_t off = p.row_off[i];
+    const int64_t loff = off - eb; // chunk-local entry offset
     const int len = static_cast<int>(p.row_off[i + 1] - off);
     for (int t = lane; t < 64; t += 32) w.tc[t] = 0;
     __syncwarp();
@@ -284,7 +291,7 @@ __global__ void __launch_bounds__(64, 8) k_tab_fwd(TabParams p) {
     kmax = warp_max(kmax);
     for (int t = lane; t < p.n_types; t += 32)
       if (w.tc[t] > p.max_nbr[t]) raise_err(p.err, DEV_OVERFLOW);
-    const int G = sort_and_group(w, p.skeys + off, nreal, kmin, kmax, lane);
+    const int G = sort_and_group(w, p.skeys + loff, nreal, kmin, kmax, lane);
     if (lane == 0) {
       atomicAdd(p.counters + 0, static_cast<unsigned long long>(nreal));
       p.n_real[i] = nreal;
@@ -292,11 +299,11 @@ __global__ void __launch_bounds__(64, 8) k_tab_fwd(TabParams p) {
     }
     for (int j = lane; j < nreal; j += 32) {
       const int k = w.od[j];
-      p.skeys[off + j] = (static_cast<uint64_t>(w.rk[k]) << 32) | w.ex[k];
+      p.skeys[loff + j] = (static_cast<uint64_t>(w.rk[k]) << 32) | w.ex[k];
     }
     for (int g = lane; g < G; g += 32) {
-      p.gbin[off + g] = w.gb[g];
-      for (int j = w.gs[g]; j < w.gs[g + 1]; ++j) p.egrp[off + w.ex[w.od[j]]] = g;
+      p.gbin[loff + g] = w.gb[g];
+      for (int j = w.gs[g]; j < w.gs[g + 1]; ++j) p.egrp[loff + w.ex[w.od[j]]] = g;
     }
     // --- moments of each (type, interval) group, then T += W . C[interval] ---
     double tacc[4][F];
@@ -315,9 +322,9 @@ __global__ void __launch_bounds__(64, 8) k_tab_fwd(TabParams p) {
         if (g < G) {
           const int j1 = w.gs[g + 1];
           for (int j = w.gs[g] + r; j < j1; j += 4) {
-            const int64_t e = off + w.ex[w.od[j]];
-            const double R[4] = {p.erc[e], p.erc[p.E + e], p.erc[2 * p.E + e], p.erc[3 * p.E + e]};
-            const double uu = p.erc[4 * p.E + e];
+            const int64_t e = loff + w.ex[w.od[j]];
+            const double R[4] = {p.erc[e], p.erc[p.es + e], p.erc[2 * p.es + e], p.erc[3 * p.es + e]};
+            const double uu = p.erc[4 * p.es + e];
             double um = 1.0;
 #pragma unroll
             for (int mm = 0; mm < 6; ++mm) {
@@ -539,6 +546,7 @@ __global__ void __launch_bounds__(64, 6) k_tab_bwd_P(TabParams p, const double* 
   const size_t istride = static_cast<size_t>(6) * p.Mp;
   const int f0 = F * lane;
   const int total = fb_list ? *fb_count * na : p.i1 - p.i0;
+  const int64_t eb = p.row_off[p.i0];
   for (int idx = blockIdx.x * wpb + wid; idx < total; idx += gridDim.x * wpb) {
     const int i = fb_list ? fb_list[idx / na] + idx % na : p.i0 + idx; // fb_list holds block starts
     if (i >= p.i1) continue;
@@ -549,7 +557,7 @@ __global__ void __launch_bounds__(64, 6) k_tab_bwd_P(TabParams p, const double* 
       if (lane == 0) raise_err(p.err, DEV_PBUF);
       G = 0;
     }
-    const uint64_t* sk = p.skeys + off;
+    const uint64_t* sk = p.skeys + (off - eb);
     double* Pout = p.Pbuf + p.goff[i] * 24;
     const double* dTi = dTg + static_cast<size_t>(i) * 4 * p.Mp;
     double dT[4][F];
@@ -648,6 +656,7 @@ __global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gid = lane >> 2, tig = lane & 3;
   const int nblk = (p.i1 - p.i0 + P2_NA - 1) / P2_NA;
+  const int64_t eb = p.row_off[p.i0];
   // output columns of this thread inside a chunk: c = 8 nt + 2 tig + h -> (slot c / 6, m = c % 6)
   int cslot[6], cm[6];
 #pragma unroll
@@ -682,7 +691,7 @@ __global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double
       const int i = i0 + tid;
       const int G = p.n_grp[i];
       if (G > 0) {
-        const int32_t* gb = p.gbin + p.row_off[i];
+        const int32_t* gb = p.gbin + (p.row_off[i] - eb);
         atomicMin(misc, gb[0]);
         atomicMax(misc + 1, gb[G - 1]);
       }
@@ -700,7 +709,7 @@ __global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double
         const int i = i0 + al;
         if (i >= p.i1) break;
         const int G = p.n_grp[i];
-        const int32_t* gb = p.gbin + p.row_off[i];
+        const int32_t* gb = p.gbin + (p.row_off[i] - eb);
         for (int g = lane; g < G; g += 32) {
           const int b = gb[g] - bmin;
           atomicOr(bm + (b >> 5), 1u << (b & 31));
@@ -751,7 +760,7 @@ __global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double
       const int i = i0 + al;
       if (i >= p.i1) break;
       const int G = p.n_grp[i];
-      const int32_t* gb = p.gbin + p.row_off[i];
+      const int32_t* gb = p.gbin + (p.row_off[i] - eb);
       for (int g = lane; g < G; g += 32) {
         const int b = gb[g] - bmin;
         const int u = wpre[b >> 5] + __popc(bm[b >> 5] & ((1u << (b & 31)) - 1u));
@@ -871,7 +880,7 @@ __global__ void __launch_bounds__(256) k_tab_bwd_g(TabParams p) {
   Env ev;
   env_of(p, ld_pos(p.pos, i), p.keys[e], ev);
   const int th = bin % p.tn;
-  const int64_t gi = p.goff[i] + p.egrp[e];
+  const int64_t gi = p.goff[i] + p.egrp[e - eb];
   if (gi >= p.pcap) {
     raise_err(p.err, DEV_PBUF);
     ge[0] = ge[1] = ge[2] = 0.0;
@@ -946,33 +955,36 @@ void launch_dT(const TabParams& p, double* dTg, cudaStream_t st, int sms) {
 
 } // namespace
 
-// Parameters of the centre range [i0, i1) of pipelined half c.
-TabParams chunk_params(Engine& E, int c, int64_t i0, int64_t i1) {
+// Parameters of the centre range [i0, i1) of the current chunk (Engine::use_chunk): window
+// pointers of its buffer set, its Pbuf region.
+TabParams chunk_params(Engine& E, int64_t i0, int64_t i1) {
   TabParams p = make_params(E);
   p.i0 = static_cast<int>(i0);
   p.i1 = static_cast<int>(i1);
-  p.Pbuf = E.Pbuf.p + static_cast<size_t>(c) * E.pbuf_cap * 24;
+  p.Pbuf = E.Pbuf.p + static_cast<size_t>(E.cur_set) * E.pbuf_cap * 24;
   return p;
 }
 
-// Total groups of a centre range (for the Pbuf capacity of its half).
+// Total groups of a centre range (for the Pbuf capacity of its chunk).
 __global__ void k_group_total(const int32_t* __restrict__ n_grp, const int64_t* __restrict__ goff, int i0, int i1,
                               int64_t* __restrict__ out) {
   if (threadIdx.x == 0 && blockIdx.x == 0) *out = i1 > i0 ? goff[i1 - 1] + n_grp[i1 - 1] : 0;
 }
 
-void Engine::launch_env(cudaStream_t st) {
-  TabParams p = make_params(*this);
-  if (p.E > 0) {
-    k_env_fwd<<<ceil_div(p.E, 256), 256, 0, st>>>(p);
-    ++launches;
+// env-mat of every entry of the rows [i0, i1): grid bound = the chunk's entry capacity
+void env_range(Engine& E, const TabParams& p, cudaStream_t st) {
+  const int64_t ne = std::min<int64_t>(p.es, p.E);
+  if (ne > 0) {
+    k_env_fwd<<<ceil_div(ne, 256), 256, 0, st>>>(p);
+    ++E.launches;
   }
 }
 
-// k_tab_fwd over centres [i0, i1) of half c, then the group offsets of that half (goff[i0..i1)
-// start at 0; half c owns Pbuf[c * pbuf_cap ...]).
-void Engine::tab_fwd_range(int c, int64_t i0, int64_t i1, cudaStream_t st) {
-  TabParams p = chunk_params(*this, c, i0, i1);
+// env + k_tab_fwd over centres [i0, i1) of chunk k, then the group offsets of the chunk
+// (goff[i0..i1) start at 0; the chunk's buffer set owns Pbuf[set * pbuf_cap ...]).
+void Engine::tab_fwd_range(int k, int64_t i0, int64_t i1, cudaStream_t st) {
+  TabParams p = chunk_params(*this, i0, i1);
+  env_range(*this, p, st);
   const int sms = sm_count(device);
   switch (Mp / 32) {
     case 1: launch_fwd_warp<1>(p, st, sms); break;
@@ -986,23 +998,24 @@ void Engine::tab_fwd_range(int c, int64_t i0, int64_t i1, cudaStream_t st) {
     default: throw InputErr("feature width 4*d1 must be at most 256");
   }
   ++launches;
-  DevBuf<unsigned char>& tmp = c == 0 ? scan_tmp : scan_tmp2;
+  DevBuf<unsigned char>& tmp = cur_set == 0 ? scan_tmp : scan_tmp2;
   const int cnt = static_cast<int>(i1 - i0);
   size_t tb = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tb, n_grp.p + i0, goff.p + i0, cnt, st);
   tmp.ensure(tb + 1);
   cub::DeviceScan::ExclusiveSum(tmp.p, tb, n_grp.p + i0, goff.p + i0, cnt, st);
-  gtot.ensure(4);
-  k_group_total<<<1, 32, 0, st>>>(n_grp.p, goff.p, static_cast<int>(i0), static_cast<int>(i1), gtot.p + c);
-  if (!h_gtotal) DPB_CUDA(cudaMallocHost(&h_gtotal, 4 * sizeof(int64_t)));
-  DPB_CUDA(cudaMemcpyAsync(h_gtotal + c, gtot.p + c, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  gtot.ensure(MAX_CHUNKS);
+  k_group_total<<<1, 32, 0, st>>>(n_grp.p, goff.p, static_cast<int>(i0), static_cast<int>(i1), gtot.p + k);
+  if (!h_gtotal) {
+    DPB_CUDA(cudaMallocHost(&h_gtotal, MAX_CHUNKS * sizeof(int64_t)));
+    std::memset(h_gtotal, 0, MAX_CHUNKS * sizeof(int64_t));
+  }
+  DPB_CUDA(cudaMemcpyAsync(h_gtotal + k, gtot.p + k, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   launches += 2;
 }
 
 void Engine::launch_tab_fwd() {
-  launch_env(stream);
   tab_fwd_range(0, 0, n, stream);
-  n_halves = 1;
   size_pbuf_if_needed();
 }
 
@@ -1027,27 +1040,26 @@ void Engine::launch_env_exact() {
 
 void Engine::grow_pbuf() {
   if (!h_gtotal) return;
-  // every region is sized for the whole system's total, so switching between the pipelined
-  // halves and a single range never overflows
+  // one region per buffer set, each sized for the largest chunk seen (+50 %)
   int64_t tot = 0;
-  for (int c = 0; c < n_halves; ++c) tot += h_gtotal[c];
+  for (int c = 0; c < n_chunks; ++c) tot = std::max(tot, h_gtotal[c]);
   const int64_t want = tot + tot / 2 + 1024;
   if (want > pbuf_cap) {
-    Pbuf.ensure(static_cast<size_t>(want) * 24 * 2); // one region per pipelined half
+    Pbuf.ensure(static_cast<size_t>(want) * 24 * ck_sets);
     pbuf_cap = want;
   }
 }
 
-void Engine::tab_bwd_range(int c, int64_t i0, int64_t i1, cudaStream_t st) {
-  TabParams p = chunk_params(*this, c, i0, i1);
+void Engine::tab_bwd_range(int, int64_t i0, int64_t i1, cudaStream_t st) {
+  TabParams p = chunk_params(*this, i0, i1);
   const int sms = sm_count(device);
-  dTbuf.ensure(static_cast<size_t>(n) * 4 * Mp);
-  const int nblk_all = ceil_div(static_cast<int64_t>(n), P2_NA);
+  double* dTw = wa(dTbuf, 4 * Mp);
+  const int nblk_all = ceil_div(ck_cap_a, P2_NA);
   fb_list.ensure(2 * (nblk_all + 1));
-  int* fbl = fb_list.p + c * (nblk_all + 1);
+  int* fbl = fb_list.p + cur_set * (nblk_all + 1);
   const int nblk = ceil_div(i1 - i0, P2_NA);
   switch (Mp / 32) {
-#define DPB_DT(F) case F: launch_dT<F>(p, dTbuf.p, st, sms); break;
+#define DPB_DT(F) case F: launch_dT<F>(p, dTw, st, sms); break;
     DPB_DT(1) DPB_DT(2) DPB_DT(3) DPB_DT(4) DPB_DT(5) DPB_DT(6) DPB_DT(7) DPB_DT(8)
 #undef DPB_DT
     default: throw InputErr("feature width 4*d1 must be at most 256");
@@ -1066,7 +1078,7 @@ void Engine::tab_bwd_range(int c, int64_t i0, int64_t i1, cudaStream_t st) {
   case F:                                                                                                     \
     DPB_CUDA(cudaFuncSetAttribute(k_tab_bwd_P2<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
                                   static_cast<int>(bytes)));                                                  \
-    k_tab_bwd_P2<F><<<std::max(1, std::min(nblk, sms)), 256, bytes, st>>>(p, dTbuf.p, fbl, fbl + nblk_all);   \
+    k_tab_bwd_P2<F><<<std::max(1, std::min(nblk, sms)), 256, bytes, st>>>(p, dTw, fbl, fbl + nblk_all);   \
     break;
       DPB_P2(1) DPB_P2(2) DPB_P2(3) DPB_P2(4)
 #undef DPB_P2
@@ -1077,14 +1089,15 @@ void Engine::tab_bwd_range(int c, int64_t i0, int64_t i1, cudaStream_t st) {
     fc = fbl + nblk_all;
   }
   switch (Mp / 32) {
-#define DPB_BW(F) case F: launch_bwd_warp<F>(p, dTbuf.p, fl, fc, P2_NA, st, sms); break;
+#define DPB_BW(F) case F: launch_bwd_warp<F>(p, dTw, fl, fc, P2_NA, st, sms); break;
     DPB_BW(1) DPB_BW(2) DPB_BW(3) DPB_BW(4) DPB_BW(5) DPB_BW(6) DPB_BW(7) DPB_BW(8)
 #undef DPB_BW
     default: throw InputErr("feature width 4*d1 must be at most 256");
   }
   ++launches;
-  if (p.E > 0) {
-    k_tab_bwd_g<<<ceil_div(p.E, 256), 256, 0, st>>>(p);
+  const int64_t ne = std::min<int64_t>(p.es, p.E);
+  if (ne > 0) {
+    k_tab_bwd_g<<<ceil_div(ne, 256), 256, 0, st>>>(p);
     ++launches;
   }
 }
