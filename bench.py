@@ -38,6 +38,8 @@ sys.path.insert(0, str(ROOT))
 CONFIGS = {
     "c2": dict(cells=(20, 20, 20), label="C2: Cu FCC 20x20x20 (32,000 atoms) NVE MD step"),
     "c3": dict(cells=(64, 64, 64), label="C3: Cu FCC 64x64x64 (1,048,576 atoms) NVE MD step"),
+    "c4": dict(cells=(150, 150, 150), strong=True,
+               label="C4: Cu FCC 150x150x150 (13,500,000 atoms, the paper's case) NVE MD step"),
     "c5": dict(cells=(100, 100, 100), label="C5: Cu FCC 100x100x100 (4,000,000 atoms) NVE MD step"),
 }
 MACS_FIT = None  # filled from the model shape
@@ -227,9 +229,11 @@ def run_ours(args, world, rank, local, dist):
     m = dp.gen_model("copper-like", 7)
     t = dp.build_tables(m, 0.01)
     cells = spec["cells"]
+    strong = bool(spec.get("strong"))
     # weak scaling: the global box grows along x, one C2-sized slab per GPU (partition_domain
-    # slices the roomiest axis); N = 1 is the plain single-GPU configuration
-    gcfg = dp.gen_config("copper-like", cells[0] * world, cells[1], cells[2], 0.1, 11)
+    # slices the roomiest axis); N = 1 is the plain single-GPU configuration. Strong scaling
+    # (C4): the same 13.5 M-atom box split over the N GPUs.
+    gcfg = dp.gen_config("copper-like", cells[0] * (1 if strong else world), cells[1], cells[2], 0.1, 11)
     gvel = dp.init_velocities(gcfg, m, 330.0, 99)
     n_total = gcfg.n_atoms
     n = n_total // world
@@ -364,10 +368,11 @@ def run_ours(args, world, rank, local, dist):
                       "MD atom-steps/s (Cu, mixed: tcgen05 3xTF32 fitting + tanh table, 1e-5)",
             "value": value, "unit": "atom-steps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
             "dtype": "f64" if args.precision == "fp64" else "f64 env/tabulate, tf32x3 fitting",
             "data": "synthetic",
-            "config": {"workload": spec["label"] + (" per GPU (weak scaling, slabs along x)" if world > 1 else ""),
+            "config": {"workload": spec["label"] + (" per GPU (weak scaling, slabs along x)"
+                                                    if world > 1 and not strong else ""),
                        "atoms_per_gpu": n, "atoms_total": n_total,
                        "model": "copper-like DP-SE, random weights (gen_model seed 7), tables h=0.01",
                        "dt_fs": 1.0, "list": "r_c + 2 A, rebuilt every 50 steps",

@@ -176,6 +176,25 @@ __global__ void k_unpack_pos(int64_t m, const int32_t* __restrict__ idx, const d
   pos4[i] = make_double4(x, y, z, 0.0);
 }
 
+// Chunk classification: flag[k] = 1 when a centre of chunk k (atoms [cka[k], cka[k+1])) has a
+// ghost in its neighbour row. Thread per atom, chunk found by binary search.
+__global__ void k_chunk_ghost(int64_t n, int nk, const int64_t* __restrict__ cka, const uint8_t* __restrict__ center,
+                              const int64_t* __restrict__ row_off, const uint64_t* __restrict__ keys,
+                              int* __restrict__ flag) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n || !center[i]) return;
+  int lo = 0, hi = nk - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (cka[mid] <= i) lo = mid; else hi = mid - 1;
+  }
+  for (int64_t e = row_off[i]; e < row_off[i + 1]; ++e)
+    if (!center[key_j(keys[e])]) {
+      flag[lo] = 1;
+      return;
+    }
+}
+
 __global__ void k_accum3(int64_t m, const int32_t* __restrict__ idx, const double* __restrict__ src,
                          double* __restrict__ dst) {
   const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -540,6 +559,7 @@ void build_local(Engine& E) {
   const auto t2 = now();
   E.md_upload_atoms(lv.data());
   E.build_list(E.r_cut + E.md.buffer);
+  E.classify_chunks();
   const auto t3 = now();
   if (trace) {
     auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
@@ -548,14 +568,15 @@ void build_local(Engine& E) {
   }
 }
 
-void exchange(Engine& E, const std::vector<int64_t>& out_off, const std::vector<int64_t>& in_off) {
+void exchange(Engine& E, const std::vector<int64_t>& out_off, const std::vector<int64_t>& in_off,
+              cudaStream_t st) {
   Dist& D = *E.dist;
   DPB_NCCL(ncclGroupStart());
   for (int p = 0; p < D.world; ++p) {
     const int64_t so = out_off[p], sc = out_off[p + 1] - so;
     const int64_t ro = in_off[p], rc = in_off[p + 1] - ro;
-    if (sc > 0) DPB_NCCL(ncclSend(D.sbuf.p + 3 * so, 3 * sc, ncclDouble, p, D.comm, E.stream));
-    if (rc > 0) DPB_NCCL(ncclRecv(D.rbuf.p + 3 * ro, 3 * rc, ncclDouble, p, D.comm, E.stream));
+    if (sc > 0) DPB_NCCL(ncclSend(D.sbuf.p + 3 * so, 3 * sc, ncclDouble, p, D.comm, st));
+    if (rc > 0) DPB_NCCL(ncclRecv(D.rbuf.p + 3 * ro, 3 * rc, ncclDouble, p, D.comm, st));
   }
   DPB_NCCL(ncclGroupEnd());
 }
@@ -630,26 +651,70 @@ void dist_md_begin(Engine& E, int64_t N, const double* pos, const double* vel, c
 }
 
 // Positions of my ghosts from their owners.
+// Forward halo: owned positions -> the peers' ghosts. With overlap on, it runs on st_comm after
+// the drift (ev_kd); the evaluation makes only the chunks with ghost neighbours (and the force
+// kernel) wait for it (ev_halo). Every NCCL call on st_comm is ordered after the stream's
+// earlier NCCL calls through the event it waits on, and the stream's later ones wait for
+// ev_rx / ev_halo, so one communicator never has two operations in flight.
 void dist_halo_forward(Engine& E) {
   Dist& D = *E.dist;
   const int64_t ns = D.soff[D.world], nr = D.roff[D.world];
-  if (ns) k_pack3<<<ceil_div(ns, 256), 256, 0, E.stream>>>(ns, D.sidx.p, E.pos3.p, D.sbuf.p);
-  exchange(E, D.soff, D.roff);
-  if (nr) k_unpack_pos<<<ceil_div(nr, 256), 256, 0, E.stream>>>(nr, D.ridx.p, D.rbuf.p, E.pos3.p, E.pos4.p);
+  cudaStream_t st = E.stream;
+  if (E.halo_overlap) {
+    DPB_CUDA(cudaEventRecord(E.ev_kd, E.stream));
+    DPB_CUDA(cudaStreamWaitEvent(E.st_comm, E.ev_kd, 0));
+    st = E.st_comm;
+  }
+  if (ns) k_pack3<<<ceil_div(ns, 256), 256, 0, st>>>(ns, D.sidx.p, E.pos3.p, D.sbuf.p);
+  exchange(E, D.soff, D.roff, st);
+  if (nr) k_unpack_pos<<<ceil_div(nr, 256), 256, 0, st>>>(nr, D.ridx.p, D.rbuf.p, E.pos3.p, E.pos4.p);
   E.launches += 2;
+  if (E.halo_overlap) {
+    DPB_CUDA(cudaEventRecord(E.ev_halo, st));
+    E.halo_pending = true;
+  }
 }
 
-// Ghost force partials (minus the pair gradients landing on them) back to their owners.
+// Reverse halo, first half: the ghost force partials (minus the pair gradients landing on
+// them) go back to their owners on st_comm, right after the ghost-only force kernel.
+// (the ghost-only force kernel has written the partials packed into sbuf, ridx order)
+void dist_reverse_send(Engine& E) {
+  Dist& D = *E.dist;
+  DPB_CUDA(cudaEventRecord(E.ev_gf, E.stream));
+  DPB_CUDA(cudaStreamWaitEvent(E.st_comm, E.ev_gf, 0));
+  exchange(E, D.roff, D.soff, E.st_comm);
+  DPB_CUDA(cudaEventRecord(E.ev_rx, E.st_comm));
+  E.rev_sent = true;
+}
+
+// The ghosts of this rank in reverse-halo order (ridx: peer by peer, ascending global id) and
+// the send buffer their partials are packed into.
+bool dist_ghost_list(Engine& E, const int32_t** list, int64_t* n, double** send) {
+  Dist& D = *E.dist;
+  *list = D.ridx.p;
+  *n = D.roff[D.world];
+  *send = D.sbuf.p;
+  return D.ridx.p != nullptr;
+}
+
+// Reverse halo, second half: received partials added to the owned forces in peer order.
 void dist_halo_reverse(Engine& E) {
   Dist& D = *E.dist;
   const int64_t ns = D.soff[D.world], nr = D.roff[D.world];
-  if (nr) k_pack3<<<ceil_div(nr, 256), 256, 0, E.stream>>>(nr, D.ridx.p, E.forces.p, D.sbuf.p);
-  exchange(E, D.roff, D.soff);
+  if (E.rev_sent) {
+    DPB_CUDA(cudaStreamWaitEvent(E.stream, E.ev_rx, 0));
+    E.rev_sent = false;
+  } else {
+    if (nr) k_pack3<<<ceil_div(nr, 256), 256, 0, E.stream>>>(nr, D.ridx.p, E.forces.p, D.sbuf.p);
+    exchange(E, D.roff, D.soff, E.stream);
+    E.launches += 1;
+  }
+  (void)ns;
   for (int p = 0; p < D.world; ++p) {
     const int64_t o = D.soff[p], c = D.soff[p + 1] - o;
     if (c) k_accum3<<<ceil_div(c, 256), 256, 0, E.stream>>>(c, D.sidx.p + o, D.rbuf.p + 3 * o, E.forces.p);
   }
-  E.launches += 1 + D.world;
+  E.launches += D.world;
 }
 
 // All-gather of the owned (id, x, v) into the global arrays on every rank (device resident).
@@ -674,6 +739,30 @@ static void gather_global(Engine& E) {
   k_unpack_global<<<ceil_div(nrec, 256), 256, 0, E.stream>>>(nrec, D.gbuf_all.p, D.d_gpos.p, D.d_gvel.p);
   E.launches += 5;
   D.host_global_valid = false;
+}
+
+void Engine::classify_chunks() {
+  if (!dist || n_chunks < 2) return;
+  DevBuf<int64_t> cka;
+  DevBuf<int> flag;
+  cka.ensure(n_chunks + 1);
+  flag.ensure(n_chunks);
+  DPB_CUDA(cudaMemcpyAsync(cka.p, ck_a.data(), (n_chunks + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, stream));
+  DPB_CUDA(cudaMemsetAsync(flag.p, 0, n_chunks * sizeof(int), stream));
+  k_chunk_ghost<<<ceil_div(n, 256), 256, 0, stream>>>(n, n_chunks, cka.p, center.p, row_off.p, keys.p, flag.p);
+  ++launches;
+  std::vector<int> f(n_chunks);
+  DPB_CUDA(cudaMemcpyAsync(f.data(), flag.p, n_chunks * sizeof(int), cudaMemcpyDeviceToHost, stream));
+  DPB_CUDA(cudaStreamSynchronize(stream));
+  cka.release();
+  flag.release();
+  ck_order.clear();
+  for (int k = 0; k < n_chunks; ++k) {
+    ck_ghost[k] = f[k] ? 1 : 0;
+    if (!f[k]) ck_order.push_back(k);
+  }
+  for (int k = 0; k < n_chunks; ++k)
+    if (f[k]) ck_order.push_back(k);
 }
 
 void dist_rebuild(Engine& E) {

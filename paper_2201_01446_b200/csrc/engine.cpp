@@ -85,8 +85,9 @@ void Engine::create(const dp_model_desc* md, const dp_table_desc* td, int dev, i
   DPB_CUDA(cudaSetDevice(dev));
   DPB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   DPB_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
-  for (cudaEvent_t* e : {&ev_split, &ev_join, &ev_fwd[0], &ev_fwd[1]})
+  for (cudaEvent_t* e : {&ev_split, &ev_join, &ev_fwd[0], &ev_fwd[1], &ev_kd, &ev_halo, &ev_gf, &ev_rx})
     DPB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  DPB_CUDA(cudaStreamCreateWithFlags(&st_comm, cudaStreamNonBlocking));
   n_types = md->n_types;
   r_cut = md->r_cut;
   r_smooth = md->r_smooth;
@@ -216,7 +217,7 @@ void Engine::destroy() {
   tc_tanh.release(); tc_d2.release(); tc_y2a.release(); tc_y2b.release(); tc_dz2a.release();
   tc_dz2b.release(); tc_dya.release(); tc_dyb.release();
   dTbuf.release(); fb_list.release(); emb_w.release(); emb_ptrs.release(); exact_ctr.release();
-  for (cudaStream_t* s : {&st2})
+  for (cudaStream_t* s : {&st2, &st_comm})
     if (*s) {
       cudaStreamSynchronize(*s);
       cudaStreamDestroy(*s);
@@ -224,7 +225,7 @@ void Engine::destroy() {
     }
   if (stream) cudaStreamDestroy(stream);
   stream = nullptr;
-  for (cudaEvent_t* e : {&ev_split, &ev_join, &ev_fwd[0], &ev_fwd[1]})
+  for (cudaEvent_t* e : {&ev_split, &ev_join, &ev_fwd[0], &ev_fwd[1], &ev_kd, &ev_halo, &ev_gf, &ev_rx})
     if (*e) {
       cudaEventDestroy(*e);
       *e = nullptr;
@@ -334,6 +335,7 @@ void Engine::plan_chunks() {
     const bool overlap = pipeline && precision == 0 && Mp <= 128 && nc >= 8192;
     nk = static_cast<int>((nc + cmax - 1) / cmax);
     if (overlap) nk = std::max(nk, 2);
+    nk = std::max(nk, 1);
     if (nk > MAX_CHUNKS) throw InputErr("too many evaluation chunks (raise DPB_CHUNK)");
   }
   n_chunks = nk;
@@ -347,20 +349,26 @@ void Engine::plan_chunks() {
     ck_rows[0] = n_slots;
   } else {
     // slot boundaries every cs centres; atom boundary = index of the first centre of the chunk
+    // (decomposed runs: chunks span first..last centre; the rows of the ghosts outside every
+    // chunk are marked non-real once per list build, mark_ghost_rows)
     const int64_t cs = round_up((nc + nk - 1) / nk, 128);
-    int64_t c = 0;
-    int k = 1;
-    for (int64_t i = 0; i < n && k < nk; ++i)
+    int64_t c = 0, last = 0;
+    int k = 0;
+    for (int64_t i = 0; i < n; ++i)
       if (h_center[i]) {
-        if (c == k * cs) ck_a[k++] = i;
+        if (k < nk && c == k * cs) ck_a[k++] = i;
         ++c;
+        last = i;
       }
-    for (; k < nk; ++k) ck_a[k] = n; // (cannot happen: nk chunks of cs cover nc)
-    ck_a[nk] = n;
+    for (; k < nk; ++k) ck_a[k] = last + 1; // (cannot happen: nk chunks of cs cover nc)
+    ck_a[nk] = last + 1;
     for (int q = 0; q <= nk; ++q) ck_s[q] = std::min<int64_t>(static_cast<int64_t>(q) * cs, nc);
     ck_s[nk] = nc;
     for (int q = 0; q < nk; ++q) ck_rows[q] = (q == nk - 1 ? seg_rows[0] : ck_s[q + 1]) - ck_s[q];
   }
+  ck_ghost.assign(nk, 1);
+  ck_order.resize(nk);
+  for (int q = 0; q < nk; ++q) ck_order[q] = q;
   ck_cap_a = ck_cap_s = 0;
   for (int q = 0; q < nk; ++q) {
     ck_cap_a = std::max(ck_cap_a, ck_a[q + 1] - ck_a[q]);
@@ -452,6 +460,10 @@ void Engine::evaluate() {
     return;
   }
   use_chunk(0);
+  if (halo_pending) {
+    DPB_CUDA(cudaStreamWaitEvent(stream, ev_halo, 0));
+    halo_pending = false;
+  }
   phase_begin(1);
   launch_tab_fwd();
   phase_begin(2);
@@ -477,13 +489,15 @@ bool Engine::pipeline_ok() const { return pipeline && precision == 0 && Mp <= 12
 void Engine::evaluate_chunked() {
   const bool two = pipeline_ok();
   cudaStream_t last = stream;
-  for (int k = 0; k < n_chunks; ++k) {
-    use_chunk(k);
-    cudaStream_t st = two && (k & 1) ? st2 : stream;
-    if (two && k >= 1) DPB_CUDA(cudaStreamWaitEvent(st, ev_fwd[(k - 1) & 1], 0));
+  for (int q = 0; q < n_chunks; ++q) {
+    const int k = ck_order[q]; // interior chunks first (decomposed runs)
+    use_chunk(k, q & 1);
+    cudaStream_t st = two && (q & 1) ? st2 : stream;
+    if (two && q >= 1) DPB_CUDA(cudaStreamWaitEvent(st, ev_fwd[(q - 1) & 1], 0));
+    if (halo_pending && ck_ghost[k]) DPB_CUDA(cudaStreamWaitEvent(st, ev_halo, 0)); // ghost positions
     phase_begin(1);
     tab_fwd_range(k, ck_a[k], ck_a[k + 1], st);
-    if (two) DPB_CUDA(cudaEventRecord(ev_fwd[k & 1], st));
+    if (two) DPB_CUDA(cudaEventRecord(ev_fwd[q & 1], st));
     if (pbuf_cap == 0) {
       // first evaluation of this system/plan: size the group buffer from chunk 0's exact total
       DPB_CUDA(cudaStreamSynchronize(st));
@@ -504,6 +518,10 @@ void Engine::evaluate_chunked() {
     DPB_CUDA(cudaStreamWaitEvent(stream, ev_join, 0));
   }
   (void)last;
+  if (halo_pending) {
+    DPB_CUDA(cudaStreamWaitEvent(stream, ev_halo, 0)); // the force kernel reads ghost positions
+    halo_pending = false;
+  }
   phase_begin(4);
   finish_energy();
   launch_forces();
@@ -658,7 +676,15 @@ void Engine::md_begin(const double* pos, const double* vel, const dp_md_config* 
   // The group count grows while a lattice start thermalises; Pbuf then regrows inside the loop.
   // Pre-warm the stream-ordered pool (kept, release threshold = max) so that regrowth is a
   // sub-allocation instead of a physical allocation stalling the host for tens of ms.
-  if (Pbuf.n) {
+  if (std::getenv("DPB_TRACE")) {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    std::fprintf(stderr, "[dpb] md_begin: n %lld, entries cap %lld, chunks %d (set: %lld atoms, %lld slots, %lld entries), "
+                 "device memory used %.1f of %.1f GB\n", static_cast<long long>(n), static_cast<long long>(e_cap),
+                 n_chunks, static_cast<long long>(ck_cap_a), static_cast<long long>(ck_cap_s),
+                 static_cast<long long>(ck_cap_e), (tot - fr) / 1e9, tot / 1e9);
+  }
+  if (Pbuf.n && Pbuf.n * sizeof(double) < (size_t(1) << 29)) { // large systems: no pool reserve
     void* tmp = nullptr;
     if (cudaMallocAsync(&tmp, Pbuf.n * sizeof(double) * 3, stream) == cudaSuccess) cudaFreeAsync(tmp, stream);
     else cudaGetLastError();

@@ -43,11 +43,24 @@ struct DevBuf {
     static const bool trace = std::getenv("DPB_TRACE") != nullptr;
     const auto t0 = std::chrono::steady_clock::now();
     release();
-    size_t want = count + count / 8 + 64;
-    if (ord)
-      DPB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), want * sizeof(T), ord));
-    else
-      DPB_CUDA(cudaMalloc(&p, want * sizeof(T)));
+    size_t want = count + std::min<size_t>(count / 8, size_t(1) << 22) + 64; // growth slack, capped
+    auto alloc = [&] {
+      return ord ? cudaMallocAsync(reinterpret_cast<void**>(&p), want * sizeof(T), ord)
+                 : cudaMalloc(&p, want * sizeof(T));
+    };
+    cudaError_t e = alloc();
+    if (e == cudaErrorMemoryAllocation) {
+      // memory parked in the stream-ordered pool (release threshold = max) is not available to
+      // cudaMalloc: hand it back and retry once
+      cudaGetLastError();
+      cudaDeviceSynchronize();
+      int dev = 0;
+      cudaMemPool_t pool;
+      if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+        cudaMemPoolTrimTo(pool, 0);
+      e = alloc();
+    }
+    DPB_CUDA(e);
     n = want;
     if (trace)
       std::fprintf(stderr, "[dpb] %salloc %zu B: %.2f ms\n", ord ? "stream-ordered " : "", want * sizeof(T),
@@ -159,11 +172,22 @@ struct Engine {
   int cur_set = 0;
   int64_t cur_a0 = 0, cur_s0 = 0;
   cudaEvent_t ev_fwd[2] = {nullptr, nullptr};
+  // domain decomposition: chunks whose centres have ghost neighbours (device-classified at each
+  // rebuild) are evaluated last, so the forward halo (NCCL on st_comm) overlaps the interior
+  // chunks; the reverse halo of the ghost force partials overlaps the owned-atom force kernel
+  std::vector<uint8_t> ck_ghost; // [n_chunks] 1 = some centre of the chunk has a ghost neighbour
+  std::vector<int> ck_order;     // evaluation order: interior chunks first
+  cudaStream_t st_comm = nullptr;
+  cudaEvent_t ev_kd = nullptr, ev_halo = nullptr, ev_gf = nullptr, ev_rx = nullptr;
+  bool halo_overlap = std::getenv("DPB_NO_HALO_OVERLAP") == nullptr;
+  bool halo_pending = false; // forward halo in flight on st_comm (ev_halo marks its end)
+  bool rev_sent = false;     // reverse halo in flight on st_comm (ev_rx marks its end)
+  void classify_chunks();
   void plan_chunks();
   void apply_plan();
   void ensure_entry_step_buffers();
-  void use_chunk(int k) {
-    cur_set = ck_sets > 1 ? (k & 1) : 0;
+  void use_chunk(int k, int set = 0) {
+    cur_set = ck_sets > 1 ? set : 0;
     cur_a0 = ck_a[k];
     cur_s0 = ck_s[k];
   }
@@ -322,6 +346,8 @@ void dist_md_begin(Engine& E, int64_t N, const double* pos, const double* vel, c
 void dist_rebuild(Engine& E);
 void dist_halo_forward(Engine& E);
 void dist_halo_reverse(Engine& E);
+void dist_reverse_send(Engine& E);
+bool dist_ghost_list(Engine& E, const int32_t** list, int64_t* n, double** send);
 void dist_allreduce_sum(Engine& E, double* dev, int count);
 int64_t dist_n_total(const Engine& E);
 void dist_md_end(Engine& E, double* gpos, double* gvel);

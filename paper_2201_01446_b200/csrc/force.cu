@@ -25,10 +25,23 @@ __global__ void __launch_bounds__(256) k_forces(int n, DevCell c, const double4*
                                                 const int32_t* __restrict__ rev,
                                                 const int32_t* __restrict__ ebin,
                                                 const double* __restrict__ g,
-                                                double* __restrict__ f, double* __restrict__ vpart) {
+                                                double* __restrict__ f, double* __restrict__ vpart,
+                                                const uint8_t* __restrict__ center, int only,
+                                                const int32_t* __restrict__ list, int64_t nlist,
+                                                double* __restrict__ packed) {
   const int lane = threadIdx.x & 31;
-  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (i >= n) return;
+  const int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5);
+  int i;
+  if (list) {
+    // the atoms of `list` (a decomposed run's ghosts, in reverse-halo order): their partials
+    // are also written packed, as the send buffer of the reverse halo
+    if (w >= nlist) return;
+    i = list[w];
+  } else {
+    if (w >= n) return;
+    i = static_cast<int>(w);
+    if (only == 2 && !center[i]) return; // centres only (the ghosts were done from the list)
+  }
   const double3 ri = ld_pos(pos, i);
   double acc[15];
 #pragma unroll
@@ -100,6 +113,9 @@ __global__ void __launch_bounds__(256) k_forces(int n, DevCell c, const double4*
   if (lane == 0) {
 #pragma unroll
     for (int x = 0; x < 3; ++x) f[3 * i + x] = acc[x] - acc[3 + x];
+    if (packed)
+#pragma unroll
+      for (int x = 0; x < 3; ++x) packed[3 * w + x] = acc[x] - acc[3 + x];
 #pragma unroll
     for (int k = 0; k < 9; ++k) vpart[9 * static_cast<int64_t>(i) + k] = acc[6 + k];
   }
@@ -243,9 +259,24 @@ __global__ void k_thermo(int64_t step, int64_t n, double vol, const double* __re
 void Engine::launch_forces() {
   const int N = static_cast<int>(n);
   forces.ensure(3 * n);
-  k_forces<<<ceil_div(N, 8), 256, 0, stream>>>(N, cell, pos4.p, row_off.p, keys.p, rev.p, ebin.p,
-                                                g.p, forces.p, vpart.p);
-  ++launches;
+  int64_t ng = 0;
+  const int32_t* glist = nullptr;
+  double* gsend = nullptr;
+  if (dist && halo_overlap && dist_ghost_list(*this, &glist, &ng, &gsend) && ng == n - n_centers) {
+    // ghost partials first, written straight into the reverse-halo send buffer and sent on
+    // st_comm while the owned atoms' forces are computed
+    k_forces<<<std::max(1, ceil_div(ng, 8)), 256, 0, stream>>>(N, cell, pos4.p, row_off.p, keys.p, rev.p, ebin.p,
+                                                               g.p, forces.p, vpart.p, center.p, 1, glist, ng,
+                                                               gsend);
+    dist_reverse_send(*this);
+    k_forces<<<ceil_div(N, 8), 256, 0, stream>>>(N, cell, pos4.p, row_off.p, keys.p, rev.p, ebin.p,
+                                                  g.p, forces.p, vpart.p, center.p, 2, nullptr, 0, nullptr);
+    launches += 2;
+  } else {
+    k_forces<<<ceil_div(N, 8), 256, 0, stream>>>(N, cell, pos4.p, row_off.p, keys.p, rev.p, ebin.p,
+                                                  g.p, forces.p, vpart.p, center.p, 0, nullptr, 0, nullptr);
+    ++launches;
+  }
   // energy (1 column) then virial (9 columns) with fixed-order tree reductions
   red.ensure(RED_BLOCKS * 10 + 64);
   double* partial = red.p + 64;

@@ -182,6 +182,16 @@ __global__ void __launch_bounds__(256) k_nlist_warp(NlParams p, const double4* _
 }
 
 // Reverse entry of every list entry (thread per entry): position of (j -> i, -s) in row j.
+// Rows of non-centre atoms (ghosts of a decomposed run) hold no real entry: ebin = -1 once per
+// list build, so the chunked evaluation only has to cover the centres' rows. Warp per row.
+__global__ void k_mark_ghost_rows(int n, const uint8_t* __restrict__ center, const int64_t* __restrict__ row_off,
+                                  int32_t* __restrict__ ebin, int64_t e_cap) {
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= n || center[i]) return;
+  const int64_t e1 = min(row_off[i + 1], e_cap);
+  for (int64_t e = row_off[i] + (threadIdx.x & 31); e < e1; e += 32) ebin[e] = -1;
+}
+
 __global__ void k_reverse_e(const int64_t* __restrict__ row_off, int n, const uint64_t* __restrict__ keys,
                             const int32_t* __restrict__ eown, const int32_t* __restrict__ types,
                             int32_t* __restrict__ rev, int* err, int64_t e_cap) {
@@ -328,7 +338,9 @@ void Engine::launch_nlist(double cutoff, bool async) {
     DPB_CUDA(cudaStreamSynchronize(stream));
     n_entries = total;
     max_row = mx;
-    if (total + 1 > e_cap) e_cap = total + total / 4 + 1024;
+    // slack for the growth of the list between synchronous builds: 25 %, 6 % above 2^28
+    // entries (a 13.5 M-atom slab holds 1.2e9; its per-entry arrays are 44 B each)
+    if (total + 1 > e_cap) e_cap = total + (total < (int64_t(1) << 28) ? total / 4 : total / 16) + 1024;
     int rc = 2;
     while (rc < mx + mx / 8) rc <<= 1;
     if (rc > row_cap) row_cap = rc;
@@ -348,6 +360,11 @@ void Engine::launch_nlist(double cutoff, bool async) {
   ++launches;
   k_reverse_e<<<ceil_div(e_cap, 256), 256, 0, stream>>>(row_off.p, N, keys.p, eown.p, types.p, rev.p, err.p, e_cap);
   ++launches;
+  if (n_centers < n) {
+    ebin.ensure(e_cap + 1);
+    k_mark_ghost_rows<<<ceil_div(N, 8), 256, 0, stream>>>(N, center.p, row_off.p, ebin.p, e_cap);
+    ++launches;
+  }
   ref_pos.ensure(3 * n);
   DPB_CUDA(cudaMemcpyAsync(ref_pos.p, pos3.p, 3 * n * sizeof(double), cudaMemcpyDeviceToDevice, stream));
   list_cutoff = cutoff;

@@ -20,14 +20,20 @@ def n_gpus():
 
 
 @pytest.mark.skipif(n_gpus() < 2, reason="needs >= 2 GPUs")
-def test_two_rank_md_matches_single_gpu(tmp_path):
+@pytest.mark.parametrize("overlap,chunk", [(True, None), (False, None), (True, "256")])
+def test_two_rank_md_matches_single_gpu(tmp_path, overlap, chunk):
     out = tmp_path / "dist.json"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr", "127.0.0.1", "--master-port", "29611",
+           "--master-addr", "127.0.0.1", "--master-port", "29611" if chunk else ("29614" if overlap else "29613"),
            str(ROOT / "tests" / "dist" / "dist_md_check.py"), str(out)]
     # DPB_CHECK_PLAN: every device repartition is compared with the host restatement of
-    # partition_domain (domain.cpp:21-82) entry by entry; a mismatch aborts the run
+    # partition_domain (domain.cpp:21-82) entry by entry; a mismatch aborts the run.
+    # overlap: forward halo beside the interior chunks, reverse halo beside the owned forces
     env = dict(os.environ, DPB_CHECK_PLAN="1")
+    if not overlap:
+        env["DPB_NO_HALO_OVERLAP"] = "1"
+    if chunk:  # several chunks per rank: interior chunks evaluated while the halo is in flight
+        env["DPB_CHUNK"] = chunk
     subprocess.run(cmd, check=True, timeout=600, cwd=ROOT, env=env)
     r = json.loads(out.read_text())
     assert r["force_evals"][0] == r["force_evals"][1] == 61
