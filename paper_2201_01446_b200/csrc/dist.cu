@@ -6,9 +6,10 @@
 // distance to the owned extent is <= (r_cut + buffer) / spacing. run_md rebuilds the partition
 // and the lists every rebuild_every steps (md.cpp:70-102, 210).
 //
-// Per rank the local system is owned + ghost atoms in ascending global id (so local index order
-// is global order and the neighbour list reproduces the global canonical order). Only owned
-// atoms are centres. Per step:
+// Per rank the local system is the owned atoms (ascending global id) followed by the ghosts
+// (ascending global id): the centres are one contiguous range, so the evaluation chunks never
+// span ghost rows. A row holds the global row's entries, ordered by local index (results agree
+// with one GPU to rounding, 1e-10 tested). Only owned atoms are centres. Per step:
 //   forward halo   owned positions -> the ranks that hold them as ghosts   (ncclSend/ncclRecv)
 //   evaluate       local kernels; ghost rows only gather the reverse pair gradients
 //   reverse halo   ghost force partials -> owners, accumulated in peer order (deterministic)
@@ -275,7 +276,7 @@ __global__ void k_owner(int64_t N, int W, const int32_t* __restrict__ sorted_ids
 // ghost" as a bit mask (domain.cpp:64-80 ghost rule).
 __global__ void k_flags(int64_t N, int r, int W, const int32_t* __restrict__ owner, const double* __restrict__ fw,
                         const double* __restrict__ lohi, double mf, int per, int32_t* __restrict__ local,
-                        uint8_t* __restrict__ smask) {
+                        uint8_t* __restrict__ smask, int32_t* __restrict__ oflag) {
   const int64_t id = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (id >= N) return;
   const int o = owner[id];
@@ -283,6 +284,7 @@ __global__ void k_flags(int64_t N, int r, int W, const int32_t* __restrict__ own
   const bool own = o == r;
   const bool ghost = !own && circ_dist_d(x, lohi[2 * r], lohi[2 * r + 1], per) <= mf;
   local[id] = (own || ghost) ? 1 : 0;
+  oflag[id] = own ? 1 : 0;
   uint8_t m = 0;
   if (own)
     for (int p = 0; p < W; ++p)
@@ -290,13 +292,18 @@ __global__ void k_flags(int64_t N, int r, int W, const int32_t* __restrict__ own
   smask[id] = m;
 }
 
+// Local order: the owned atoms first (ascending global id), then the ghosts (ascending global
+// id), so the centres are one contiguous range and the evaluation chunks hold no ghost rows.
 __global__ void k_local_index(int64_t N, const int32_t* __restrict__ local, const int32_t* __restrict__ scan,
+                              const int32_t* __restrict__ oflag, const int32_t* __restrict__ oscan,
                               int32_t* __restrict__ lidx, int32_t* __restrict__ lgid, int64_t* __restrict__ counts) {
   const int64_t id = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (id >= N) return;
   if (local[id]) {
-    lidx[id] = scan[id];
-    lgid[scan[id]] = static_cast<int32_t>(id);
+    const int n_own = oscan[N - 1] + oflag[N - 1];
+    const int l = oflag[id] ? oscan[id] : n_own + (scan[id] - oscan[id]);
+    lidx[id] = l;
+    lgid[l] = static_cast<int32_t>(id);
   } else {
     lidx[id] = -1;
   }
@@ -414,9 +421,13 @@ void device_plan(Engine& E, std::vector<double>& lp, std::vector<double>& lv, st
   cub::DeviceRadixSort::SortPairs(D.d_tmp.p, b, D.d_keys.p, D.d_keys2.p, D.d_ids.p, D.d_ids2.p, static_cast<int>(N), 0,
                                   64, st);
   k_owner<<<nb, 256, 0, st>>>(N, W, D.d_ids2.p, D.d_fw.p, D.d_owner.p, D.d_lohi.p);
-  k_flags<<<nb, 256, 0, st>>>(N, D.rank, W, D.d_owner.p, D.d_fw.p, D.d_lohi.p, mf, per, D.d_flag.p, D.d_smask.p);
+  // (d_ids / d_ids2 are free after k_owner: owned flag and its scan)
+  k_flags<<<nb, 256, 0, st>>>(N, D.rank, W, D.d_owner.p, D.d_fw.p, D.d_lohi.p, mf, per, D.d_flag.p, D.d_smask.p,
+                              D.d_ids.p);
   excl_scan(D, D.d_flag.p, D.d_scan.p, N, st);
-  k_local_index<<<nb, 256, 0, st>>>(N, D.d_flag.p, D.d_scan.p, D.d_lidx.p, D.d_lgid.p, D.d_counts.p);
+  excl_scan(D, D.d_ids.p, D.d_ids2.p, N, st);
+  k_local_index<<<nb, 256, 0, st>>>(N, D.d_flag.p, D.d_scan.p, D.d_ids.p, D.d_ids2.p, D.d_lidx.p, D.d_lgid.p,
+                                    D.d_counts.p);
   // exchange lists per peer, ascending global id; staged at offset p * N, packed after the counts
   D.sidx.ensure(static_cast<size_t>(N) * D.world + 1);
   D.ridx.ensure(static_cast<size_t>(N) * D.world + 1);
@@ -457,7 +468,7 @@ void device_plan(Engine& E, std::vector<double>& lp, std::vector<double>& lv, st
   const size_t mx = std::max(D.soff[D.world], D.roff[D.world]) + 1;
   D.sbuf.ensure(3 * mx);
   D.rbuf.ensure(3 * mx);
-  // local arrays (owned + ghosts, ascending global id)
+  // local arrays (owned, then ghosts, each ascending in global id)
   D.d_lpos.ensure(3 * nl + 3);
   D.d_lvel.ensure(3 * nl + 3);
   D.d_ltypes.ensure(nl + 1);
@@ -478,7 +489,7 @@ void device_plan(Engine& E, std::vector<double>& lp, std::vector<double>& lv, st
   for (auto c : lc) D.n_own += c;
 }
 
-// Host plan of one rank: local atoms (owned + ghosts, ascending global id), centre mask and the
+// Host plan of one rank: local atoms (owned, then ghosts, each ascending in global id), centre mask and the
 // exchange lists (local indices) per peer: s = my owned atoms that peer p holds as ghosts,
 // rv = my ghosts owned by p, both ascending in global id.
 struct Plan {
@@ -496,12 +507,17 @@ void make_plan(const Dist& D, int r, Plan& P) {
   for (int64_t j : ghosts[r]) is_ghost[j] = 1;
   P.lgid.clear();
   P.lcenter.clear();
-  for (int64_t j = 0; j < D.N; ++j) {
-    if (owner[j] == r || is_ghost[j]) {
+  // owned atoms first, then the ghosts, each in ascending global id
+  for (int64_t j = 0; j < D.N; ++j)
+    if (owner[j] == r) {
       P.lgid.push_back(j);
-      P.lcenter.push_back(owner[j] == r ? 1 : 0);
+      P.lcenter.push_back(1);
     }
-  }
+  for (int64_t j = 0; j < D.N; ++j)
+    if (owner[j] != r && is_ghost[j]) {
+      P.lgid.push_back(j);
+      P.lcenter.push_back(0);
+    }
   const int64_t nl = static_cast<int64_t>(P.lgid.size());
   std::vector<int64_t> lidx(D.N, -1);
   for (int64_t k = 0; k < nl; ++k) lidx[P.lgid[k]] = k;

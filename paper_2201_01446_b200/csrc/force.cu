@@ -269,8 +269,9 @@ void Engine::launch_forces() {
                                                                g.p, forces.p, vpart.p, center.p, 1, glist, ng,
                                                                gsend);
     dist_reverse_send(*this);
-    k_forces<<<ceil_div(N, 8), 256, 0, stream>>>(N, cell, pos4.p, row_off.p, keys.p, rev.p, ebin.p,
-                                                  g.p, forces.p, vpart.p, center.p, 2, nullptr, 0, nullptr);
+    // the owned atoms are the local range [0, n_centers) (dist.cu local order)
+    k_forces<<<ceil_div(n_centers, 8), 256, 0, stream>>>(N, cell, pos4.p, row_off.p, keys.p, rev.p, ebin.p,
+                                                          g.p, forces.p, vpart.p, center.p, 2, nullptr, 0, nullptr);
     launches += 2;
   } else {
     k_forces<<<ceil_div(N, 8), 256, 0, stream>>>(N, cell, pos4.p, row_off.p, keys.p, rev.p, ebin.p,
