@@ -281,7 +281,8 @@ def run_ours(args, world, rank, local, dist):
     # roofline of the dominant kernel group: the fitting-net FP64 DMMA GEMMs
     fit_ms, fit_cnt = phases["fitting"]
     fit_flop_launch = fitting_flops_per_atom(m) * n
-    fit_launch_ms = fit_ms / max(fit_cnt, 1)
+    # one phase window per evaluation chunk (large systems run in chunks): per step = / nb
+    fit_launch_ms = fit_ms / max(nb, 1)
     mixed = args.precision == "mixed"
     if mixed:
         # 3xTF32: three tensor-core products per FP64-equivalent MAC, against the TF32 dense peak

@@ -90,6 +90,9 @@ __global__ void __launch_bounds__(256) k_env_fwd(TabParams p) {
 // ---------------------------------------------------------------- per-warp shared memory
 constexpr int HCAP = 256; // counting-sort bins; wider (type, interval) ranges use a bitonic sort
 constexpr int GB = 8;     // groups per batch
+#ifndef TAB_FWD_MINB
+#define TAB_FWD_MINB 6 // 2-warp CTAs per SM: 6 -> up to 168 registers (coefficient prefetch buffers)
+#endif
 
 struct FwdSmem {
   uint32_t* rk; // [scap] bin of real k (list order)
@@ -252,7 +255,7 @@ __device__ int sort_and_group(const FwdSmem& w, uint64_t* scratch, int nreal, in
 // ---------------------------------------------------------------- k_tab_fwd (warp per centre)
 // Features are owned in contiguous runs: lane l holds f = F*l .. F*l + F-1.
 template <int F>
-__global__ void __launch_bounds__(64, 8) k_tab_fwd(TabParams p) {
+__global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
@@ -269,9 +272,11 @@ __global__ void __launch_bounds__(64, 8) k_tab_fwd(TabParams p) {
     __syncwarp();
     // --- compaction of the reals (list order), per-type counts ---
     int nreal = 0, kmin = 0x7fffffff, kmax = -1;
+    int bin_nx = lane < len ? p.ebin[off + lane] : -1; // next 32 bins in flight
     for (int base = 0; base < len; base += 32) {
       const int e = base + lane;
-      const int bin = e < len ? p.ebin[off + e] : -1;
+      const int bin = bin_nx;
+      if (base + 32 < len) bin_nx = e + 32 < len ? p.ebin[off + e + 32] : -1;
       const bool real = bin >= 0;
       const unsigned m = __ballot_sync(0xffffffffu, real);
       const int t = real ? bin / p.tn : -1;
@@ -311,7 +316,29 @@ __global__ void __launch_bounds__(64, 8) k_tab_fwd(TabParams p) {
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int q = 0; q < F; ++q) tacc[a][q] = 0.0;
+    // coefficient rows of the next group are loaded while the current one is contracted (and the
+    // first group of a batch while its moments are accumulated): the contraction was waiting on
+    // these L2 loads (long-scoreboard stalls, ncu source view)
+    double cn[6][F];
+    auto load_c = [&](int gidx) {
+      const double* C = p.tab + static_cast<size_t>(w.gb[gidx]) * istride + f0;
+#pragma unroll
+      for (int mm = 0; mm < 6; ++mm) {
+        if constexpr (F % 2 == 0) {
+#pragma unroll
+          for (int q = 0; q < F; q += 2) {
+            const double2 v = __ldg(reinterpret_cast<const double2*>(C + mm * p.Mp + q));
+            cn[mm][q] = v.x;
+            cn[mm][q + 1] = v.y;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < F; ++q) cn[mm][q] = __ldg(C + mm * p.Mp + q);
+        }
+      }
+    };
     for (int g0 = 0; g0 < G; g0 += GB) {
+      load_c(g0);
       {
         // 4 lanes per group split its members; reduce-scatter leaves lane r with W[a = r][0..5]
         const int gl = lane >> 2, r = lane & 3;
@@ -321,16 +348,31 @@ __global__ void __launch_bounds__(64, 8) k_tab_fwd(TabParams p) {
         for (int k = 0; k < 24; ++k) Wv[k] = 0.0;
         if (g < G) {
           const int j1 = w.gs[g + 1];
-          for (int j = w.gs[g] + r; j < j1; j += 4) {
+          // members j, j + 4 of this lane loaded together (two gathers in flight), accumulated in
+          // member order
+          for (int j = w.gs[g] + r; j < j1; j += 8) {
+            const bool two = j + 4 < j1;
             const int64_t e = loff + w.ex[w.od[j]];
+            const int64_t e2 = two ? loff + w.ex[w.od[j + 4]] : e;
             const double R[4] = {p.erc[e], p.erc[p.es + e], p.erc[2 * p.es + e], p.erc[3 * p.es + e]};
             const double uu = p.erc[4 * p.es + e];
+            const double R2[4] = {p.erc[e2], p.erc[p.es + e2], p.erc[2 * p.es + e2], p.erc[3 * p.es + e2]};
+            const double uu2 = p.erc[4 * p.es + e2];
             double um = 1.0;
 #pragma unroll
             for (int mm = 0; mm < 6; ++mm) {
 #pragma unroll
               for (int a = 0; a < 4; ++a) Wv[a * 6 + mm] += R[a] * um;
               um *= uu;
+            }
+            if (two) {
+              um = 1.0;
+#pragma unroll
+              for (int mm = 0; mm < 6; ++mm) {
+#pragma unroll
+                for (int a = 0; a < 4; ++a) Wv[a * 6 + mm] += R2[a] * um;
+                um *= uu2;
+              }
             }
           }
         }
@@ -359,23 +401,13 @@ __global__ void __launch_bounds__(64, 8) k_tab_fwd(TabParams p) {
       __syncwarp();
       const int gn = min(GB, G - g0);
       for (int gg = 0; gg < gn; ++gg) {
-        const double* C = p.tab + static_cast<size_t>(w.gb[g0 + gg]) * istride + f0;
         const double* Wg = w.W + gg * 24;
         double c[6][F];
 #pragma unroll
-        for (int mm = 0; mm < 6; ++mm) {
-          if constexpr (F % 2 == 0) {
+        for (int mm = 0; mm < 6; ++mm)
 #pragma unroll
-            for (int q = 0; q < F; q += 2) {
-              const double2 v = __ldg(reinterpret_cast<const double2*>(C + mm * p.Mp + q));
-              c[mm][q] = v.x;
-              c[mm][q + 1] = v.y;
-            }
-          } else {
-#pragma unroll
-            for (int q = 0; q < F; ++q) c[mm][q] = __ldg(C + mm * p.Mp + q);
-          }
-        }
+          for (int q = 0; q < F; ++q) c[mm][q] = cn[mm][q];
+        if (gg + 1 < gn) load_c(g0 + gg + 1);
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
 #pragma unroll

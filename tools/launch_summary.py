@@ -9,7 +9,7 @@ for r in rows:
         d = dict(zip(hdr, r))
         if d['Metric Name'] != 'gpu__time_duration.sum': continue
         v = float(d['Metric Value'].replace(',', '')); u = d['Metric Unit']
-        v = v / 1e3 if u == 'nsecond' else (v * 1e3 if u == 'msecond' else v)
+        v = v / 1e3 if u in ('nsecond', 'ns') else (v * 1e3 if u in ('msecond', 'ms') else v)
         k = d['Kernel Name'].split('(')[0][-48:]
         agg[k][0] += 1; agg[k][1] += v
 tot = sum(v[1] for v in agg.values())

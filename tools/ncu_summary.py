@@ -12,10 +12,15 @@ txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", "
                      capture_output=True, text=True).stdout
 r = list(csv.reader(txt.splitlines()))
 h = r[0]
+units = r[1]
+tu = units[h.index('gpu__time_duration.sum')]
+scale = {'ns': 1e-6, 'nsecond': 1e-6, 'us': 1e-3, 'usecond': 1e-3, 'ms': 1.0, 'msecond': 1.0}.get(tu, 1.0)
 lines = [f"# {title}", "%-34s " % "kernel" + " ".join("%11s" % s for s in short)]
 for x in r[2:]:
     k = x[h.index('Kernel Name')].split('(')[0].replace('void ', '').replace('dpb::', '').replace('<unnamed>::', '')
     k = k.replace('(anonymous namespace)::', '')[-34:]
-    lines.append("%-34s " % k + " ".join("%11s" % x[h.index(c)][:10] for c in cols))
+    vals = [x[h.index(c)] for c in cols]
+    vals[0] = "%.4f" % (float(vals[0].replace(',', '')) * scale)
+    lines.append("%-34s " % k + " ".join("%11s" % v[:10] for v in vals))
 open(out, "w").write("\n".join(lines) + "\n")
 print("\n".join(lines))
