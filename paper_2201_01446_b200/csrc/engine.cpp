@@ -64,6 +64,7 @@ void Engine::upload_tables(const dp_table_desc& tdr) {
     }
   tab.ensure(tbuf.size());
   DPB_CUDA(cudaMemcpy(tab.p, tbuf.data(), tbuf.size() * sizeof(double), cudaMemcpyHostToDevice));
+  ++tab_ver;
   tab_block = B;
   pbuf_cap = 0;
 }

@@ -113,7 +113,9 @@ struct Engine {
   DevBuf<unsigned long long> exact_ctr;
   DevBuf<double> dTbuf;  // [n][4][Mp] adjoint of T (tabulate backward)
   DevBuf<int> fb_list;   // atom blocks left to the per-warp projection kernel (+ count)
-  DevBuf<float> tab32; // mixed mode copy
+  DevBuf<float> tab32; // mixed mode: FP32 copy of tab for the forward contraction
+  uint64_t tab_ver = 0, tab32_ver = ~0ull; // tab32 is refreshed when tab changes
+  void ensure_tab32();
   // fitting weights per type and layer: wt = W^T [outp][inp], w = W [inp][outp]
   std::vector<DevBuf<double>> fit_wt, fit_w, fit_b;
   std::vector<DevBuf<double>> fit_wout;

@@ -618,6 +618,7 @@ void Engine::build_tables_gpu(double step, uint64_t* n_out, double* x_end_out, d
                         cudaMemcpyDeviceToHost));
   if (install) {
     tab.ensure(static_cast<size_t>(n_types) * n * 6 * Mp);
+    ++tab_ver;
     DPB_CUDA(cudaMemcpyAsync(tab.p, eng.p, static_cast<size_t>(n_types) * n * 6 * Mp * sizeof(double),
                              cudaMemcpyDeviceToDevice, stream));
     tab_x0 = x0;

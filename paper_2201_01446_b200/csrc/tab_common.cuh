@@ -26,6 +26,7 @@ struct TabParams {
   double* Pbuf;         // [sum groups][24]
   int64_t pcap;         // groups Pbuf can hold
   const double* tab;    // [type][interval][6][Mp]
+  const float* tab32;   // the same in FP32 (mixed mode forward contraction) or null
   const int* max_nbr;
   DevCell c;
   double rc2, rs, rc;
@@ -211,6 +212,7 @@ inline TabParams make_params(Engine& E) {
   p.Pbuf = E.Pbuf.p;
   p.pcap = E.pbuf_cap;
   p.tab = E.tab.p;
+  p.tab32 = E.precision == 1 ? E.tab32.p : nullptr;
   p.max_nbr = E.d_max_nbr.p;
   p.c = E.cell;
   p.rc2 = E.r_cut * E.r_cut;

@@ -254,8 +254,12 @@ __device__ int sort_and_group(const FwdSmem& w, uint64_t* scratch, int nreal, in
 
 // ---------------------------------------------------------------- k_tab_fwd (warp per centre)
 // Features are owned in contiguous runs: lane l holds f = F*l .. F*l + F-1.
-template <int F>
+// F32 (mixed mode, SURVEY §8d C3 "mixed-precision tabulate_fusion"): the contraction T += W . C
+// runs on FP32 coefficients and accumulators (half the coefficient traffic, 2x the FP64 rate);
+// the moments W stay FP64. FP64 mode (F32 = false) is the parity path.
+template <int F, bool F32 = false>
 __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
+  using acc_t = typename std::conditional<F32, float, double>::type;
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
@@ -311,29 +315,49 @@ __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
       for (int j = w.gs[g]; j < w.gs[g + 1]; ++j) p.egrp[loff + w.ex[w.od[j]]] = g;
     }
     // --- moments of each (type, interval) group, then T += W . C[interval] ---
-    double tacc[4][F];
+    acc_t tacc[4][F];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int q = 0; q < F; ++q) tacc[a][q] = 0.0;
+      for (int q = 0; q < F; ++q) tacc[a][q] = acc_t(0);
     // coefficient rows of the next group are loaded while the current one is contracted (and the
     // first group of a batch while its moments are accumulated): the contraction was waiting on
     // these L2 loads (long-scoreboard stalls, ncu source view)
-    double cn[6][F];
+    acc_t cn[6][F];
     auto load_c = [&](int gidx) {
-      const double* C = p.tab + static_cast<size_t>(w.gb[gidx]) * istride + f0;
+      if constexpr (F32) {
+        const float* C = p.tab32 + static_cast<size_t>(w.gb[gidx]) * istride + f0;
+#pragma unroll
+        for (int mm = 0; mm < 6; ++mm) {
+          if constexpr (F % 4 == 0) {
+#pragma unroll
+            for (int q = 0; q < F; q += 4) {
+              const float4 v = __ldg(reinterpret_cast<const float4*>(C + mm * p.Mp + q));
+              cn[mm][q] = v.x;
+              cn[mm][q + 1] = v.y;
+              cn[mm][q + 2] = v.z;
+              cn[mm][q + 3] = v.w;
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < F; ++q) cn[mm][q] = __ldg(C + mm * p.Mp + q);
+          }
+        }
+        return;
+      }
+      const double* C = reinterpret_cast<const double*>(p.tab) + static_cast<size_t>(w.gb[gidx]) * istride + f0;
 #pragma unroll
       for (int mm = 0; mm < 6; ++mm) {
         if constexpr (F % 2 == 0) {
 #pragma unroll
           for (int q = 0; q < F; q += 2) {
             const double2 v = __ldg(reinterpret_cast<const double2*>(C + mm * p.Mp + q));
-            cn[mm][q] = v.x;
-            cn[mm][q + 1] = v.y;
+            cn[mm][q] = static_cast<acc_t>(v.x);
+            cn[mm][q + 1] = static_cast<acc_t>(v.y);
           }
         } else {
 #pragma unroll
-          for (int q = 0; q < F; ++q) cn[mm][q] = __ldg(C + mm * p.Mp + q);
+          for (int q = 0; q < F; ++q) cn[mm][q] = static_cast<acc_t>(__ldg(C + mm * p.Mp + q));
         }
       }
     };
@@ -402,7 +426,7 @@ __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
       const int gn = min(GB, G - g0);
       for (int gg = 0; gg < gn; ++gg) {
         const double* Wg = w.W + gg * 24;
-        double c[6][F];
+        acc_t c[6][F];
 #pragma unroll
         for (int mm = 0; mm < 6; ++mm)
 #pragma unroll
@@ -412,7 +436,7 @@ __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
         for (int a = 0; a < 4; ++a) {
 #pragma unroll
           for (int mm = 0; mm < 6; ++mm) {
-            const double wa = Wg[a * 6 + mm];
+            const acc_t wa = static_cast<acc_t>(Wg[a * 6 + mm]);
 #pragma unroll
             for (int q = 0; q < F; ++q) tacc[a][q] += wa * c[mm][q];
           }
@@ -957,15 +981,26 @@ int sm_count(int dev) {
   return s > 0 ? s : 148;
 }
 
-template <int F>
-void launch_fwd_warp(const TabParams& p, cudaStream_t st, int sms) {
+template <int F, bool F32>
+void launch_fwd_warp2(const TabParams& p, cudaStream_t st, int sms) {
   const size_t bytes = 2 * fwd_smem_bytes(p.scap, p.Mp);
   if (bytes > 227 * 1024) throw NumErr("neighbour rows too long for the tabulate kernel");
-  DPB_CUDA(cudaFuncSetAttribute(k_tab_fwd<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  DPB_CUDA(cudaFuncSetAttribute(k_tab_fwd<F, F32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(bytes)));
   const int blocks = std::max(1, std::min(ceil_div(p.i1 - p.i0, 2), sms * 32));
-  k_tab_fwd<F><<<blocks, 64, bytes, st>>>(p);
+  k_tab_fwd<F, F32><<<blocks, 64, bytes, st>>>(p);
   DPB_CUDA(cudaGetLastError());
+}
+
+template <int F>
+void launch_fwd_warp(const TabParams& p, cudaStream_t st, int sms) {
+  if (p.tab32) launch_fwd_warp2<F, true>(p, st, sms);
+  else launch_fwd_warp2<F, false>(p, st, sms);
+}
+
+__global__ void k_to_f32(int64_t n, const double* __restrict__ x, float* __restrict__ y) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) y[i] = static_cast<float>(x[i]);
 }
 
 template <int F>
@@ -1014,7 +1049,18 @@ void env_range(Engine& E, const TabParams& p, cudaStream_t st) {
 
 // env + k_tab_fwd over centres [i0, i1) of chunk k, then the group offsets of the chunk
 // (goff[i0..i1) start at 0; the chunk's buffer set owns Pbuf[set * pbuf_cap ...]).
+// FP32 copy of the coefficient table for the mixed-mode forward contraction
+void Engine::ensure_tab32() {
+  if (precision != 1 || tab32_ver == tab_ver) return;
+  const int64_t cnt = static_cast<int64_t>(n_types) * static_cast<int64_t>(tab_n) * 6 * Mp;
+  tab32.ensure(cnt);
+  k_to_f32<<<ceil_div(cnt, 256), 256, 0, stream>>>(cnt, tab.p, tab32.p);
+  DPB_CUDA(cudaStreamSynchronize(stream));
+  tab32_ver = tab_ver;
+}
+
 void Engine::tab_fwd_range(int k, int64_t i0, int64_t i1, cudaStream_t st) {
+  ensure_tab32();
   TabParams p = chunk_params(*this, i0, i1);
   env_range(*this, p, st);
   const int sms = sm_count(device);
