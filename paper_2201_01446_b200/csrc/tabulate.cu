@@ -91,7 +91,13 @@ __global__ void __launch_bounds__(256) k_env_fwd(TabParams p) {
 constexpr int HCAP = 256; // counting-sort bins; wider (type, interval) ranges use a bitonic sort
 constexpr int GB = 8;     // groups per batch
 #ifndef TAB_FWD_MINB
-#define TAB_FWD_MINB 6 // 2-warp CTAs per SM: 6 -> up to 168 registers (coefficient prefetch buffers)
+#define TAB_FWD_MINB 8 // 2-warp CTAs per SM: 128 registers, 16 warps per SM
+#endif
+#ifndef TAB_EBIN_PREFETCH
+#define TAB_EBIN_PREFETCH 1
+#endif
+#ifndef TAB_MOMENT_PAIR
+#define TAB_MOMENT_PAIR 1 // members per lane iteration of the moment sums (2: two gathers in flight, measured neutral)
 #endif
 
 struct FwdSmem {
@@ -276,11 +282,17 @@ __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
     __syncwarp();
     // --- compaction of the reals (list order), per-type counts ---
     int nreal = 0, kmin = 0x7fffffff, kmax = -1;
+#if TAB_EBIN_PREFETCH
     int bin_nx = lane < len ? p.ebin[off + lane] : -1; // next 32 bins in flight
+#endif
     for (int base = 0; base < len; base += 32) {
       const int e = base + lane;
+#if TAB_EBIN_PREFETCH
       const int bin = bin_nx;
       if (base + 32 < len) bin_nx = e + 32 < len ? p.ebin[off + e + 32] : -1;
+#else
+      const int bin = e < len ? p.ebin[off + e] : -1;
+#endif
       const bool real = bin >= 0;
       const unsigned m = __ballot_sync(0xffffffffu, real);
       const int t = real ? bin / p.tn : -1;
@@ -320,11 +332,9 @@ __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int q = 0; q < F; ++q) tacc[a][q] = acc_t(0);
-    // coefficient rows of the next group are loaded while the current one is contracted (and the
-    // first group of a batch while its moments are accumulated): the contraction was waiting on
-    // these L2 loads (long-scoreboard stalls, ncu source view)
-    acc_t cn[6][F];
-    auto load_c = [&](int gidx) {
+    // coefficient rows of one group (a register prefetch of the next group was measured: it
+    // raised the kernel to 168 registers, 12 instead of 16 warps per SM, and ran 3 % slower)
+    auto load_c = [&](int gidx, acc_t (&cn)[6][F]) {
       if constexpr (F32) {
         const float* C = p.tab32 + static_cast<size_t>(w.gb[gidx]) * istride + f0;
 #pragma unroll
@@ -362,7 +372,6 @@ __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
       }
     };
     for (int g0 = 0; g0 < G; g0 += GB) {
-      load_c(g0);
       {
         // 4 lanes per group split its members; reduce-scatter leaves lane r with W[a = r][0..5]
         const int gl = lane >> 2, r = lane & 3;
@@ -374,8 +383,8 @@ __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
           const int j1 = w.gs[g + 1];
           // members j, j + 4 of this lane loaded together (two gathers in flight), accumulated in
           // member order
-          for (int j = w.gs[g] + r; j < j1; j += 8) {
-            const bool two = j + 4 < j1;
+          for (int j = w.gs[g] + r; j < j1; j += 4 * TAB_MOMENT_PAIR) {
+            const bool two = TAB_MOMENT_PAIR == 2 && j + 4 < j1;
             const int64_t e = loff + w.ex[w.od[j]];
             const int64_t e2 = two ? loff + w.ex[w.od[j + 4]] : e;
             const double R[4] = {p.erc[e], p.erc[p.es + e], p.erc[2 * p.es + e], p.erc[3 * p.es + e]};
@@ -427,11 +436,7 @@ __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
       for (int gg = 0; gg < gn; ++gg) {
         const double* Wg = w.W + gg * 24;
         acc_t c[6][F];
-#pragma unroll
-        for (int mm = 0; mm < 6; ++mm)
-#pragma unroll
-          for (int q = 0; q < F; ++q) c[mm][q] = cn[mm][q];
-        if (gg + 1 < gn) load_c(g0 + gg + 1);
+        load_c(g0 + gg, c);
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
 #pragma unroll
