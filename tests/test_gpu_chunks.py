@@ -108,3 +108,18 @@ def test_chunk_size_rejects_negative(cu):
     pot = dp.DeepPot(m, t)
     with pytest.raises(dp.InputError):
         pot.set_chunk_size(-1)
+
+
+def test_c3_chunk_size_bitwise_at_scale(cu):
+    """BASELINE C3 size (1,048,576 atoms): 8 chunks of 131,072 vs 32 of 32,768 centres, both on
+    two streams, bitwise equal; forces sum to zero (a size-independent property)."""
+    m, t = cu
+    c = dp.gen_config("copper-like", 64, 64, 64, 0.1, 11)
+    pot = dp.DeepPot(m, t)
+    a = pot.compute(c)
+    pot.set_chunk_size(32768)
+    b = pot.compute(c)
+    same(a, b)
+    fsum = np.abs(a.forces.sum(axis=0)).max()
+    assert fsum <= 1e-9 * c.n_atoms * np.abs(a.forces).max()
+    pot.close()
