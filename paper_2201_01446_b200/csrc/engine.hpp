@@ -4,7 +4,7 @@
 //   types[n]           int32
 //   row_off[n+1]       int64 CSR offsets of the neighbour rows (list cutoff = r_cut + skin)
 //   keys[E]            uint64 packed (type_j, j, shift) -- rows sorted = type-sectored canonical
-//   rev[E]             int32 position of the reverse entry (j -> i, -s) inside row j
+//   rev[E]             uint32 global index of the reverse entry (j -> i, -s) (E < 2^32)
 //   skeys[E]           uint64 per-step real neighbours of each row sorted by (type, interval)
 //   T[n][4][Mp]        contraction T = sum_k R_k (x) G(s_k)
 //   D/dD[slots][K0p]   descriptor rows (fitting input / its gradient), slot = type-sorted atom
@@ -148,7 +148,7 @@ struct Engine {
   int row_cap = 0;        // row length capacity (power of two)
   DevBuf<int64_t> row_off;
   DevBuf<uint64_t> keys;
-  DevBuf<int32_t> rev;
+  DevBuf<uint32_t> rev; // global index of the reverse entry (one dependent load less in k_forces)
   DevBuf<int32_t> bin_of, bin_start, bin_atoms, bin_fill;
   DevBuf<double> frac;
   DevBuf<double> ref_pos;

@@ -19,10 +19,17 @@ namespace {
 // Only real entries (ebin >= 0) contribute; the k-th real term of the row (in list order, which
 // filtering by cutoff preserves) is always summed by lane k mod 32, so the result is bitwise
 // independent of the list cutoff, as the reference's is (SURVEY.md §8.1 pitfall 1).
-__global__ void __launch_bounds__(256) k_forces(int n, DevCell c, const double4* __restrict__ pos,
+#ifndef FORCES_PREFETCH
+#define FORCES_PREFETCH 1
+#endif
+#ifndef FORCES_MINB
+#define FORCES_MINB 3 // 3 CTAs (24 warps) per SM: 80 registers with the prefetch (91 uncapped ran 18 % slower)
+#endif
+
+__global__ void __launch_bounds__(256, FORCES_MINB) k_forces(int n, DevCell c, const double4* __restrict__ pos,
                                                 const int64_t* __restrict__ row_off,
                                                 const uint64_t* __restrict__ keys,
-                                                const int32_t* __restrict__ rev,
+                                                const uint32_t* __restrict__ rev,
                                                 const int32_t* __restrict__ ebin,
                                                 const double* __restrict__ g,
                                                 double* __restrict__ f, double* __restrict__ vpart,
@@ -48,16 +55,40 @@ __global__ void __launch_bounds__(256) k_forces(int n, DevCell c, const double4*
   for (int k = 0; k < 15; ++k) acc[k] = 0.0;
   const int64_t e0 = row_off[i], e1 = row_off[i + 1];
   int co = 0, cr = 0;
+#if FORCES_PREFETCH
+  // the next 32 entries' key / reverse index / own bin are loaded one iteration ahead
+  uint64_t key_n = 0;
+  int64_t m_n = 0;
+  int eo_n = -1;
+  if (e0 + lane < e1) {
+    key_n = keys[e0 + lane];
+    m_n = rev[e0 + lane];
+    eo_n = ebin[e0 + lane];
+  }
+#endif
   for (int64_t base = e0; base < e1; base += 32) {
     const int64_t e = base + lane;
     const bool valid = e < e1;
     double go[3] = {0.0, 0.0, 0.0}, gr[3] = {0.0, 0.0, 0.0}, d[3] = {0.0, 0.0, 0.0};
     bool fo = false, fr = false;
+#if FORCES_PREFETCH
+    const uint64_t key = key_n;
+    const int64_t m = m_n; // reverse entry (j -> i, -s), global index
+    const int eo = eo_n;
+    if (e + 32 < e1) {
+      key_n = keys[e + 32];
+      m_n = rev[e + 32];
+      eo_n = ebin[e + 32];
+    }
+#endif
     if (valid) {
+#if !FORCES_PREFETCH
       const uint64_t key = keys[e];
+      const int64_t m = rev[e]; // reverse entry (j -> i, -s), global index
+      const int eo = ebin[e];
+#endif
       const int j = key_j(key);
-      const int64_t m = row_off[j] + rev[e];
-      fo = ebin[e] >= 0;
+      fo = eo >= 0;
       fr = ebin[m] >= 0;
       if (fo) {
         go[0] = g[3 * e];

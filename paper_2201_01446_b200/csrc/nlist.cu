@@ -194,7 +194,7 @@ __global__ void k_mark_ghost_rows(int n, const uint8_t* __restrict__ center, con
 
 __global__ void k_reverse_e(const int64_t* __restrict__ row_off, int n, const uint64_t* __restrict__ keys,
                             const int32_t* __restrict__ eown, const int32_t* __restrict__ types,
-                            int32_t* __restrict__ rev, int* err, int64_t e_cap) {
+                            uint32_t* __restrict__ rev, int* err, int64_t e_cap) {
   const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (e >= e_cap || e >= row_off[n]) return;
   const int i = eown[e];
@@ -214,7 +214,7 @@ __global__ void k_reverse_e(const int64_t* __restrict__ row_off, int n, const ui
     raise_err(err, DEV_ROW_CAP);
     rev[e] = 0;
   } else {
-    rev[e] = static_cast<int32_t>(lo - r0);
+    rev[e] = static_cast<uint32_t>(lo);
   }
 }
 
@@ -347,6 +347,7 @@ void Engine::launch_nlist(double cutoff, bool async) {
   } else {
     n_entries = -1; // known on the device only (row_off[n])
   }
+  if (e_cap >= (int64_t(1) << 32)) throw NumErr("more than 2^32 neighbour entries on one GPU");
   keys.ensure(e_cap + 1);
   rev.ensure(e_cap + 1);
   eown.ensure(e_cap + 1);
