@@ -39,6 +39,7 @@ struct GemmArgs {
   double* dyout;      // [M][ldc]
   double* dzout;      // [M][ldc] or null
   int ldc, ldx, ldd; // ldd: pitch of dyin / tprev / dzout
+  int ntn, ntm;       // column / row tiles
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -68,10 +69,13 @@ __global__ void __launch_bounds__(128) k_gemm(GemmArgs g) {
   const int lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 1, wn = warp & 1;
   const int gid = lane >> 2, tig = lane & 3;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int KT = g.K / BK;
+  // persistent over tiles when the grid is capped (g.ntn column tiles x g.ntm row tiles): fewer
+  // resident CTAs per SM leave room for the other stream's tabulate kernels on the same SMs
+  for (int tile = blockIdx.x; tile < g.ntn * g.ntm; tile += gridDim.x) {
+  const int m0 = (tile / g.ntn) * BM, n0 = (tile % g.ntn) * BN;
   const double* A = g.A + static_cast<size_t>(m0) * g.lda;
   const double* B = g.Bt + static_cast<size_t>(n0) * g.ldb;
-  const int KT = g.K / BK;
 
   auto load_stage = [&](int stage, int kt) {
     const int k0 = kt * BK;
@@ -162,6 +166,8 @@ __global__ void __launch_bounds__(128) k_gemm(GemmArgs g) {
       }
     }
   }
+  __syncthreads(); // the next tile's prologue overwrites the stage buffers
+  }
 }
 
 // Readout: E = b_out + y . w_out (warp per row); dZ_L = w_out (1 - t^2); dY_L = w_out.
@@ -203,7 +209,17 @@ void launch_gemm(const GemmArgs& a, int rows, int N, cudaStream_t st) {
                                   static_cast<int>(bytes)));
     init = true;
   }
-  k_gemm<EPI, BN, STAGES><<<dim3(N / BN, rows / BM), 128, bytes, st>>>(a);
+  GemmArgs g = a;
+  g.ntn = N / BN;
+  g.ntm = rows / BM;
+  int tiles = g.ntn * g.ntm, grid = tiles;
+  static const int cap = std::getenv("DPB_GEMM_CTAS") ? std::atoi(std::getenv("DPB_GEMM_CTAS")) : 0;
+  if (cap > 0) {
+    static int sms = 0;
+    if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    grid = std::min(tiles, cap * (sms > 0 ? sms : 148));
+  }
+  k_gemm<EPI, BN, STAGES><<<grid, 128, bytes, st>>>(g);
   DPB_CUDA(cudaGetLastError());
 }
 
