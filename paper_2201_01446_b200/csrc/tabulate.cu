@@ -47,10 +47,12 @@ __global__ void __launch_bounds__(256) k_env_fwd(TabParams p) {
   const bool in_range = e < p.E && e < p.row_off[p.i1];
   if (in_range && el >= p.es) raise_err(p.err, DEV_LIST_CAP); // chunk entry capacity (never expected)
   const bool live = in_range && el < p.es;
-  if (live && !p.center[p.eown[e]]) p.ebin[e] = -1;
-  if (live && p.center[p.eown[e]]) {
-    const int i = p.eown[e];
-    const uint64_t key = p.keys[e];
+  // owner and key loaded together (independent), then the centre flag and the positions
+  const int i = live ? p.eown[e] : 0;
+  const uint64_t key = live ? p.keys[e] : 0;
+  const bool cen = live && p.center[i];
+  if (live && !cen) p.ebin[e] = -1;
+  if (cen) {
     int sh[3];
     key_shift(key, sh);
     double d[3];
@@ -934,14 +936,18 @@ __global__ void __launch_bounds__(256) k_tab_bwd_g(TabParams p) {
   const int64_t eb = p.row_off[p.i0];
   const int64_t e = eb + eo;
   if (e >= p.E || e >= p.row_off[p.i1]) return;
+  // bin, owner, group and key loaded together (independent; egrp is unset for non-real entries
+  // but inside the chunk buffer), so a real entry waits for one latency, not three
   const int bin = p.ebin[e];
+  const int i = p.eown[e];
+  const int grp = p.egrp[e - eb];
+  const uint64_t key = p.keys[e];
   double* ge = p.g + 3 * e;
   if (bin < 0) return; // never read: k_forces gathers only real entries (own and reverse)
-  const int i = p.eown[e];
+  const int64_t gi = p.goff[i] + grp;
   Env ev;
-  env_of(p, ld_pos(p.pos, i), p.keys[e], ev);
+  env_of(p, ld_pos(p.pos, i), key, ev);
   const int th = bin % p.tn;
-  const int64_t gi = p.goff[i] + p.egrp[e - eb];
   if (gi >= p.pcap) {
     raise_err(p.err, DEV_PBUF);
     ge[0] = ge[1] = ge[2] = 0.0;
