@@ -86,7 +86,7 @@ void Engine::create(const dp_model_desc* md, const dp_table_desc* td, int dev, i
   DPB_CUDA(cudaSetDevice(dev));
   DPB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   DPB_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
-  for (cudaEvent_t* e : {&ev_split, &ev_join, &ev_fwd[0], &ev_fwd[1], &ev_kd, &ev_halo, &ev_gf, &ev_rx})
+  for (cudaEvent_t* e : {&ev_join, &ev_fwd[0], &ev_fwd[1], &ev_kd, &ev_halo, &ev_gf, &ev_rx})
     DPB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   DPB_CUDA(cudaStreamCreateWithFlags(&st_comm, cudaStreamNonBlocking));
   n_types = md->n_types;
@@ -226,7 +226,7 @@ void Engine::destroy() {
     }
   if (stream) cudaStreamDestroy(stream);
   stream = nullptr;
-  for (cudaEvent_t* e : {&ev_split, &ev_join, &ev_fwd[0], &ev_fwd[1], &ev_kd, &ev_halo, &ev_gf, &ev_rx})
+  for (cudaEvent_t* e : {&ev_join, &ev_fwd[0], &ev_fwd[1], &ev_kd, &ev_halo, &ev_gf, &ev_rx})
     if (*e) {
       cudaEventDestroy(*e);
       *e = nullptr;

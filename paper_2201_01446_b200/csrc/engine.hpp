@@ -219,9 +219,9 @@ struct Engine {
   int64_t* h_gtotal = nullptr;  // pinned: total groups per chunk of the last evaluation
   static constexpr int MAX_CHUNKS = 4096;
   DevBuf<int64_t> gtot;
-  DevBuf<unsigned char> scan_tmp2;
-  cudaStream_t st2 = nullptr; // second half of a pipelined evaluation
-  cudaEvent_t ev_split = nullptr, ev_join = nullptr;
+  DevBuf<unsigned char> scan_tmp2; // scan scratch of buffer set 1
+  cudaStream_t st2 = nullptr; // odd chunks of a two-stream evaluation
+  cudaEvent_t ev_join = nullptr; // end of the second stream's chunks
   bool pipeline = std::getenv("DPB_NO_PIPELINE") == nullptr;
   void grow_pbuf();
   DevBuf<int32_t> n_real;
