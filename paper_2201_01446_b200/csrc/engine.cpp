@@ -198,7 +198,7 @@ void Engine::destroy() {
   types.release(); center.release(); slot_of.release(); atom_of.release(); row_off.release(); keys.release();
   rev.release(); bin_of.release(); bin_start.release(); bin_atoms.release(); bin_fill.release();
   frac.release(); ref_pos.release(); row_len.release(); nl_len.release(); scan_tmp.release();
-  skeys.release(); eown.release(); ebin.release(); egrp.release(); gbin.release(); erc.release(); n_grp.release(); goff.release(); Pbuf.release(); pbuf_cap = 0; n_real.release(); T.release(); D.release(); dD.release(); rel(act_t);
+  skeys.release(); eown.release(); ebin.release(); egrp.release(); gbin.release(); erc.release(); n_grp.release(); goff.release(); wbase.release(); wcnt.release(); Pbuf.release(); pbuf_cap = 0; n_real.release(); T.release(); D.release(); dD.release(); rel(act_t);
   rel(act_y); dz.release(); dy.release(); dz2.release(); dy2.release(); e_slot.release();
   e_atom.release(); g.release(); vpart.release(); forces.release();
   red.release(); counters.release(); err.release(); acc_fac.release();
@@ -420,6 +420,7 @@ void Engine::ensure_step_buffers() {
   n_real.ensure(n);
   n_grp.ensure(n + 1);
   goff.ensure(n + 1);
+  wbase.ensure(n + 1);
   pos4.ensure(n);
   pos3.ensure(3 * n);
 }

@@ -215,6 +215,9 @@ struct Engine {
   DevBuf<int32_t> n_grp;        // [n+1]
   DevBuf<int64_t> goff;         // [n+1]
   DevBuf<double> Pbuf;          // [groups][24]
+  DevBuf<int64_t> wbase;        // [n+1] forward moments: first Pbuf group of each centre
+  DevBuf<unsigned long long> wcnt; // [2] forward moments: group allocation counter per buffer set
+  bool t2_ok() const;           // forward contraction on the FP64 tensor pipe (k_tab_fwd_T2)
   int64_t pbuf_cap = 0;
   int64_t* h_gtotal = nullptr;  // pinned: total groups per chunk of the last evaluation
   static constexpr int MAX_CHUNKS = 4096;

@@ -25,6 +25,9 @@ struct TabParams {
   const int64_t* goff;  // [n+1] exclusive scan of n_grp
   double* Pbuf;         // [sum groups][24]
   int64_t pcap;         // groups Pbuf can hold
+  int64_t* wbase;       // [n] forward W-mode: first Pbuf group of each centre's moments (-1: none)
+  unsigned long long* wcnt; // forward W-mode: group allocation counter of the chunk
+  int count_only;       // forward W-mode: groups only (first evaluation sizes Pbuf from them)
   const double* tab;    // [type][interval][6][Mp]
   const float* tab32;   // the same in FP32 (mixed mode forward contraction) or null
   const int* max_nbr;
@@ -211,6 +214,9 @@ inline TabParams make_params(Engine& E) {
   p.goff = E.goff.p;
   p.Pbuf = E.Pbuf.p;
   p.pcap = E.pbuf_cap;
+  p.wbase = E.wbase.p;
+  p.wcnt = E.wcnt.p;
+  p.count_only = 0;
   p.tab = E.tab.p;
   p.tab32 = E.precision == 1 ? E.tab32.p : nullptr;
   p.max_nbr = E.d_max_nbr.p;

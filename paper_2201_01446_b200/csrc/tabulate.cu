@@ -265,7 +265,11 @@ __device__ int sort_and_group(const FwdSmem& w, uint64_t* scratch, int nreal, in
 // F32 (mixed mode, SURVEY §8d C3 "mixed-precision tabulate_fusion"): the contraction T += W . C
 // runs on FP32 coefficients and accumulators (half the coefficient traffic, 2x the FP64 rate);
 // the moments W stay FP64. FP64 mode (F32 = false) is the parity path.
-template <int F, bool F32 = false>
+// WM (FP64 W-mode): the kernel stops after the sort and the group moments, which it
+// writes to Pbuf[wbase[i] + g][a][m] (groups allocated per centre from p.wcnt); k_tab_fwd_T2 then
+// contracts them with the coefficients on the FP64 tensor pipe and forms T and D. p.count_only:
+// n_grp only (first evaluation of a system, to size Pbuf).
+template <int F, bool F32 = false, bool WM = false>
 __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
   using acc_t = typename std::conditional<F32, float, double>::type;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -316,9 +320,23 @@ __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
       if (w.tc[t] > p.max_nbr[t]) raise_err(p.err, DEV_OVERFLOW);
     const int G = sort_and_group(w, p.skeys + loff, nreal, kmin, kmax, lane);
     if (lane == 0) {
-      atomicAdd(p.counters + 0, static_cast<unsigned long long>(nreal));
+      if (!WM || !p.count_only) atomicAdd(p.counters + 0, static_cast<unsigned long long>(nreal));
       p.n_real[i] = nreal;
       p.n_grp[i] = G;
+    }
+    int64_t wb = -1;
+    if constexpr (WM) {
+      if (p.count_only) {
+        __syncwarp();
+        continue;
+      }
+      if (lane == 0) {
+        const int64_t b = static_cast<int64_t>(atomicAdd(p.wcnt, static_cast<unsigned long long>(G)));
+        if (b + G > p.pcap) raise_err(p.err, DEV_PBUF);
+        else wb = b;
+        p.wbase[i] = wb;
+      }
+      wb = __shfl_sync(0xffffffffu, wb, 0);
     }
     for (int j = lane; j < nreal; j += 32) {
       const int k = w.od[j];
@@ -327,6 +345,12 @@ __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
     for (int g = lane; g < G; g += 32) {
       p.gbin[loff + g] = w.gb[g];
       for (int j = w.gs[g]; j < w.gs[g + 1]; ++j) p.egrp[loff + w.ex[w.od[j]]] = g;
+    }
+    if constexpr (WM) {
+      if (wb < 0) {
+        __syncwarp();
+        continue;
+      }
     }
     // --- moments of each (type, interval) group, then T += W . C[interval] ---
     acc_t tacc[4][F];
@@ -429,6 +453,14 @@ __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
             Wv[k] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
           }
         }
+        if constexpr (WM) {
+          if (g < G) {
+            double* Wg = p.Pbuf + (wb + g) * 24 + r * 6;
+#pragma unroll
+            for (int mm = 0; mm < 6; mm += 2) *reinterpret_cast<double2*>(Wg + mm) = make_double2(Wv[mm], Wv[mm + 1]);
+          }
+          continue;
+        }
         if (g < G)
 #pragma unroll
           for (int mm = 0; mm < 6; ++mm) w.W[gl * 24 + r * 6 + mm] = Wv[mm];
@@ -450,6 +482,10 @@ __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
         }
       }
       __syncwarp();
+    }
+    if constexpr (WM) {
+      __syncwarp();
+      continue;
     }
     // --- T out, D = T<^T T (contract.hpp:9-17) ---
     double* ts = w.ts;
@@ -930,6 +966,306 @@ __global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double
   }
 }
 
+// ---------------------------------------------------------------- k_tab_fwd_T2 (CTA, FP64 tensor pipe)
+// The forward contraction T[(i,a)][p] = sum_groups sum_m W[i][g][a][m] C[bin(g)][m][p] of 32
+// consecutive centres at once (the mirror of k_tab_bwd_P2): the union of their intervals is staged
+// once in shared memory (cp.async, double-buffered, 4 intervals per stage) together with the
+// matching slice of the moments written by k_tab_fwd<WM>, and contracted on DMMA.8x8x4 with
+// rows = (centre, a), k = (interval, m), columns = features. Each interval occupies 8 k-rows
+// (6 coefficients + 2 zero rows), so a centre's sum runs over its own intervals in ascending order
+// whatever the other centres of the block touch (absent intervals add exact zeros, and m-tiles with
+// neither centre in an interval skip it): T is bitwise independent of the block composition and
+// hence of the chunking. The per-warp kernel streamed 6 KB of coefficients per (centre, interval)
+// through L1; here each staged interval serves all 32 centres. T goes out coalesced and
+// D = T<^T T (contract.hpp:9-17) is formed from the staged T. Blocks whose union exceeds T2_UCAP
+// intervals (fine tables) contract per warp from the same moments.
+constexpr int T2_NA = 32, T2_CB = 4, T2_UCAP = 128, T2_UW = T2_UCAP / 32, T2_BMW = 256, T2_AP = 36;
+constexpr int T2_THREADS = 512; // 16 warps, one m-tile (2 centres x 4 rows) each
+
+__host__ __device__ inline size_t t2_region_bytes(int Mp) {
+  const int pitch = Mp + 4;
+  const size_t stg = (static_cast<size_t>(2) * 8 * T2_CB * pitch + static_cast<size_t>(2) * 4 * T2_NA * T2_AP) * 8;
+  const size_t ts = static_cast<size_t>(T2_THREADS / 32) * 4 * (pitch - 4) * 8; // per-warp T (wide blocks)
+  return stg > ts ? stg : ts;
+}
+
+__host__ __device__ inline size_t t2_smem_bytes(int Mp) {
+  return t2_region_bytes(Mp) + T2_NA * sizeof(int64_t) +
+         (2 * T2_BMW + T2_UCAP + T2_NA / 2 * T2_UW + 4) * sizeof(int) + T2_NA * T2_UCAP * sizeof(int16_t);
+}
+
+template <int F>
+__global__ void __launch_bounds__(T2_THREADS, 1) k_tab_fwd_T2(TabParams p) {
+  constexpr int Mp = 32 * F, pitch = Mp + 4, units = Mp / 2, NT = Mp / 8, CR = 8 * T2_CB;
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* Cs = reinterpret_cast<double*>(smem);          // [2][CR][pitch] coefficient rows (k x features)
+  double* As = Cs + 2 * CR * pitch;                      // [2][128][AP] moments (rows x k)
+  int64_t* wb_s = reinterpret_cast<int64_t*>(smem + t2_region_bytes(Mp)); // [NA] first group in Pbuf
+  uint32_t* bm = reinterpret_cast<uint32_t*>(wb_s + T2_NA);              // [BMW] union bitmap
+  int* wpre = reinterpret_cast<int*>(bm + T2_BMW);                       // [BMW] popcount prefix
+  int* ubin = wpre + T2_BMW;                                             // [UCAP] union bins
+  uint32_t* mtmask = reinterpret_cast<uint32_t*>(ubin + T2_UCAP);        // [NA/2][UW] per m-tile union
+  int* misc = reinterpret_cast<int*>(mtmask + T2_NA / 2 * T2_UW);        // bmin, bmax, U
+  int16_t* gidx = reinterpret_cast<int16_t*>(misc + 4);                  // [NA][UCAP] group of slot or -1
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;         // warp = m-tile = centres 2w, 2w+1
+  const int gid = lane >> 2, tig = lane & 3;
+  const int nblk = (p.i1 - p.i0 + T2_NA - 1) / T2_NA;
+  const int64_t eb = p.row_off[p.i0];
+  for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const int i0 = p.i0 + blk * T2_NA;
+    const int na = min(T2_NA, p.i1 - i0);
+    if (tid == 0) {
+      misc[0] = 0x7fffffff;
+      misc[1] = -1;
+    }
+    for (int q = tid; q < T2_NA * T2_UCAP / 2; q += T2_THREADS) reinterpret_cast<int32_t*>(gidx)[q] = -1;
+    for (int q = tid; q < T2_NA / 2 * T2_UW; q += T2_THREADS) mtmask[q] = 0u;
+    if (tid < T2_NA) wb_s[tid] = tid < na ? p.wbase[i0 + tid] : -1;
+    __syncthreads();
+    if (tid < na) {
+      const int i = i0 + tid;
+      const int G = p.n_grp[i];
+      if (G > 0) {
+        const int32_t* gb = p.gbin + (p.row_off[i] - eb);
+        atomicMin(misc, gb[0]);
+        atomicMax(misc + 1, gb[G - 1]);
+      }
+    }
+    __syncthreads();
+    const int bmin = misc[0], bmax = misc[1];
+    const int range = bmax < 0 ? 0 : bmax - bmin + 1;
+    const int nw = (range + 31) >> 5;
+    const bool wide = nw > T2_BMW;
+    if (!wide)
+      for (int w = tid; w < nw; w += T2_THREADS) bm[w] = 0u;
+    __syncthreads();
+    if (!wide) {
+      for (int al = warp * 2; al < warp * 2 + 2 && al < na; ++al) {
+        const int i = i0 + al;
+        const int G = p.n_grp[i];
+        const int32_t* gb = p.gbin + (p.row_off[i] - eb);
+        for (int g = lane; g < G; g += 32) {
+          const int b = gb[g] - bmin;
+          atomicOr(bm + (b >> 5), 1u << (b & 31));
+        }
+      }
+    }
+    __syncthreads();
+    if (!wide && warp == 0) {
+      constexpr int PER = T2_BMW / 32;
+      int c[PER], s = 0;
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int w = lane * PER + k;
+        c[k] = w < nw ? __popc(bm[w]) : 0;
+        s += c[k];
+      }
+      int tot;
+      int ex = warp_excl_scan(s, lane, &tot);
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int w = lane * PER + k;
+        if (w < nw) {
+          wpre[w] = ex;
+          uint32_t bits = bm[w];
+          int at = ex;
+          while (bits) {
+            const int bit = __ffs(bits) - 1;
+            bits &= bits - 1;
+            if (at < T2_UCAP) ubin[at] = bmin + 32 * w + bit;
+            ++at;
+          }
+        }
+        ex += c[k];
+      }
+      if (lane == 0) misc[2] = tot;
+    }
+    __syncthreads();
+    const int U = range == 0 ? 0 : misc[2];
+    if (wide || U > T2_UCAP) {
+      // per-warp contraction from the moments (groups ascending, then a, m as k_tab_fwd); lanes
+      // own features f0 .. f0 + F - 1; T[a][0..Mp) of the centre staged per warp for D
+      const int f0 = F * lane;
+      double* ts = Cs + warp * 4 * Mp;
+      for (int al = warp * 2; al < warp * 2 + 2 && al < na; ++al) {
+        double tacc[4][F];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int q = 0; q < F; ++q) tacc[a][q] = 0.0;
+        const int i = i0 + al;
+        const int64_t wb = wb_s[al];
+        if (wb >= 0) {
+          const int G = p.n_grp[i];
+          const int32_t* gb = p.gbin + (p.row_off[i] - eb);
+          for (int g = 0; g < G; ++g) {
+            const double* C = p.tab + static_cast<size_t>(gb[g]) * 6 * Mp + f0;
+            const double* Wg = p.Pbuf + (wb + g) * 24;
+            double c[6][F];
+#pragma unroll
+            for (int mm = 0; mm < 6; ++mm)
+#pragma unroll
+              for (int q = 0; q < F; ++q) c[mm][q] = __ldg(C + mm * Mp + q);
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+              for (int mm = 0; mm < 6; ++mm) {
+                const double wa = Wg[a * 6 + mm];
+#pragma unroll
+                for (int q = 0; q < F; ++q) tacc[a][q] += wa * c[mm][q];
+              }
+          }
+        }
+        double* Ti = p.T + static_cast<size_t>(i) * 4 * Mp;
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int q = 0; q < F; ++q) {
+            Ti[a * Mp + f0 + q] = tacc[a][q];
+            ts[a * Mp + f0 + q] = tacc[a][q];
+          }
+        __syncwarp();
+        const int slot = p.slot_of[i];
+        if (slot >= 0 && f0 < p.M) {
+          double* Drow = p.D + static_cast<size_t>(slot) * p.K0p;
+          for (int qq = 0; qq < p.mlt; ++qq) {
+            const double t0 = ts[qq], t1 = ts[Mp + qq], t2 = ts[2 * Mp + qq], t3 = ts[3 * Mp + qq];
+#pragma unroll
+            for (int q = 0; q < F; ++q) {
+              double v = t0 * tacc[0][q];
+              v += t1 * tacc[1][q];
+              v += t2 * tacc[2][q];
+              v += t3 * tacc[3][q];
+              Drow[qq * p.M + f0 + q] = v;
+            }
+          }
+        }
+        __syncwarp();
+      }
+      __syncthreads();
+      continue;
+    }
+    // slot -> group of each centre, and the union each m-tile (2 centres) really needs
+    for (int al = warp * 2; al < warp * 2 + 2 && al < na; ++al) {
+      const int i = i0 + al;
+      const int G = p.n_grp[i];
+      const int32_t* gb = p.gbin + (p.row_off[i] - eb);
+      for (int g = lane; g < G; g += 32) {
+        const int b = gb[g] - bmin;
+        const int u = wpre[b >> 5] + __popc(bm[b >> 5] & ((1u << (b & 31)) - 1u));
+        gidx[al * T2_UCAP + u] = static_cast<int16_t>(g);
+        atomicOr(mtmask + (al >> 1) * T2_UW + (u >> 5), 1u << (u & 31));
+      }
+    }
+    __syncthreads();
+    const int nch = (U + T2_CB - 1) / T2_CB;
+    auto stage = [&](int ch, int buf) {
+      double* cdst = Cs + buf * CR * pitch;
+      for (int q = tid; q < CR * units; q += T2_THREADS) {
+        const int row = q / units, c2 = q % units;
+        const int u = ch * T2_CB + (row >> 3), m = row & 7;
+        double* dst = cdst + row * pitch + 2 * c2;
+        if (m < 6 && u < U)
+          tc::cp_async16(dst, p.tab + static_cast<size_t>(ubin[u]) * 6 * Mp + m * Mp + 2 * c2);
+        else
+          dst[0] = dst[1] = 0.0;
+      }
+      double* adst = As + buf * 4 * T2_NA * T2_AP;
+      for (int q = tid; q < 4 * T2_NA * T2_CB * 4; q += T2_THREADS) {
+        const int row = q >> 4, ul = (q >> 2) & 3, piece = q & 3;
+        const int al = row >> 2, a = row & 3;
+        const int u = ch * T2_CB + ul;
+        const int g = u < U ? gidx[al * T2_UCAP + u] : -1;
+        const int64_t wb = wb_s[al];
+        double* dst = adst + row * T2_AP + ul * 8 + piece * 2;
+        if (piece < 3 && g >= 0 && wb >= 0)
+          tc::cp_async16(dst, p.Pbuf + (wb + g) * 24 + a * 6 + piece * 2);
+        else
+          dst[0] = dst[1] = 0.0;
+      }
+      tc::cp_commit();
+    };
+    double acc[NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+    if (nch > 0) stage(0, 0);
+    for (int ch = 0; ch < nch; ++ch) {
+      if (ch + 1 < nch) {
+        stage(ch + 1, (ch + 1) & 1);
+        tc::cp_wait<1>();
+      } else {
+        tc::cp_wait<0>();
+      }
+      __syncthreads();
+      const double* cs = Cs + (ch & 1) * CR * pitch + tig * pitch + gid;
+      const double* as = As + (ch & 1) * 4 * T2_NA * T2_AP + (warp * 8 + gid) * T2_AP + tig;
+      const unsigned nm = (mtmask[warp * T2_UW + ((ch * T2_CB) >> 5)] >> ((ch * T2_CB) & 31)) & 15u;
+#pragma unroll
+      for (int ul = 0; ul < T2_CB; ++ul) {
+        if (!((nm >> ul) & 1u)) continue;
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          const int k0 = ul * 8 + ks * 4;
+          const double av = as[k0];
+          const double* bp = cs + k0 * pitch;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) dmma884(acc[nt][0], acc[nt][1], av, bp[nt * 8]);
+        }
+      }
+      __syncthreads();
+    }
+    // T out straight from the accumulators: row (centre 2w + gid / 4, a = gid % 4)
+    const int al_me = warp * 2 + (gid >> 2);
+    if (al_me < na) {
+      double* Tr = p.T + (static_cast<size_t>(i0) * 4 + warp * 8 + gid) * Mp + 2 * tig;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) *reinterpret_cast<double2*>(Tr + nt * 8) = make_double2(acc[nt][0], acc[nt][1]);
+    }
+    // D = T<^T T per centre (contract.hpp:9-17) on DMMA with k = a: the operand fragments
+    // B[a = tig][p = 8 nt + gid] = T[a][p] (and A[q][a] = B of tile q / 8) are shuffled out of the
+    // accumulators of the thread holding row (c, a) = 4 c + tig, columns 8 nt + 2 (gid / 2) + {0, 1}
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int al = warp * 2 + c;
+      if (al >= na) break;
+      const int slot = p.slot_of[i0 + al];
+      if (slot < 0) continue;
+      const int src = (4 * c + tig) * 4 + (gid >> 1);
+      const bool odd = gid & 1;
+      double* Drow = p.D + static_cast<size_t>(slot) * p.K0p;
+      for (int qt = 0; qt * 8 < p.mlt; ++qt) {
+        double aq = 0.0;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+          if (nt == qt) {
+            const double v0 = __shfl_sync(0xffffffffu, acc[nt][0], src);
+            const double v1 = __shfl_sync(0xffffffffu, acc[nt][1], src);
+            aq = odd ? v1 : v0;
+          }
+        const int q = qt * 8 + gid;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const double v0 = __shfl_sync(0xffffffffu, acc[nt][0], src);
+          const double v1 = __shfl_sync(0xffffffffu, acc[nt][1], src);
+          double d0 = 0.0, d1 = 0.0;
+          dmma884(d0, d1, aq, odd ? v1 : v0);
+          const int pc = nt * 8 + 2 * tig;
+          if (q < p.mlt) {
+            double* dst = Drow + q * p.M + pc;
+            if (pc + 1 < p.M && (p.M & 1) == 0) {
+              *reinterpret_cast<double2*>(dst) = make_double2(d0, d1);
+            } else {
+              if (pc < p.M) dst[0] = d0;
+              if (pc + 1 < p.M) dst[1] = d1;
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------- k_tab_bwd_g (thread per entry)
 __global__ void __launch_bounds__(256) k_tab_bwd_g(TabParams p) {
   const int64_t eo = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -1070,11 +1406,88 @@ void Engine::ensure_tab32() {
   tab32_ver = tab_ver;
 }
 
+// Opt-in (DPB_T2=1): measured at C2 the moments kernel + k_tab_fwd_T2 take 0.49 ms per 16k-centre
+// chunk against 0.46 ms for the per-warp k_tab_fwd with warm L2, and the 152 KB CTAs co-reside
+// worse with the other stream's GEMMs (5.23 vs 5.13 ms/step); DESIGN.md §9.
+bool Engine::t2_ok() const {
+  static const bool on = std::getenv("DPB_T2") != nullptr && std::getenv("DPB_T2")[0] == '1';
+  return on && precision == 0 && Mp <= 128;
+}
+
+template <int F>
+void launch_fwd_wm(const TabParams& p, cudaStream_t st, int sms) {
+  const size_t bytes = 2 * fwd_smem_bytes(p.scap, p.Mp);
+  if (bytes > 227 * 1024) throw NumErr("neighbour rows too long for the tabulate kernel");
+  DPB_CUDA(cudaFuncSetAttribute(k_tab_fwd<F, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(bytes)));
+  const int blocks = std::max(1, std::min(ceil_div(p.i1 - p.i0, 2), sms * 32));
+  k_tab_fwd<F, false, true><<<blocks, 64, bytes, st>>>(p);
+  DPB_CUDA(cudaGetLastError());
+}
+
+template <int F>
+void launch_fwd_t2(const TabParams& p, cudaStream_t st, int sms) {
+  const size_t bytes = t2_smem_bytes(32 * F);
+  DPB_CUDA(cudaFuncSetAttribute(k_tab_fwd_T2<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+  const int nblk = ceil_div(p.i1 - p.i0, T2_NA);
+  k_tab_fwd_T2<F><<<std::max(1, std::min(nblk, sms)), T2_THREADS, bytes, st>>>(p);
+  DPB_CUDA(cudaGetLastError());
+}
+
 void Engine::tab_fwd_range(int k, int64_t i0, int64_t i1, cudaStream_t st) {
   ensure_tab32();
   TabParams p = chunk_params(*this, i0, i1);
   env_range(*this, p, st);
   const int sms = sm_count(device);
+  // group offsets of the chunk -> goff, its total -> h_gtotal[k] (pinned, read at Pbuf sizing)
+  auto scan_groups = [&] {
+    DevBuf<unsigned char>& tmp = cur_set == 0 ? scan_tmp : scan_tmp2;
+    const int cnt = static_cast<int>(i1 - i0);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, n_grp.p + i0, goff.p + i0, cnt, st);
+    tmp.ensure(tb + 1);
+    cub::DeviceScan::ExclusiveSum(tmp.p, tb, n_grp.p + i0, goff.p + i0, cnt, st);
+    gtot.ensure(MAX_CHUNKS);
+    k_group_total<<<1, 32, 0, st>>>(n_grp.p, goff.p, static_cast<int>(i0), static_cast<int>(i1), gtot.p + k);
+    if (!h_gtotal) {
+      DPB_CUDA(cudaMallocHost(&h_gtotal, MAX_CHUNKS * sizeof(int64_t)));
+      std::memset(h_gtotal, 0, MAX_CHUNKS * sizeof(int64_t));
+    }
+    DPB_CUDA(cudaMemcpyAsync(h_gtotal + k, gtot.p + k, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    launches += 2;
+  };
+  if (t2_ok()) {
+    // moments (k_tab_fwd<WM>) into this chunk's Pbuf region, then the tensor-pipe contraction
+    auto wm = [&](const TabParams& q) {
+      switch (Mp / 32) {
+#define DPB_WM(F) case F: launch_fwd_wm<F>(q, st, sms); break;
+        DPB_WM(1) DPB_WM(2) DPB_WM(3) DPB_WM(4)
+#undef DPB_WM
+      }
+      ++launches;
+    };
+    if (pbuf_cap == 0) {
+      // first evaluation of this system/plan: exact group total of this chunk (one sync)
+      p.count_only = 1;
+      wm(p);
+      scan_groups();
+      DPB_CUDA(cudaStreamSynchronize(st));
+      grow_pbuf();
+      p = chunk_params(*this, i0, i1);
+    }
+    wcnt.ensure(2);
+    p.wcnt = wcnt.p + cur_set;
+    DPB_CUDA(cudaMemsetAsync(p.wcnt, 0, sizeof(unsigned long long), st));
+    wm(p);
+    switch (Mp / 32) {
+#define DPB_T2(F) case F: launch_fwd_t2<F>(p, st, sms); break;
+      DPB_T2(1) DPB_T2(2) DPB_T2(3) DPB_T2(4)
+#undef DPB_T2
+    }
+    ++launches;
+    scan_groups();
+    return;
+  }
   switch (Mp / 32) {
     case 1: launch_fwd_warp<1>(p, st, sms); break;
     case 2: launch_fwd_warp<2>(p, st, sms); break;
@@ -1087,20 +1500,7 @@ void Engine::tab_fwd_range(int k, int64_t i0, int64_t i1, cudaStream_t st) {
     default: throw InputErr("feature width 4*d1 must be at most 256");
   }
   ++launches;
-  DevBuf<unsigned char>& tmp = cur_set == 0 ? scan_tmp : scan_tmp2;
-  const int cnt = static_cast<int>(i1 - i0);
-  size_t tb = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tb, n_grp.p + i0, goff.p + i0, cnt, st);
-  tmp.ensure(tb + 1);
-  cub::DeviceScan::ExclusiveSum(tmp.p, tb, n_grp.p + i0, goff.p + i0, cnt, st);
-  gtot.ensure(MAX_CHUNKS);
-  k_group_total<<<1, 32, 0, st>>>(n_grp.p, goff.p, static_cast<int>(i0), static_cast<int>(i1), gtot.p + k);
-  if (!h_gtotal) {
-    DPB_CUDA(cudaMallocHost(&h_gtotal, MAX_CHUNKS * sizeof(int64_t)));
-    std::memset(h_gtotal, 0, MAX_CHUNKS * sizeof(int64_t));
-  }
-  DPB_CUDA(cudaMemcpyAsync(h_gtotal + k, gtot.p + k, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  launches += 2;
+  scan_groups();
 }
 
 void Engine::launch_tab_fwd() {
