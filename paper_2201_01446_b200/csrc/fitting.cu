@@ -60,7 +60,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 
 // BN = 64 (4 DMMA column tiles per warp) or 80 (5): 240-wide layers tile exactly with 80.
 template <int EPI, int BN, int STAGES>
-__global__ void __launch_bounds__(128) k_gemm(GemmArgs g) {
+__device__ __forceinline__ void gemm_body(const GemmArgs& g) {
   constexpr int NT = BN / 16; // 8-wide column tiles per warp (2 warps across BN)
   extern __shared__ __align__(16) double sm[];
   double* As = sm;                                // [STAGES][BM][PITCH]
@@ -170,6 +170,18 @@ __global__ void __launch_bounds__(128) k_gemm(GemmArgs g) {
   }
 }
 
+template <int EPI, int BN, int STAGES>
+__global__ void __launch_bounds__(128) k_gemm(GemmArgs g) {
+  gemm_body<EPI, BN, STAGES>(g);
+}
+
+// Short-K (240-wide hidden) layers capped at 128 registers: 4 CTAs (16 warps) per SM instead of 3
+// (C2 fitting phase 2.74 -> see DESIGN.md §3)
+template <int EPI, int BN, int STAGES>
+__global__ void __launch_bounds__(128, 4) k_gemm4(GemmArgs g) {
+  gemm_body<EPI, BN, STAGES>(g);
+}
+
 // Readout: E = b_out + y . w_out (warp per row); dZ_L = w_out (1 - t^2); dY_L = w_out.
 __global__ void k_readout(int rows, int ld, int width, const double* __restrict__ y,
                           const double* __restrict__ t, const double* __restrict__ wout,
@@ -203,10 +215,11 @@ __global__ void k_scatter_energy(int64_t slots, const int32_t* __restrict__ atom
 template <int EPI, int BN, int STAGES>
 void launch_gemm(const GemmArgs& a, int rows, int N, cudaStream_t st) {
   const size_t bytes = static_cast<size_t>(STAGES) * (BM + BN) * PITCH * sizeof(double);
+  static const bool four = BN == 80 && STAGES == 2 && std::getenv("DPB_GEMM_NO4") == nullptr;
+  auto kern = four ? k_gemm4<EPI, BN, STAGES> : k_gemm<EPI, BN, STAGES>;
   static bool init = false;
   if (!init) {
-    DPB_CUDA(cudaFuncSetAttribute(k_gemm<EPI, BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(bytes)));
+    DPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
     init = true;
   }
   GemmArgs g = a;
@@ -219,7 +232,7 @@ void launch_gemm(const GemmArgs& a, int rows, int N, cudaStream_t st) {
     if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     grid = std::min(tiles, cap * (sms > 0 ? sms : 148));
   }
-  k_gemm<EPI, BN, STAGES><<<grid, 128, bytes, st>>>(g);
+  kern<<<grid, 128, bytes, st>>>(g);
   DPB_CUDA(cudaGetLastError());
 }
 
