@@ -726,6 +726,7 @@ __global__ void __launch_bounds__(64, 6) k_tab_bwd_P(TabParams p, const double* 
 // here coefficient traffic drops by ~20x and the MACs run on the tensor pipe. Only the (centre,
 // interval) pairs the centre really has are written (Pbuf, same layout as the per-warp kernel).
 constexpr int P2_NA = 32, P2_CB = 4, P2_UCAP = 128, P2_UW = P2_UCAP / 32, P2_BMW = 256;
+constexpr int P2_THREADS = 512; // 16 warps, one m-tile (2 centres x 4 rows) each
 
 __host__ __device__ inline size_t p2_smem_bytes(int Mp) {
   const int pitch = Mp + 4;
@@ -740,7 +741,7 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 }
 
 template <int F>
-__global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double* __restrict__ dTg,
+__global__ void __launch_bounds__(P2_THREADS, 1) k_tab_bwd_P2(TabParams p, const double* __restrict__ dTg,
                                                        int* __restrict__ fb_list, int* __restrict__ fb_count) {
   constexpr int Mp = 32 * F, pitch = Mp + 4, units = Mp / 2;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -769,7 +770,7 @@ __global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double
   for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
     const int i0 = p.i0 + blk * P2_NA;
     // dT rows of the 32 centres (contiguous in dTg)
-    for (int q = tid; q < 4 * P2_NA * units; q += 256) {
+    for (int q = tid; q < 4 * P2_NA * units; q += P2_THREADS) {
       const int row = q / units, c2 = q % units;
       double* dst = dTs + row * pitch + 2 * c2;
       if (i0 + (row >> 2) < p.i1)
@@ -782,8 +783,8 @@ __global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double
       misc[0] = 0x7fffffff;
       misc[1] = -1;
     }
-    for (int q = tid; q < P2_NA * P2_UCAP / 2; q += 256) reinterpret_cast<int32_t*>(gidx)[q] = -1;
-    for (int q = tid; q < P2_NA / 2 * P2_UW; q += 256) mtmask[q] = 0u;
+    for (int q = tid; q < P2_NA * P2_UCAP / 2; q += P2_THREADS) reinterpret_cast<int32_t*>(gidx)[q] = -1;
+    for (int q = tid; q < P2_NA / 2 * P2_UW; q += P2_THREADS) mtmask[q] = 0u;
     __syncthreads();
     // interval range of the block: each centre's group bins are sorted (gbin, written by k_tab_fwd)
     if (tid < P2_NA && i0 + tid < p.i1) {
@@ -801,10 +802,10 @@ __global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double
     const int nw = (range + 31) >> 5;
     const bool wide = nw > P2_BMW;
     if (!wide)
-      for (int w = tid; w < nw; w += 256) bm[w] = 0u;
+      for (int w = tid; w < nw; w += P2_THREADS) bm[w] = 0u;
     __syncthreads();
     if (!wide) {
-      for (int al = warp * 4; al < warp * 4 + 4; ++al) {
+      for (int al = warp * 2; al < warp * 2 + 2; ++al) {
         const int i = i0 + al;
         if (i >= p.i1) break;
         const int G = p.n_grp[i];
@@ -855,7 +856,7 @@ __global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double
       continue;
     }
     // slot -> group of each centre, and the union each m-tile (2 centres) really needs
-    for (int al = warp * 4; al < warp * 4 + 4; ++al) {
+    for (int al = warp * 2; al < warp * 2 + 2; ++al) {
       const int i = i0 + al;
       if (i >= p.i1) break;
       const int G = p.n_grp[i];
@@ -867,13 +868,13 @@ __global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double
         atomicOr(mtmask + (al >> 1) * P2_UW + (u >> 5), 1u << (u & 31));
       }
     }
-    // this thread's two output rows (one per m-tile): centre, component, group base
-    int r_al[2], r_a[2];
-    int64_t r_base[2];
-    bool r_ok[2];
+    // this thread's output row (the warp's m-tile): centre, component, group base
+    int r_al[1], r_a[1];
+    int64_t r_base[1];
+    bool r_ok[1];
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt) {
-      const int r = warp * 16 + mt * 8 + gid;
+    for (int mt = 0; mt < 1; ++mt) {
+      const int r = warp * 8 + gid;
       r_al[mt] = r >> 2;
       r_a[mt] = r & 3;
       const int i = i0 + r_al[mt];
@@ -888,7 +889,7 @@ __global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double
     const int nch = (U + P2_CB - 1) / P2_CB;
     auto stage = [&](int ch, int buf) {
       double* dst0 = Cs + buf * 6 * P2_CB * pitch;
-      for (int q = tid; q < 6 * P2_CB * units; q += 256) {
+      for (int q = tid; q < 6 * P2_CB * units; q += P2_THREADS) {
         const int row = q / units, c2 = q % units;
         const int u = ch * P2_CB + row / 6, m = row % 6;
         double* dst = dst0 + row * pitch + 2 * c2;
@@ -909,48 +910,38 @@ __global__ void __launch_bounds__(256, 1) k_tab_bwd_P2(TabParams p, const double
       }
       __syncthreads();
       const double* cs = Cs + (ch & 1) * 6 * P2_CB * pitch;
-      double acc[2][3][2];
+      double acc[1][3][2];
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < 3; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-      const double* a0 = dTs + (warp * 16 + gid) * pitch + tig;
+      for (int nt = 0; nt < 3; ++nt) acc[0][nt][0] = acc[0][nt][1] = 0.0;
+      const double* a0 = dTs + (warp * 8 + gid) * pitch + tig;
       const double* b0 = cs + gid * pitch + tig;
-      // n-tile nt covers chunk slots {nt, nt+1} (columns 8 nt .. 8 nt + 7 of 6 per slot); an m-tile
-      // needs it only if one of its two centres has one of those intervals
+      // n-tile nt covers chunk slots {nt, nt+1} (columns 8 nt .. 8 nt + 7 of 6 per slot); the
+      // m-tile needs it only if one of its two centres has one of those intervals
       const int sh = (ch * P2_CB) & 31, wd = (ch * P2_CB) >> 5;
-      const unsigned n0 = (mtmask[(2 * warp) * P2_UW + wd] >> sh) & 15u;
-      const unsigned n1 = (mtmask[(2 * warp + 1) * P2_UW + wd] >> sh) & 15u;
-      const unsigned use = ((n0 & 3u) ? 1u : 0u) | ((n0 & 6u) ? 2u : 0u) | ((n0 & 12u) ? 4u : 0u) |
-                           ((n1 & 3u) ? 8u : 0u) | ((n1 & 6u) ? 16u : 0u) | ((n1 & 12u) ? 32u : 0u);
-      if (use == 0x3fu) {
+      const unsigned n0 = (mtmask[warp * P2_UW + wd] >> sh) & 15u;
+      const unsigned use = ((n0 & 3u) ? 1u : 0u) | ((n0 & 6u) ? 2u : 0u) | ((n0 & 12u) ? 4u : 0u);
+      if (use == 7u) {
 #pragma unroll 4
         for (int k = 0; k < Mp; k += 4) {
-          const double av0 = a0[k], av1 = a0[8 * pitch + k];
+          const double av0 = a0[k];
           const double bv0 = b0[k], bv1 = b0[8 * pitch + k], bv2 = b0[16 * pitch + k];
           dmma884(acc[0][0][0], acc[0][0][1], av0, bv0);
           dmma884(acc[0][1][0], acc[0][1][1], av0, bv1);
           dmma884(acc[0][2][0], acc[0][2][1], av0, bv2);
-          dmma884(acc[1][0][0], acc[1][0][1], av1, bv0);
-          dmma884(acc[1][1][0], acc[1][1][1], av1, bv1);
-          dmma884(acc[1][2][0], acc[1][2][1], av1, bv2);
         }
       } else if (use) {
 #pragma unroll 2
         for (int k = 0; k < Mp; k += 4) {
-          const double av0 = a0[k], av1 = a0[8 * pitch + k];
+          const double av0 = a0[k];
           const double bv0 = b0[k], bv1 = b0[8 * pitch + k], bv2 = b0[16 * pitch + k];
           if (use & 1u) dmma884(acc[0][0][0], acc[0][0][1], av0, bv0);
           if (use & 2u) dmma884(acc[0][1][0], acc[0][1][1], av0, bv1);
           if (use & 4u) dmma884(acc[0][2][0], acc[0][2][1], av0, bv2);
-          if (use & 8u) dmma884(acc[1][0][0], acc[1][0][1], av1, bv0);
-          if (use & 16u) dmma884(acc[1][1][0], acc[1][1][1], av1, bv1);
-          if (use & 32u) dmma884(acc[1][2][0], acc[1][2][1], av1, bv2);
         }
       }
       // scatter the (centre, interval) pairs that exist into Pbuf
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
+      for (int mt = 0; mt < 1; ++mt) {
         if (!r_ok[mt]) continue;
         const int16_t* gi = gidx + r_al[mt] * P2_UCAP + ch * P2_CB;
         double* pb = p.Pbuf + r_base[mt] * 24 + r_a[mt] * 6;
@@ -1567,7 +1558,7 @@ void Engine::tab_bwd_range(int, int64_t i0, int64_t i1, cudaStream_t st) {
   case F:                                                                                                     \
     DPB_CUDA(cudaFuncSetAttribute(k_tab_bwd_P2<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
                                   static_cast<int>(bytes)));                                                  \
-    k_tab_bwd_P2<F><<<std::max(1, std::min(nblk, sms)), 256, bytes, st>>>(p, dTw, fbl, fbl + nblk_all);   \
+    k_tab_bwd_P2<F><<<std::max(1, std::min(nblk, sms)), P2_THREADS, bytes, st>>>(p, dTw, fbl, fbl + nblk_all);   \
     break;
       DPB_P2(1) DPB_P2(2) DPB_P2(3) DPB_P2(4)
 #undef DPB_P2
