@@ -589,6 +589,7 @@ __global__ void __launch_bounds__(256, 2) k_tab_dT(TabParams p, double* __restri
     const int slot = p.slot_of[i];
     const double* dDrow = p.dD + static_cast<size_t>(slot < 0 ? 0 : slot) * p.K0p;
     const bool fon = f0 < p.M && slot >= 0;
+    const bool vec = ((p.M | p.K0p) & 1) == 0; // 16-byte aligned dD pairs
     for (int q0 = 0; q0 < p.mlt; q0 += 4) {
       double part[16];
 #pragma unroll
@@ -598,8 +599,23 @@ __global__ void __launch_bounds__(256, 2) k_tab_dT(TabParams p, double* __restri
         const int qq = q0 + ql;
         if (qq < p.mlt) {
           double dq[F];
+          if constexpr (F % 2 == 0) {
+            if (vec) {
 #pragma unroll
-          for (int q = 0; q < F; ++q) dq[q] = fon ? dDrow[qq * p.M + f0 + q] : 0.0;
+              for (int q = 0; q < F; q += 2) {
+                const double2 v = fon ? *reinterpret_cast<const double2*>(dDrow + qq * p.M + f0 + q)
+                                      : make_double2(0.0, 0.0);
+                dq[q] = v.x;
+                dq[q + 1] = v.y;
+              }
+            } else {
+#pragma unroll
+              for (int q = 0; q < F; ++q) dq[q] = fon ? dDrow[qq * p.M + f0 + q] : 0.0;
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < F; ++q) dq[q] = fon ? dDrow[qq * p.M + f0 + q] : 0.0;
+          }
 #pragma unroll
           for (int a = 0; a < 4; ++a) {
             const double ta = ts[a * p.Mp + qq];
