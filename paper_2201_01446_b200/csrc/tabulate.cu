@@ -973,19 +973,17 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_tab_bwd_P2(TabParams p, const
   }
 }
 
-// ---------------------------------------------------------------- k_tab_fwd_T2 (CTA, FP64 tensor pipe)
-// The forward contraction T[(i,a)][p] = sum_groups sum_m W[i][g][a][m] C[bin(g)][m][p] of 32
-// consecutive centres at once (the mirror of k_tab_bwd_P2): the union of their intervals is staged
-// once in shared memory (cp.async, double-buffered, 4 intervals per stage) together with the
-// matching slice of the moments written by k_tab_fwd<WM>, and contracted on DMMA.8x8x4 with
-// rows = (centre, a), k = (interval, m), columns = features. Each interval occupies 8 k-rows
-// (6 coefficients + 2 zero rows), so a centre's sum runs over its own intervals in ascending order
-// whatever the other centres of the block touch (absent intervals add exact zeros, and m-tiles with
-// neither centre in an interval skip it): T is bitwise independent of the block composition and
-// hence of the chunking. The per-warp kernel streamed 6 KB of coefficients per (centre, interval)
-// through L1; here each staged interval serves all 32 centres. T goes out coalesced and
-// D = T<^T T (contract.hpp:9-17) is formed from the staged T. Blocks whose union exceeds T2_UCAP
-// intervals (fine tables) contract per warp from the same moments.
+// ---------------------------------------------------------------- k_tab_fwd_T2 (CTA, staged union)
+// The forward contraction T[i][a][p] = sum_groups sum_m W[i][g][a][m] C[bin(g)][m][p] of 32
+// consecutive centres per CTA: the union of their intervals is staged once in shared memory
+// (cp.async, double-buffered, 4 intervals per stage, 8 rows each) together with the matching
+// slice of the moments written by k_tab_fwd<WM>; each warp then contracts its two centres from
+// shared memory with lanes owning features. The per-warp k_tab_fwd streams 6 KB of coefficients
+// per (centre, interval) from L2 (the hot table does not fit the L1 left beside its shared
+// memory); here each staged interval serves all 32 centres. Per accumulator the FMA chain is the
+// per-warp kernel's (intervals ascending, m ascending), so T and D are bitwise identical to it.
+// (A first version contracted on DMMA with rows = (centre, a), k = (interval, m): slower, see
+// DESIGN.md §9.) Blocks whose union exceeds T2_UCAP intervals contract per warp from the moments.
 constexpr int T2_NA = 32, T2_CB = 4, T2_UCAP = 128, T2_UW = T2_UCAP / 32, T2_BMW = 256, T2_AP = 36;
 constexpr int T2_THREADS = 512; // 16 warps, one m-tile (2 centres x 4 rows) each
 
@@ -1192,9 +1190,18 @@ __global__ void __launch_bounds__(T2_THREADS, 1) k_tab_fwd_T2(TabParams p) {
       }
       tc::cp_commit();
     };
-    double acc[NT][2];
+    // per-warp contraction of its two centres from the staged slice, lanes own features
+    // f0 .. f0 + F - 1: for each of the centre's intervals (ascending), for m, for a,
+    // T[a][f] += W[a][m] C[m][f] -- per accumulator the same FMA chain as k_tab_fwd, so T and D
+    // are bitwise those of the per-warp kernel
+    const int f0 = F * lane;
+    double tacc[2][4][F];
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int q = 0; q < F; ++q) tacc[c][a][q] = 0.0;
     if (nch > 0) stage(0, 0);
     for (int ch = 0; ch < nch; ++ch) {
       if (ch + 1 < nch) {
@@ -1204,70 +1211,97 @@ __global__ void __launch_bounds__(T2_THREADS, 1) k_tab_fwd_T2(TabParams p) {
         tc::cp_wait<0>();
       }
       __syncthreads();
-      const double* cs = Cs + (ch & 1) * CR * pitch + tig * pitch + gid;
-      const double* as = As + (ch & 1) * 4 * T2_NA * T2_AP + (warp * 8 + gid) * T2_AP + tig;
-      const unsigned nm = (mtmask[warp * T2_UW + ((ch * T2_CB) >> 5)] >> ((ch * T2_CB) & 31)) & 15u;
+      const double* cs = Cs + (ch & 1) * CR * pitch + f0;
+      const double* as = As + (ch & 1) * 4 * T2_NA * T2_AP;
+      const bool ok0 = warp * 2 < na && wb_s[warp * 2] >= 0;
+      const bool ok1 = warp * 2 + 1 < na && wb_s[warp * 2 + 1] >= 0;
+      const int16_t* g0 = gidx + (warp * 2) * T2_UCAP + ch * T2_CB;
+      const double* w0 = as + (warp * 2) * 4 * T2_AP;
+      const double* w1 = w0 + 4 * T2_AP;
+      for (int ul = 0; ul < T2_CB && ch * T2_CB + ul < U; ++ul) {
+        // both centres of the warp share the staged coefficient rows of an interval they both have
+        const bool h0 = ok0 && g0[ul] >= 0, h1 = ok1 && g0[T2_UCAP + ul] >= 0;
+        if (!(h0 || h1)) continue;
+        const double* cr = cs + ul * 8 * pitch;
+        const double* wr0 = w0 + ul * 8;
+        const double* wr1 = w1 + ul * 8;
 #pragma unroll
-      for (int ul = 0; ul < T2_CB; ++ul) {
-        if (!((nm >> ul) & 1u)) continue;
+        for (int m = 0; m < 6; ++m) {
+          double cm[F];
+          if constexpr (F % 2 == 0) {
 #pragma unroll
-        for (int ks = 0; ks < 2; ++ks) {
-          const int k0 = ul * 8 + ks * 4;
-          const double av = as[k0];
-          const double* bp = cs + k0 * pitch;
+            for (int q = 0; q < F; q += 2) {
+              const double2 v = *reinterpret_cast<const double2*>(cr + m * pitch + q);
+              cm[q] = v.x;
+              cm[q + 1] = v.y;
+            }
+          } else {
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) dmma884(acc[nt][0], acc[nt][1], av, bp[nt * 8]);
-        }
-      }
-      __syncthreads();
-    }
-    // T out straight from the accumulators: row (centre 2w + gid / 4, a = gid % 4)
-    const int al_me = warp * 2 + (gid >> 2);
-    if (al_me < na) {
-      double* Tr = p.T + (static_cast<size_t>(i0) * 4 + warp * 8 + gid) * Mp + 2 * tig;
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) *reinterpret_cast<double2*>(Tr + nt * 8) = make_double2(acc[nt][0], acc[nt][1]);
-    }
-    // D = T<^T T per centre (contract.hpp:9-17) on DMMA with k = a: the operand fragments
-    // B[a = tig][p = 8 nt + gid] = T[a][p] (and A[q][a] = B of tile q / 8) are shuffled out of the
-    // accumulators of the thread holding row (c, a) = 4 c + tig, columns 8 nt + 2 (gid / 2) + {0, 1}
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const int al = warp * 2 + c;
-      if (al >= na) break;
-      const int slot = p.slot_of[i0 + al];
-      if (slot < 0) continue;
-      const int src = (4 * c + tig) * 4 + (gid >> 1);
-      const bool odd = gid & 1;
-      double* Drow = p.D + static_cast<size_t>(slot) * p.K0p;
-      for (int qt = 0; qt * 8 < p.mlt; ++qt) {
-        double aq = 0.0;
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-          if (nt == qt) {
-            const double v0 = __shfl_sync(0xffffffffu, acc[nt][0], src);
-            const double v1 = __shfl_sync(0xffffffffu, acc[nt][1], src);
-            aq = odd ? v1 : v0;
+            for (int q = 0; q < F; ++q) cm[q] = cr[m * pitch + q];
           }
-        const int q = qt * 8 + gid;
+          if (h0) {
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          const double v0 = __shfl_sync(0xffffffffu, acc[nt][0], src);
-          const double v1 = __shfl_sync(0xffffffffu, acc[nt][1], src);
-          double d0 = 0.0, d1 = 0.0;
-          dmma884(d0, d1, aq, odd ? v1 : v0);
-          const int pc = nt * 8 + 2 * tig;
-          if (q < p.mlt) {
-            double* dst = Drow + q * p.M + pc;
-            if (pc + 1 < p.M && (p.M & 1) == 0) {
-              *reinterpret_cast<double2*>(dst) = make_double2(d0, d1);
-            } else {
-              if (pc < p.M) dst[0] = d0;
-              if (pc + 1 < p.M) dst[1] = d1;
+            for (int a = 0; a < 4; ++a) {
+              const double wa = wr0[a * T2_AP + m];
+#pragma unroll
+              for (int q = 0; q < F; ++q) tacc[0][a][q] += wa * cm[q];
+            }
+          }
+          if (h1) {
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+              const double wa = wr1[a * T2_AP + m];
+#pragma unroll
+              for (int q = 0; q < F; ++q) tacc[1][a][q] += wa * cm[q];
             }
           }
         }
       }
+      __syncthreads();
+    }
+    // T out, D = T<^T T (contract.hpp:9-17) as in k_tab_fwd (T of the centre staged per warp)
+    double* ts = Cs + warp * 4 * Mp;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int al = warp * 2 + c;
+      if (al >= na) break;
+      const int i = i0 + al;
+      double* Ti = p.T + static_cast<size_t>(i) * 4 * Mp;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int q = 0; q < F; ++q) {
+          Ti[a * Mp + f0 + q] = tacc[c][a][q];
+          ts[a * Mp + f0 + q] = tacc[c][a][q];
+        }
+      __syncwarp();
+      const int slot = p.slot_of[i];
+      if (slot >= 0 && f0 < p.M) {
+        double* Drow = p.D + static_cast<size_t>(slot) * p.K0p;
+        for (int qq = 0; qq < p.mlt; ++qq) {
+          const double t0 = ts[qq], t1 = ts[Mp + qq], t2 = ts[2 * Mp + qq], t3 = ts[3 * Mp + qq];
+          double dv[F];
+#pragma unroll
+          for (int q = 0; q < F; ++q) {
+            double v = t0 * tacc[c][0][q];
+            v += t1 * tacc[c][1][q];
+            v += t2 * tacc[c][2][q];
+            v += t3 * tacc[c][3][q];
+            dv[q] = v;
+          }
+          double* dst = Drow + qq * p.M + f0;
+          if constexpr (F % 2 == 0) {
+            if ((p.M & 1) == 0) {
+#pragma unroll
+              for (int q = 0; q < F; q += 2) *reinterpret_cast<double2*>(dst + q) = make_double2(dv[q], dv[q + 1]);
+              continue;
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < F; ++q) dst[q] = dv[q];
+        }
+      }
+      __syncwarp();
     }
     __syncthreads();
   }
@@ -1413,9 +1447,9 @@ void Engine::ensure_tab32() {
   tab32_ver = tab_ver;
 }
 
-// Opt-in (DPB_T2=1): measured at C2 the moments kernel + k_tab_fwd_T2 take 0.49 ms per 16k-centre
-// chunk against 0.46 ms for the per-warp k_tab_fwd with warm L2, and the 152 KB CTAs co-reside
-// worse with the other stream's GEMMs (5.23 vs 5.13 ms/step); DESIGN.md §9.
+// Opt-in (DPB_T2=1), results bitwise equal to the default path: measured at C2 the moments kernel
+// + k_tab_fwd_T2 take 0.19 + 0.40 ms per 16k-centre chunk against 0.42 ms for the per-warp
+// k_tab_fwd (step 5.33 vs 5.01 ms); DESIGN.md §9.
 bool Engine::t2_ok() const {
   static const bool on = std::getenv("DPB_T2") != nullptr && std::getenv("DPB_T2")[0] == '1';
   return on && precision == 0 && Mp <= 128;

@@ -1,8 +1,8 @@
-"""Opt-in forward contraction on the FP64 tensor pipe (DPB_T2=1: k_tab_fwd<WM> moments +
+"""Forward contraction from a staged 32-centre interval union (DPB_T2=1: k_tab_fwd<WM> moments +
 k_tab_fwd_T2, tabulate.cu). Run in a subprocess because the switch is read once per process.
-Checks: within 1e-10 of the oracle, counters equal, and bitwise independent of
-the chunking, including chunk sizes that shift the 32-centre block boundaries (each interval
-takes 8 k-rows, so a centre's sum never depends on the other centres of its block)."""
+Checks: bitwise equal to the per-warp k_tab_fwd path (same FMA chain per accumulator), within
+1e-10 of the oracle, counters equal, and bitwise independent of the chunking,
+including chunk sizes that shift the 32-centre block boundaries."""
 import json
 import os
 import subprocess
@@ -52,6 +52,11 @@ def test_t2_forward_parity_and_chunk_bitwise():
     m = dp.gen_model("copper-like", 7)
     t = dp.build_tables(m, 0.01)
     c = dp.gen_config("copper-like", 8, 8, 8, 0.1, 11)
+    ref = dp.DeepPot(m, t).compute(c)  # this process: the per-warp forward kernel
+    assert base["e"] == ref.energy
+    assert np.array_equal(np.array(base["f"]), ref.forces)
+    assert np.array_equal(np.array(base["v"]), ref.virial)
+    assert np.array_equal(np.array(base["ae"]), ref.per_atom_energy)
     ro, co = O.or_compute(c, m, t)
     assert abs(base["e"] - ro.energy) <= 1e-10 * abs(ro.energy)
     assert O.normwise(np.array(base["f"]), ro.forces) <= 1e-10
