@@ -1330,7 +1330,15 @@ __global__ void __launch_bounds__(256) k_tab_bwd_g(TabParams p) {
     ge[0] = ge[1] = ge[2] = 0.0;
     return;
   }
-  const double* P = p.Pbuf + gi * 24;
+  // the group's 24 projections as 12 16-byte loads (a Pbuf row is 192 B, 16-byte aligned)
+  const double2* P2 = reinterpret_cast<const double2*>(p.Pbuf + gi * 24);
+  double P[24];
+#pragma unroll
+  for (int q = 0; q < 12; ++q) {
+    const double2 v = __ldg(P2 + q);
+    P[2 * q] = v.x;
+    P[2 * q + 1] = v.y;
+  }
   const double R[4] = {ev.s, ev.s * ev.u[0], ev.s * ev.u[1], ev.s * ev.u[2]};
   const double uu = ev.s - node_x(p.x0, p.h, th);
   double drow[4], dsum = 0.0;
