@@ -56,6 +56,17 @@ __device__ __forceinline__ float tf32_rna(float x) {
   return __uint_as_float(r);
 }
 
+// L2 prefetch of [ptr, ptr + bytes) by the bulk-copy engine: one instruction, no destination
+// registers. The range is widened to 16-byte boundaries (the bulk-prefetch granularity); every
+// DevBuf carries at least 64 elements of slack past its end, and allocations are 256-B aligned.
+__device__ __forceinline__ void l2_prefetch(const void* ptr, size_t bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(ptr) & ~uintptr_t(15);
+  const uintptr_t e = (reinterpret_cast<uintptr_t>(ptr) + bytes + 15) & ~uintptr_t(15);
+  if (e > a)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a), "r"(static_cast<uint32_t>(e - a))
+                 : "memory");
+}
+
 __device__ __forceinline__ double node_x(double x0, double h, int th) {
   return __dadd_rn(x0, __dmul_rn(static_cast<double>(th), h));
 }
