@@ -383,4 +383,40 @@ int ref_read_model(const char* path, const dp_preset* s, double* blob, uint64_t*
   });
 }
 
+// bench.py --impl reference / cpu_baseline: the reference's MD-step cost on its OWN inputs, built
+// entirely by its public API (gen_model model_io.hpp:40, build_tables table.hpp:42, gen_config
+// model_io.hpp:45, build_neighbor_list neighbor.hpp:31) -- nothing of the product involved.
+// Per step: one compute_energy_forces_virial_tabulated (fused.hpp:70-73) with n_workers threads on
+// the list built once at r_c + skin (cell path). list_s = that build, eval_s[k] = step k's
+// evaluation (wall clock). Runs `warmup` untimed evaluations, then up to max_steps timed ones,
+// stopping early once budget_s seconds of timed work are done (at least min_steps).
+int ref_bench_steps(const char* preset, int nx, int ny, int nz, double jitter, uint64_t cfg_seed,
+                    uint64_t model_seed, double h, double skin, int n_workers, int warmup,
+                    int max_steps, int min_steps, double budget_s, int64_t* n_atoms, double* list_s,
+                    double* eval_s, int* n_done, double* energy) {
+  return guarded([&] {
+    const Preset& p = get_preset(preset);
+    auto m = gen_model(p, model_seed);
+    auto tabs = build_tables(m, h);
+    auto cfg = gen_config(p, nx, ny, nz, jitter, cfg_seed);
+    *n_atoms = cfg.n_atoms;
+    auto t0 = std::chrono::steady_clock::now();
+    auto list = build_neighbor_list(cfg, m.r_cut + skin);
+    *list_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    EvalResult r;
+    for (int k = 0; k < warmup; ++k) r = compute_energy_forces_virial_tabulated(cfg, m, tabs, list, n_workers);
+    double total = 0.0;
+    int done = 0;
+    while (done < max_steps && (done < min_steps || total < budget_s)) {
+      auto a = std::chrono::steady_clock::now();
+      r = compute_energy_forces_virial_tabulated(cfg, m, tabs, list, n_workers);
+      eval_s[done] = std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count();
+      total += eval_s[done++];
+    }
+    *n_done = done;
+    *energy = r.energy;
+  });
+}
+
 } // extern "C"
+

@@ -286,3 +286,11 @@ def ref_read_model(path: str, model_like: dp.DPModel):
     _chk(L.ref_read_model(path.encode(), C.byref(model_like.shape._c()), _dp(blob), C.byref(seed)), L,
          "ref_last_error")
     return blob, seed.value
+
+
+def ref_init_velocities(cfg: dp.AtomicConfig, model: dp.DPModel, t_init: float, seed: int) -> np.ndarray:
+    """init_velocities (md.cpp:14-55) of the unmodified reference."""
+    v = np.empty((cfg.n_atoms, 3))
+    _chk(ref().ref_init_velocities(C.byref(model.shape._c()), cfg.n_atoms, _dp(cfg.pos), _ip(cfg.type),
+                                   _dp(cfg.h), t_init, seed, _dp(v)), ref(), "ref_last_error")
+    return v
