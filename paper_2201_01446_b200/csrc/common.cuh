@@ -17,6 +17,15 @@
 
 namespace dpb {
 
+// Dynamic shared memory above 48 KB needs a per-function, per-device opt-in. Handles on several
+// devices may live in one process (one per host thread), so the opt-in is recorded per
+// (function, device, size) under a lock instead of a process-wide static flag.
+void smem_optin_raw(const void* fn, size_t bytes);
+template <class K>
+inline void smem_optin(K* kern, size_t bytes) {
+  smem_optin_raw(reinterpret_cast<const void*>(kern), bytes);
+}
+
 // Error codes raised by kernels into Workspace::err (first writer wins).
 enum DevErr : int {
   DEV_OK = 0,

@@ -798,6 +798,10 @@ void dist_rebuild(Engine& E) {
                  std::chrono::duration<double, std::milli>(t2 - t1).count());
 }
 
+void dist_agree_err(Engine& E) {
+  DPB_NCCL(ncclAllReduce(E.err.p, E.err.p, 1, ncclInt32, ncclMax, E.dist->comm, E.stream));
+}
+
 void dist_md_end(Engine& E, double* gpos, double* gvel) {
   Dist& D = *E.dist;
   gather_global(E);

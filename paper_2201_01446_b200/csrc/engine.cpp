@@ -3,10 +3,25 @@
 //   compute_energy_forces_virial_tabulated   fused.cpp:245-288
 //   run_md / rebuild / evaluate              md.cpp:70-134, 151-231
 #include <cstring>
+#include <mutex>
+#include <set>
+#include <tuple>
 
 #include "engine.hpp"
 
 namespace dpb {
+
+void smem_optin_raw(const void* fn, size_t bytes) {
+  if (bytes <= 48 * 1024) return;
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, size_t>> done;
+  int dev = 0;
+  DPB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({fn, dev, bytes})) return;
+  DPB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+  done.insert({fn, dev, bytes});
+}
 
 std::string& global_error() {
   static thread_local std::string e;
@@ -233,6 +248,10 @@ void Engine::destroy() {
     }
   gtot.release();
   scan_tmp2.release();
+  if (h_gtotal) {
+    cudaFreeHost(h_gtotal);
+    h_gtotal = nullptr;
+  }
 }
 
 void Engine::set_config(int64_t nn, const double* pos, const int32_t* ty, const double* box,
@@ -592,6 +611,9 @@ void Engine::phase_collect(double* ms, uint64_t* counts) {
 }
 
 void Engine::check_err() {
+  // decomposed runs: every rank raises the same error together (a rank that threw alone would
+  // leave its peers blocked in the next collective)
+  if (dist) dist_agree_err(*this);
   int code = 0;
   DPB_CUDA(cudaMemcpyAsync(&code, err.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
   DPB_CUDA(cudaStreamSynchronize(stream));
@@ -695,6 +717,8 @@ void Engine::md_begin(const double* pos, const double* vel, const dp_md_config* 
 
 void Engine::md_steps(int64_t k) {
   if (!md_active) throw InputErr("no MD run in progress");
+  if (k < 0 || md_step + k > md.n_steps)
+    throw InputErr("MD step count exceeds the configured n_steps of this run");
   MdScratch& S = scratch;
   const double half = 0.5 * md.dt;
   for (int64_t it = 0; it < k; ++it) {
@@ -706,7 +730,9 @@ void Engine::md_steps(int64_t k) {
       if (dist)
         dist_rebuild(*this);
       else
-        build_list(r_cut + md.buffer, true); // no host sync: capacities are checked on the device
+        // synchronous sizing (one read-back every rebuild_every steps): the list capacity always
+        // fits the new list, so no kernel ever indexes past it
+        build_list(r_cut + md.buffer);
     } else if (dist) {
       phase_begin(6);
       dist_halo_forward(*this);

@@ -354,6 +354,7 @@ void dist_halo_reverse(Engine& E);
 void dist_reverse_send(Engine& E);
 bool dist_ghost_list(Engine& E, const int32_t** list, int64_t* n, double** send);
 void dist_allreduce_sum(Engine& E, double* dev, int count);
+void dist_agree_err(Engine& E); // err := max over ranks
 int64_t dist_n_total(const Engine& E);
 void dist_md_end(Engine& E, double* gpos, double* gvel);
 

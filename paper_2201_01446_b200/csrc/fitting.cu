@@ -217,11 +217,7 @@ void launch_gemm(const GemmArgs& a, int rows, int N, cudaStream_t st) {
   const size_t bytes = static_cast<size_t>(STAGES) * (BM + BN) * PITCH * sizeof(double);
   static const bool four = BN == 80 && STAGES == 2 && std::getenv("DPB_GEMM_NO4") == nullptr;
   auto kern = four ? k_gemm4<EPI, BN, STAGES> : k_gemm<EPI, BN, STAGES>;
-  static bool init = false;
-  if (!init) {
-    DPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
-    init = true;
-  }
+  smem_optin(kern, bytes);
   GemmArgs g = a;
   g.ntn = N / BN;
   g.ntm = rows / BM;

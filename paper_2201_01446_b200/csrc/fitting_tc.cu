@@ -332,12 +332,7 @@ template <int EPI, int BN>
 void launch_tc(const float* A2, const float* B2, int rows, int N, TArgs g, cudaStream_t st) {
   constexpr int PIPE = TST * (TBM + BN) * TBKB;
   const size_t smem = static_cast<size_t>(PIPE > STAGE_BYTES ? PIPE : STAGE_BYTES) + 8 * (2 * TST + 1) + 16 + 1024;
-  static bool init = false;
-  if (!init) {
-    DPB_CUDA(cudaFuncSetAttribute(k_tc_gemm<EPI, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-    init = true;
-  }
+  smem_optin(k_tc_gemm<EPI, BN>, smem);
   const uint64_t row_bytes = static_cast<uint64_t>(2) * g.kseg * 4;
   const CUtensorMap ta = byte_map(A2, rows, row_bytes, TBM);
   const CUtensorMap tb = byte_map(B2, N, row_bytes, BN);

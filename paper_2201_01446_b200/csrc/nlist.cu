@@ -357,6 +357,7 @@ void Engine::launch_nlist(double cutoff, bool async) {
   ++launches;
   const int cap = row_cap;
   if (cap > 8192) throw NumErr("neighbour row longer than 8192 entries");
+  smem_optin(k_sort_rows, cap * sizeof(uint64_t));
   k_sort_rows<<<N, 256, cap * sizeof(uint64_t), stream>>>(N, row_off.p, keys.p, cap, err.p);
   ++launches;
   k_reverse_e<<<ceil_div(e_cap, 256), 256, 0, stream>>>(row_off.p, N, keys.p, eown.p, types.p, rev.p, err.p, e_cap);

@@ -102,3 +102,19 @@ def test_nve_energy_conservation_fine_table():
     mean_ke = np.mean([r.ke for r in res.thermo])
     assert drift <= 1e-4 * mean_ke
     assert res.staleness_checks == 200 and res.max_drift_seen <= 1.0
+
+
+def test_md_step_past_configured_count_is_input_error():
+    """dp_md_step beyond MDConfig.n_steps must not run past the thermo buffer."""
+    m = dp.make_test_model(1, 4, 6, 12, 2, [16], 5.0, 4.0, 947)
+    t = dp.build_tables(m, 0.01)
+    c = dp.make_random_config(8, 1, 9.0, 2.2, 97)
+    v = dp.init_velocities(c, m, 50.0, 7)
+    pot = dp.DeepPot(m, t)
+    pot.md_begin(c, v, dp.MDConfig(n_steps=5, thermo_every=1))
+    pot.md_step(3)
+    with pytest.raises(dp.InputError):
+        pot.md_step(3)
+    pot.md_step(2)
+    res = pot.md_end()
+    assert res.force_evals == 6 and [r.step for r in res.thermo] == list(range(6))
