@@ -160,6 +160,17 @@ int dp_compute(dp_handle* h, int64_t n, const double* pos, const int32_t* types,
                double* virial, double* atom_energy);
 int dp_counters_get(const dp_handle* h, dp_counters* out);
 
+/* The same operator on the CALLER's neighbour list, exactly the reference signature
+ * compute_energy_forces_virial_tabulated(cfg, model, tables, list) (fused.hpp:70-73): list =
+ * NeighborList (neighbor.hpp:14-23) flattened to offsets[n+1], j[offsets[n]], shift[3*offsets[n]].
+ * The list must be full and symmetric (every (i -> j, s) has its (j -> i, -s), as
+ * build_neighbor_list returns it) at any cutoff >= r_cut; entries beyond r_cut are filtered
+ * exactly as env_mat.cpp:32 does. Returns 2 (InputError) for an asymmetric or malformed list. */
+int dp_compute_list(dp_handle* h, int64_t n, const double* pos, const int32_t* types,
+                    const double box[9], const uint8_t pbc[3], const int64_t* offsets,
+                    const int32_t* j, const int32_t* shift, double* energy, double* forces,
+                    double* virial, double* atom_energy);
+
 /* build_neighbor_list (neighbor.cpp:162-179) on the GPU, canonical order (ascending j, then
  * shift lexicographic). Two calls: dp_neighbor_list_build returns the total entry count, then
  * dp_neighbor_list_get copies offsets[n+1], j[total] and shift[3*total] to host. */

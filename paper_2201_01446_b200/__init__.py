@@ -130,6 +130,7 @@ def _lib():
         "dp_last_error": ([P], C.c_char_p),
         "dp_set_skin": ([P, C.c_double], I),
         "dp_compute": ([P, I64, D, I32P, D, U8P, D, D, D, D], I),
+        "dp_compute_list": ([P, I64, D, I32P, D, U8P, C.POINTER(C.c_int64), I32P, I32P, D, D, D, D], I),
         "dp_counters_get": ([P, C.POINTER(_Counters)], I),
         "dp_neighbor_list_build": ([P, I64, D, I32P, D, U8P, C.c_double, C.POINTER(I64)], I),
         "dp_neighbor_list_get": ([P, C.POINTER(I64), I32P, I32P], I),
@@ -670,6 +671,26 @@ class DeepPot:
         ae = np.empty(n, dtype=np.float64)
         rc = _lib().dp_compute(self._h, n, _dp(cfg.pos), _ip(cfg.type), _dp(cfg.h),
                                _u8(cfg.periodic), C.byref(e), _dp(f), _dp(v), _dp(ae))
+        _check(rc, self._h)
+        c = _Counters()
+        _lib().dp_counters_get(self._h, C.byref(c))
+        self.counters = FusedCounters(c.rows_forward, c.rows_backward, c.extrapolations)
+        return EvalResult(e.value, ae, f, v)
+
+    def compute_with_list(self, cfg: AtomicConfig, nlist: "NeighborList") -> EvalResult:
+        """compute_energy_forces_virial_tabulated(cfg, model, tables, list) (fused.hpp:70-73) on
+        the caller's full, symmetric neighbour list (any cutoff >= r_cut)."""
+        n = cfg.n_atoms
+        e = C.c_double()
+        f = np.empty((n, 3), dtype=np.float64)
+        v = np.empty(9, dtype=np.float64)
+        ae = np.empty(n, dtype=np.float64)
+        off = np.ascontiguousarray(nlist.offsets, dtype=np.int64)
+        j = np.ascontiguousarray(nlist.j, dtype=np.int32)
+        sh = np.ascontiguousarray(nlist.shift, dtype=np.int32).reshape(-1)
+        rc = _lib().dp_compute_list(self._h, n, _dp(cfg.pos), _ip(cfg.type), _dp(cfg.h), _u8(cfg.periodic),
+                                    off.ctypes.data_as(C.POINTER(C.c_int64)), _ip(j), _ip(sh), C.byref(e),
+                                    _dp(f), _dp(v), _dp(ae))
         _check(rc, self._h)
         c = _Counters()
         _lib().dp_counters_get(self._h, C.byref(c))

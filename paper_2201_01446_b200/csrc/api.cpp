@@ -73,6 +73,23 @@ int dp_compute(dp_handle* h, int64_t n, const double* pos, const int32_t* types,
   });
 }
 
+int dp_compute_list(dp_handle* h, int64_t n, const double* pos, const int32_t* types, const double box[9],
+                    const uint8_t pbc[3], const int64_t* offsets, const int32_t* j, const int32_t* shift,
+                    double* energy, double* forces, double* virial, double* atom_energy) {
+  if (!h) return DP_INPUT_ERROR;
+  return guard_call(&h->eng.last_error, [&] {
+    dpb::Engine& E = h->eng;
+    if (!energy || !forces || !virial) throw InputErr("null output array");
+    E.set_config(n, pos, types, box, pbc);
+    E.import_list(offsets, j, shift);
+    E.reset_counters();
+    E.evaluate_retry();
+    E.list_valid = false; // the caller's list serves this call only
+    E.fetch_results(energy, forces, virial, atom_energy);
+    E.read_counters();
+  });
+}
+
 int dp_set_chunk_size(dp_handle* h, int64_t centres) {
   if (!h) return DP_INPUT_ERROR;
   if (centres < 0) return DP_INPUT_ERROR;

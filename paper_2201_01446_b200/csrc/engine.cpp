@@ -51,6 +51,7 @@ void raise_device_error(int code) {
     case DEV_PBUF: throw NumErr("tabulate group buffer overflow (retry: it grows at the next rebuild)");
     case DEV_TABLE_VERIFY: throw NumErr("table verification failed at a node");
     case DEV_LIST_CAP: throw NumErr("neighbour list grew past its capacity (+25 %) between MD rebuilds");
+    case DEV_ASYMMETRIC: throw InputErr("neighbour list is not symmetric: an entry (i -> j, s) has no (j -> i, -s)");
     case DEV_STALE: throw NumErr("neighbor list stale: an atom moved more than half the buffer since the last rebuild");
     default: throw CudaErr("unknown device error " + std::to_string(code));
   }
@@ -120,40 +121,53 @@ void Engine::create(const dp_model_desc* md, const dp_table_desc* td, int dev, i
     if (max_nbr[t] <= 0) throw InputErr("model max_nbr entries must be positive");
     if (!(masses[t] > 0.0)) throw InputErr("model masses must be positive");
   }
-  // fitting structure (identical across centre types)
-  const dp_fitting_desc& f0 = md->fitting[0];
-  if (f0.n_layers < 1) throw InputErr("fitting net needs at least one hidden layer");
-  if (f0.widths[0] != K0) throw InputErr("fitting input width does not match descriptor");
-  for (int t = 1; t < n_types; ++t) {
-    const dp_fitting_desc& f = md->fitting[t];
-    if (f.n_layers != f0.n_layers) throw InputErr("fitting nets of all types must share a shape");
-    for (int k = 0; k <= f.n_layers; ++k)
-      if (f.widths[k] != f0.widths[k]) throw InputErr("fitting nets of all types must share a shape");
-  }
-  const int L = f0.n_layers;
-  layers.resize(L);
+  // fitting structure, per centre type
+  tlayers.assign(n_types, {});
+  fit_off.assign(n_types + 1, 0);
   widthp_max = 16;
-  for (int k = 0; k < L; ++k) {
-    FitLayer& fl = layers[k];
-    fl.in = f0.widths[k];
-    fl.out = f0.widths[k + 1];
-    if (fl.out <= 0) throw InputErr("fitting layer widths are inconsistent");
-    fl.inp = k == 0 ? K0p : pad_width(fl.in);
-    fl.outp = pad_width(fl.out);
-    fl.shortcut = fl.in == fl.out;
-    widthp_max = std::max(widthp_max, fl.outp);
+  max_layers = 0;
+  for (int t = 0; t < n_types; ++t) {
+    const dp_fitting_desc& f = md->fitting[t];
+    if (f.n_layers < 1) throw InputErr("fitting net needs at least one hidden layer");
+    if (!f.widths || !f.w || !f.b || !f.w_out) throw InputErr("null fitting net array");
+    if (f.widths[0] != K0) throw InputErr("fitting input width does not match descriptor");
+    std::vector<FitLayer>& ls = tlayers[t];
+    ls.resize(f.n_layers);
+    for (int k = 0; k < f.n_layers; ++k) {
+      FitLayer& fl = ls[k];
+      fl.in = f.widths[k];
+      fl.out = f.widths[k + 1];
+      if (fl.out <= 0) throw InputErr("fitting layer widths are inconsistent");
+      fl.inp = k == 0 ? K0p : pad_width(fl.in);
+      fl.outp = pad_width(fl.out);
+      fl.shortcut = fl.in == fl.out;
+      widthp_max = std::max(widthp_max, fl.outp);
+    }
+    fit_off[t + 1] = fit_off[t] + f.n_layers;
+    max_layers = std::max(max_layers, f.n_layers);
+  }
+  layers = tlayers[0];
+  uniform_fit = true;
+  for (int t = 1; t < n_types; ++t) {
+    if (tlayers[t].size() != layers.size()) uniform_fit = false;
+    else
+      for (size_t k = 0; k < layers.size(); ++k)
+        if (tlayers[t][k].out != layers[k].out) uniform_fit = false;
   }
   if (td) upload_tables(*td);
   // fitting weights, zero padded
-  fit_wt.resize(n_types * L);
-  fit_w.resize(n_types * L);
-  fit_b.resize(n_types * L);
+  const int nfit = fit_off[n_types];
+  fit_wt.resize(nfit);
+  fit_w.resize(nfit);
+  fit_b.resize(nfit);
   fit_wout.resize(n_types);
   b_out.resize(n_types);
   for (int t = 0; t < n_types; ++t) {
     const dp_fitting_desc& f = md->fitting[t];
+    const std::vector<FitLayer>& ls = tlayers[t];
+    const int L = static_cast<int>(ls.size());
     for (int k = 0; k < L; ++k) {
-      const FitLayer& fl = layers[k];
+      const FitLayer& fl = ls[k];
       std::vector<double> w(static_cast<size_t>(fl.inp) * fl.outp, 0.0), wt(w.size(), 0.0),
           b(fl.outp, 0.0);
       for (int u = 0; u < fl.in; ++u)
@@ -163,9 +177,9 @@ void Engine::create(const dp_model_desc* md, const dp_table_desc* td, int dev, i
           wt[static_cast<size_t>(v) * fl.inp + u] = x;
         }
       for (int v = 0; v < fl.out; ++v) b[v] = f.b[k][v];
-      DevBuf<double>& dw = fit_w[t * L + k];
-      DevBuf<double>& dwt = fit_wt[t * L + k];
-      DevBuf<double>& db = fit_b[t * L + k];
+      DevBuf<double>& dw = fit_w[fit_off[t] + k];
+      DevBuf<double>& dwt = fit_wt[fit_off[t] + k];
+      DevBuf<double>& db = fit_b[fit_off[t] + k];
       dw.ensure(w.size());
       dwt.ensure(wt.size());
       db.ensure(b.size());
@@ -173,8 +187,8 @@ void Engine::create(const dp_model_desc* md, const dp_table_desc* td, int dev, i
       DPB_CUDA(cudaMemcpy(dwt.p, wt.data(), wt.size() * 8, cudaMemcpyHostToDevice));
       DPB_CUDA(cudaMemcpy(db.p, b.data(), b.size() * 8, cudaMemcpyHostToDevice));
     }
-    const int last = layers[L - 1].out;
-    std::vector<double> wo(layers[L - 1].outp, 0.0);
+    const int last = ls[L - 1].out;
+    std::vector<double> wo(ls[L - 1].outp, 0.0);
     for (int v = 0; v < last; ++v) wo[v] = f.w_out[v];
     fit_wout[t].ensure(wo.size());
     DPB_CUDA(cudaMemcpy(fit_wout[t].p, wo.data(), wo.size() * 8, cudaMemcpyHostToDevice));
@@ -409,7 +423,7 @@ void Engine::apply_plan() {
 
 void Engine::ensure_step_buffers() {
   if (plan_dirty) plan_chunks();
-  const int L = static_cast<int>(layers.size());
+  const int L = max_layers;
   const size_t sa = static_cast<size_t>(ck_sets) * ck_cap_a, ss = static_cast<size_t>(ck_sets) * ck_cap_s;
   T.ensure(sa * 4 * Mp);
   dTbuf.ensure(sa * 4 * Mp);

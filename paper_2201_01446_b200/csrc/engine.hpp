@@ -98,7 +98,13 @@ struct Engine {
   int d1 = 0, M = 0, Mp = 0, mlt = 0, K0 = 0, K0p = 0;
   std::vector<double> masses;
   std::vector<int> max_nbr;
-  std::vector<FitLayer> layers; // same structure for every centre type
+  // fitting nets per centre type (model.cpp:30-47 validates each net on its own, so depth and
+  // widths may differ between types); fit_*[fit_off[t] + k] hold type t's layer k
+  std::vector<std::vector<FitLayer>> tlayers;
+  std::vector<int> fit_off;
+  int max_layers = 0;
+  bool uniform_fit = true;
+  std::vector<FitLayer> layers; // type 0's layers (= every type's when uniform_fit)
   int widthp_max = 0;
   // tables, device layout [type][interval][6][Mp]
   double tab_x0 = 0, tab_h = 0;
@@ -285,6 +291,8 @@ struct Engine {
   // neighbour list at `cutoff`, device resident
   void build_list(double cutoff, bool async = false);
   void sync_entry_count();
+  void finish_list(double cutoff);
+  void import_list(const int64_t* offsets, const int32_t* j, const int32_t* shift);
   void download_list(int64_t* offsets, int32_t* j, int32_t* shift);
   // one evaluation on the current positions/list; results stay on device
   void evaluate();

@@ -255,7 +255,9 @@ void scatter_energy(Engine& E) {
 }
 
 void Engine::fitting_type_rows(int t, int64_t r0_, int64_t rows_, cudaStream_t st) {
+  const std::vector<FitLayer>& layers = tlayers[t]; // this centre type's net (model.cpp:151-203)
   const int L = static_cast<int>(layers.size());
+  const int fo = fit_off[t];
   const int wpm = widthp_max;
   const int rows = static_cast<int>(rows_);
   const size_t r0 = static_cast<size_t>(r0_);
@@ -267,10 +269,10 @@ void Engine::fitting_type_rows(int t, int64_t r0_, int64_t rows_, cudaStream_t s
     GemmArgs a{};
     a.A = x;
     a.lda = ldx;
-    a.Bt = fit_wt[t * L + k].p;
+    a.Bt = fit_wt[fo + k].p;
     a.ldb = fl.inp;
     a.K = fl.inp;
-    a.bias = fit_b[t * L + k].p;
+    a.bias = fit_b[fo + k].p;
     a.xin = fl.shortcut ? x : nullptr;
     a.ldx = ldx;
     a.tout = ws(act_t[k], wpm) + r0 * wpm;
@@ -297,7 +299,7 @@ void Engine::fitting_type_rows(int t, int64_t r0_, int64_t rows_, cudaStream_t s
     GemmArgs a{};
     a.A = dzc;
     a.lda = wpm;
-    a.Bt = fit_w[t * L + k].p; // W [inp][outp]: K = outp contiguous
+    a.Bt = fit_w[fo + k].p; // W [inp][outp]: K = outp contiguous
     a.ldb = fl.outp;
     a.K = fl.outp;
     a.dyin = fl.shortcut ? dyc : nullptr;

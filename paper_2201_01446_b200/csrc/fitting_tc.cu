@@ -392,6 +392,7 @@ void ensure_zeroed(DevBuf<float>& b, size_t count, cudaStream_t st) {
 } // namespace
 
 void Engine::prepare_mixed() {
+  if (!uniform_fit) throw InputErr("mixed precision needs the same fitting-net shape for every centre type");
   for (size_t k = 1; k < layers.size(); ++k)
     if (layers[k].outp != widthp_max || layers[k].inp != widthp_max)
       throw InputErr("mixed precision needs equal hidden widths");

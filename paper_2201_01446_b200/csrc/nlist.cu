@@ -211,7 +211,7 @@ __global__ void k_reverse_e(const int64_t* __restrict__ row_off, int n, const ui
       hi = mid;
   }
   if (lo >= r1 || keys[lo] != want) {
-    raise_err(err, DEV_ROW_CAP);
+    raise_err(err, DEV_ASYMMETRIC); // the list is not symmetric (a supplied list can be)
     rev[e] = 0;
   } else {
     rev[e] = static_cast<uint32_t>(lo);
@@ -355,6 +355,13 @@ void Engine::launch_nlist(double cutoff, bool async) {
       p, pos4.p, frac.p, types.p, bin_of.p, bin_start.p, bin_atoms.p, nullptr, row_off.p, keys.p, eown.p, err.p,
       e_cap);
   ++launches;
+  finish_list(cutoff);
+}
+
+// Rows are filled (keys, eown, row_off, capacities): sort them into the type-sectored canonical
+// order, index the reverse entries, mark ghost rows, snapshot the positions.
+void Engine::finish_list(double cutoff) {
+  const int N = static_cast<int>(n);
   const int cap = row_cap;
   if (cap > 8192) throw NumErr("neighbour row longer than 8192 entries");
   smem_optin(k_sort_rows, cap * sizeof(uint64_t));
@@ -371,6 +378,52 @@ void Engine::launch_nlist(double cutoff, bool async) {
   DPB_CUDA(cudaMemcpyAsync(ref_pos.p, pos3.p, 3 * n * sizeof(double), cudaMemcpyDeviceToDevice, stream));
   list_cutoff = cutoff;
   list_valid = true;
+}
+
+// A caller-supplied NeighborList (neighbor.hpp:18-23: full, symmetric, rows canonical or not),
+// as compute_energy_forces_virial_tabulated takes it (fused.hpp:70-73). Validated on the host,
+// packed into keys, then sorted and reverse-indexed on the device like a built list.
+void Engine::import_list(const int64_t* off, const int32_t* jj, const int32_t* sh) {
+  if (!off || !jj || !sh) throw InputErr("null neighbour list array");
+  if (off[0] != 0) throw InputErr("neighbour list offsets must start at 0");
+  int mx = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (off[i + 1] < off[i]) throw InputErr("neighbour list offsets must be non-decreasing");
+    mx = std::max<int64_t>(mx, off[i + 1] - off[i]);
+  }
+  const int64_t total = off[n];
+  std::vector<uint64_t> k(total + 1);
+  std::vector<int32_t> own(total + 1);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t e = off[i]; e < off[i + 1]; ++e) {
+      const int j = jj[e];
+      if (j < 0 || j >= n) throw InputErr("neighbour index out of range");
+      for (int x = 0; x < 3; ++x)
+        if (sh[3 * e + x] < -511 || sh[3 * e + x] > 511) throw InputErr("neighbour shift outside +-511 cells");
+      k[e] = make_key(h_types[j], j, sh[3 * e], sh[3 * e + 1], sh[3 * e + 2]);
+      own[e] = static_cast<int32_t>(i);
+    }
+  n_entries = total;
+  max_row = mx;
+  if (total + 1 > e_cap) e_cap = total + total / 8 + 1024;
+  int rc = 2;
+  while (rc < mx + mx / 8) rc <<= 1;
+  row_cap = std::max(row_cap, rc);
+  if (e_cap >= (int64_t(1) << 32)) throw NumErr("more than 2^32 neighbour entries on one GPU");
+  row_off.ensure(n + 1);
+  keys.ensure(e_cap + 1);
+  rev.ensure(e_cap + 1);
+  eown.ensure(e_cap + 1);
+  DPB_CUDA(cudaMemcpyAsync(row_off.p, off, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, stream));
+  DPB_CUDA(cudaMemcpyAsync(keys.p, k.data(), total * sizeof(uint64_t), cudaMemcpyHostToDevice, stream));
+  DPB_CUDA(cudaMemcpyAsync(eown.p, own.data(), total * sizeof(int32_t), cudaMemcpyHostToDevice, stream));
+  finish_list(0.0);
+  DPB_CUDA(cudaStreamSynchronize(stream)); // host staging buffers go out of scope
+  if (pbuf_cap > 0) grow_pbuf();
+  if (plan_dirty) apply_plan();
+  ebin.ensure(e_cap + 1);
+  g.ensure(3 * e_cap + 3);
+  ensure_entry_step_buffers();
 }
 
 void Engine::download_list(int64_t* offsets, int32_t* jout, int32_t* shift) {

@@ -229,3 +229,22 @@ def test_c3_jittered_translation_and_balance(cu):
     assert O.normwise(a.forces, b.forces) <= 1e-9
     fsum = np.abs(a.forces.sum(axis=0)).max()
     assert fsum <= 1e-9 * c.n_atoms * np.abs(a.forces).max()
+
+
+def test_caller_supplied_list_matches_reference_operator(cu):
+    """dp_compute_list: the reference signature compute_energy_forces_virial_tabulated(cfg, model,
+    tables, list) on the reference's own list (brute path at 10 A and cell path at 8 A)."""
+    m, t, pot = cu
+    c = dp.gen_config("copper-like", 8, 8, 8, 0.1, 11)
+    ro, co = O.or_compute(c, m, t)
+    for cut, brute in ((10.0, True), (8.0, False)):
+        L = O.or_neighbor_list(c, cut, brute)
+        r = pot.compute_with_list(c, L)
+        check(r, ro, pot.counters, co)
+    # asymmetric list -> InputError, and the handle stays usable
+    L = O.or_neighbor_list(c, 8.0)
+    bad = dp.NeighborList(L.cutoff, L.offsets.copy(), L.j.copy(), L.shift.copy())
+    bad.j[0] = (bad.j[0] + 1) % c.n_atoms
+    with pytest.raises(dp.InputError):
+        pot.compute_with_list(c, bad)
+    check(pot.compute(c), ro, pot.counters, co)
