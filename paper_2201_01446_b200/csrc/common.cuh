@@ -37,8 +37,9 @@ enum DevErr : int {
   DEV_STALE = 6,       // list stale in MD (md.cpp:211-217)
   DEV_PBUF = 7,        // tabulate group buffer too small (grows at the next list rebuild)
   DEV_TABLE_VERIFY = 8, // GPU-built table does not reproduce the net at a node (table.cpp:133-147)
-  DEV_LIST_CAP = 9,    // asynchronous MD rebuild produced more entries than the list capacity
+  DEV_LIST_CAP = 9,    // a row's entries exceed the chunk's entry capacity (sized from the list)
   DEV_ASYMMETRIC = 10, // list entry (i -> j, s) without its reverse (j -> i, -s)
+  DEV_GCAP = 11,       // more real pairs than the compact pair-gradient buffer holds
 };
 
 // Cell as the kernels see it (geom.hpp:14-44).

@@ -50,7 +50,8 @@ void raise_device_error(int code) {
     case DEV_ROW_CAP: throw NumErr("neighbour row exceeds the kernel capacity");
     case DEV_PBUF: throw NumErr("tabulate group buffer overflow (retry: it grows at the next rebuild)");
     case DEV_TABLE_VERIFY: throw NumErr("table verification failed at a node");
-    case DEV_LIST_CAP: throw NumErr("neighbour list grew past its capacity (+25 %) between MD rebuilds");
+    case DEV_LIST_CAP: throw NumErr("neighbour rows exceed the evaluation chunk's entry capacity");
+    case DEV_GCAP: throw NumErr("more real pairs than the pair-gradient buffer holds (12.5 % above the last list build)");
     case DEV_ASYMMETRIC: throw InputErr("neighbour list is not symmetric: an entry (i -> j, s) has no (j -> i, -s)");
     case DEV_STALE: throw NumErr("neighbor list stale: an atom moved more than half the buffer since the last rebuild");
     default: throw CudaErr("unknown device error " + std::to_string(code));
@@ -225,9 +226,9 @@ void Engine::destroy() {
   tab.release(); tab32.release(); rel(fit_wt); rel(fit_w); rel(fit_b); rel(fit_wout);
   d_max_nbr.release(); tanh_tab.release(); pos4.release(); pos3.release(); vel3.release();
   types.release(); center.release(); slot_of.release(); atom_of.release(); row_off.release(); keys.release();
-  rev.release(); bin_of.release(); bin_start.release(); bin_atoms.release(); bin_fill.release();
+  rev.release(); ridx.release(); inner_cnt.release(); bin_of.release(); bin_start.release(); bin_atoms.release(); bin_fill.release();
   frac.release(); ref_pos.release(); row_len.release(); nl_len.release(); scan_tmp.release();
-  skeys.release(); eown.release(); ebin.release(); egrp.release(); gbin.release(); erc.release(); n_grp.release(); goff.release(); wbase.release(); wcnt.release(); Pbuf.release(); pbuf_cap = 0; n_real.release(); T.release(); D.release(); dD.release(); rel(act_t);
+  rec.release(); egrp.release(); gbin.release(); realoff.release(); rbase.release(); sscr.release(); xbin.release(); xrc.release(); n_grp.release(); goff.release(); Pbuf.release(); pbuf_cap = 0; n_real.release(); T.release(); D.release(); dD.release(); rel(act_t);
   rel(act_y); dz.release(); dy.release(); dz2.release(); dy2.release(); e_slot.release();
   e_atom.release(); g.release(); vpart.release(); forces.release();
   red.release(); counters.release(); err.release(); acc_fac.release();
@@ -453,7 +454,8 @@ void Engine::ensure_step_buffers() {
   n_real.ensure(n);
   n_grp.ensure(n + 1);
   goff.ensure(n + 1);
-  wbase.ensure(n + 1);
+  realoff.ensure(n + 1);
+  rbase.ensure(MAX_CHUNKS + 1);
   pos4.ensure(n);
   pos3.ensure(3 * n);
 }
@@ -464,10 +466,10 @@ void Engine::ensure_entry_step_buffers() {
   if (e_cap == 0) return;
   ck_cap_e = n_chunks == 1 ? e_cap : std::min<int64_t>(e_cap, ck_cap_a * std::max(row_cap, 1));
   const size_t se = static_cast<size_t>(ck_sets) * ck_cap_e;
-  skeys.ensure(se + 1);
   egrp.ensure(se + 1);
   gbin.ensure(se + 1);
-  erc.ensure(5 * se + 5);
+  sscr.ensure(se + 1);
+  rec.ensure(8 * se + 8);
 }
 
 void Engine::upload_positions(const double* pos) {
@@ -475,15 +477,10 @@ void Engine::upload_positions(const double* pos) {
   launch_pos4(*this);
 }
 
-void Engine::build_list(double cutoff, bool async) {
+void Engine::build_list(double cutoff) {
   phase_begin(0);
-  launch_nlist(cutoff, async);
+  launch_nlist(cutoff);
   phase_end();
-  if (pbuf_cap > 0) grow_pbuf();
-  if (plan_dirty) apply_plan();
-  ebin.ensure(e_cap + 1);
-  g.ensure(3 * e_cap + 3);
-  ensure_entry_step_buffers();
 }
 
 void Engine::evaluate() {
@@ -524,6 +521,7 @@ bool Engine::pipeline_ok() const { return pipeline && precision == 0 && Mp <= 12
 void Engine::evaluate_chunked() {
   const bool two = pipeline_ok();
   cudaStream_t last = stream;
+  DPB_CUDA(cudaMemsetAsync(rbase.p, 0, sizeof(int64_t), stream)); // pair-gradient base of chunk 0
   for (int q = 0; q < n_chunks; ++q) {
     const int k = ck_order[q]; // interior chunks first (decomposed runs)
     use_chunk(k, q & 1);
@@ -531,7 +529,7 @@ void Engine::evaluate_chunked() {
     if (two && q >= 1) DPB_CUDA(cudaStreamWaitEvent(st, ev_fwd[(q - 1) & 1], 0));
     if (halo_pending && ck_ghost[k]) DPB_CUDA(cudaStreamWaitEvent(st, ev_halo, 0)); // ghost positions
     phase_begin(1);
-    tab_fwd_range(k, ck_a[k], ck_a[k + 1], st);
+    tab_fwd_range(k, q, ck_a[k], ck_a[k + 1], st);
     if (two) DPB_CUDA(cudaEventRecord(ev_fwd[q & 1], st));
     if (pbuf_cap == 0) {
       // first evaluation of this system/plan: size the group buffer from chunk 0's exact total

@@ -4,12 +4,14 @@
 //   types[n]           int32
 //   row_off[n+1]       int64 CSR offsets of the neighbour rows (list cutoff = r_cut + skin)
 //   keys[E]            uint64 packed (type_j, j, shift) -- rows sorted = type-sectored canonical
-//   rev[E]             uint32 global index of the reverse entry (j -> i, -s) (E < 2^32)
-//   skeys[E]           uint64 per-step real neighbours of each row sorted by (type, interval)
+//   rev[E]             uint16 position of the reverse entry (j -> i, -s) inside row j
+//   ridx[E]            int16 per step: rank of a real entry among its row's reals (list order), -1
+//   realoff[n+1]       int64 per step: first compact pair-gradient slot of each centre
+//   rec[Ec][8]         chunk-local per-real records (R0..R3, u, d) in list-rank order
 //   T[n][4][Mp]        contraction T = sum_k R_k (x) G(s_k)
 //   D/dD[slots][K0p]   descriptor rows (fitting input / its gradient), slot = type-sorted atom
 //   act[...]           fitting activations (t_k, y_k) and adjoints (dz_k, dy_k) per layer
-//   g[E]               double3 pair gradient dE_i/dd_ij at the list entry (0 if not real)
+//   g[G]               double3 pair gradient dE_i/dd_ij of real pair k of centre i at realoff[i] + k
 //   vpart[n][9]        per-centre virial partials, reduced in a fixed order
 #pragma once
 
@@ -154,7 +156,11 @@ struct Engine {
   int row_cap = 0;        // row length capacity (power of two)
   DevBuf<int64_t> row_off;
   DevBuf<uint64_t> keys;
-  DevBuf<uint32_t> rev; // global index of the reverse entry (one dependent load less in k_forces)
+  DevBuf<uint16_t> rev; // position of the reverse entry inside row j (rows <= 8192 entries)
+  DevBuf<int16_t> ridx; // per step: list-order rank of a real entry within its row, -1 otherwise
+  DevBuf<unsigned long long> inner_cnt; // list build: entries inside r_cut (pair-gradient capacity)
+  int64_t g_cap = 0;    // compact pair-gradient capacity (pairs)
+  void set_gcap(int64_t pairs);
   DevBuf<int32_t> bin_of, bin_start, bin_atoms, bin_fill;
   DevBuf<double> frac;
   DevBuf<double> ref_pos;
@@ -165,7 +171,7 @@ struct Engine {
   // ---- chunked evaluation ----
   // Centres are evaluated in chunks of consecutive slots (single centre type; one chunk for
   // several types). Every per-centre step buffer (T, dT, D, dD, activations) and the per-entry
-  // step arrays (erc, skeys, gbin, egrp) exist twice (two buffer sets, chunk k uses set k % 2)
+  // step arrays (rec, sscr, gbin, egrp) exist twice (two buffer sets, chunk k uses set k % 2)
   // and are sized for one chunk, so the step working set no longer grows with the system
   // (13.5 M atoms would need ~1 TB unchunked). Kernels keep global atom / slot indices: the
   // window pointers wa()/ws() are based so that index a0 (s0) of the current chunk lands at
@@ -214,16 +220,16 @@ struct Engine {
   void evaluate_chunked();
 
   // ---- per-step buffers ----
-  DevBuf<uint64_t> skeys;      // [E] reals sorted by (type, interval)
-  DevBuf<int32_t> eown;         // [E] centre of each list entry
-  DevBuf<int32_t> ebin, egrp, gbin;   // [E] bin of real entries (-1 else), group index
-  DevBuf<double> erc;           // [5][E] per-entry R0..R3, u
+  DevBuf<uint64_t> sscr;        // [sets][Ec] sort scratch of k_tab_fwd (wide bin ranges)
+  DevBuf<double> rec;           // [sets][Ec][8] per-real records R0..R3, u, d0..d2 (list-rank order)
+  DevBuf<int32_t> egrp, gbin;   // [sets][Ec] group of real k; the centre's group bins (ascending)
+  DevBuf<int64_t> realoff;      // [n+1] first compact pair-gradient slot of each centre
+  DevBuf<int64_t> rbase;        // [MAX_CHUNKS+1] pair-gradient base of each chunk (evaluation order)
+  DevBuf<int32_t> xbin;         // exact path: [E] neighbour type of a real entry, -1 otherwise
+  DevBuf<double> xrc;           // exact path: [4][E] R0..R3 per entry
   DevBuf<int32_t> n_grp;        // [n+1]
   DevBuf<int64_t> goff;         // [n+1]
   DevBuf<double> Pbuf;          // [groups][24]
-  DevBuf<int64_t> wbase;        // [n+1] forward moments: first Pbuf group of each centre
-  DevBuf<unsigned long long> wcnt; // [2] forward moments: group allocation counter per buffer set
-  bool t2_ok() const;           // forward contraction on the FP64 tensor pipe (k_tab_fwd_T2)
   int64_t pbuf_cap = 0;
   int64_t* h_gtotal = nullptr;  // pinned: total groups per chunk of the last evaluation
   static constexpr int MAX_CHUNKS = 4096;
@@ -289,7 +295,7 @@ struct Engine {
                   const uint8_t* pbc, const uint8_t* center_mask = nullptr);
   void upload_positions(const double* pos);
   // neighbour list at `cutoff`, device resident
-  void build_list(double cutoff, bool async = false);
+  void build_list(double cutoff);
   void sync_entry_count();
   void finish_list(double cutoff);
   void import_list(const int64_t* offsets, const int32_t* j, const int32_t* shift);
@@ -302,9 +308,11 @@ struct Engine {
   void reset_counters();
   void read_counters();
   // kernels (defined in the .cu files)
-  void launch_nlist(double cutoff, bool async);
+  void launch_nlist(double cutoff);
   void launch_tab_fwd();
-  void tab_fwd_range(int c, int64_t i0, int64_t i1, cudaStream_t st);
+  void tab_fwd_range(int k, int q, int64_t i0, int64_t i1, cudaStream_t st);
+  bool virial_in_forces = false; // exact path: the force kernel forms the virial (no records)
+  void zero_ghost_vpart();
   void tab_bwd_range(int c, int64_t i0, int64_t i1, cudaStream_t st);
   void size_pbuf_if_needed();
   void fitting_rows(int64_t r0, int64_t rows, cudaStream_t st); // FP64, single centre type

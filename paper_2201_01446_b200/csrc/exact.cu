@@ -15,6 +15,8 @@
 // G and G' instead of keeping 2 x 128 doubles per pair in HBM, so any system size runs in the
 // same memory as the tabulated path. The fitting net and the force gather are shared with the
 // tabulated path.
+#include <cub/cub.cuh>
+
 #include "tab_common.cuh"
 
 namespace dpb {
@@ -124,13 +126,71 @@ __device__ void embed_warp(const EmbPtrs& w, int d1, const double (&s)[NP], doub
 
 __host__ __device__ __forceinline__ int emb_scratch(int d1) { return 3 * NP * (d1 + 2 * d1); }
 
+// ---------------------------------------------------------------- env-mat (thread per entry)
+// prod_env_mat for the exact path (env_mat.cpp:29-71): real filter and R = (s, s d/r) per list
+// entry; xbin = neighbour type of a real entry, -1 otherwise (the exact path evaluates the
+// embedding net itself, so there is no table interval).
+__global__ void __launch_bounds__(256) k_env_exact(TabParams p) {
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (e >= p.E || e >= p.row_off[p.n]) return;
+  // owner of the entry: binary search of row_off (the exact path is a validation path)
+  int lo = 0, hi = p.n;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (p.row_off[mid] <= e) lo = mid;
+    else hi = mid;
+  }
+  const int i = lo;
+  const uint64_t key = p.keys[e];
+  int bin = -1;
+  if (p.center[i]) {
+    int sh[3];
+    key_shift(key, sh);
+    double d[3];
+    disp_exact(p.c, ld_pos(p.pos, i), ld_pos(p.pos, key_j(key)), sh[0], sh[1], sh[2], d);
+    const double r2 = norm2_exact(d);
+    if (r2 < 1e-12) {
+      raise_err(p.err, DEV_OVERLAP); // env_mat.cpp:33
+    } else if (r2 < p.rc2) {
+      const double r = sqrt(r2);
+      const double ir = 1.0 / r;
+      const double s = switch_fn(r, p.rs, p.rc) * ir;
+      bin = key_type(key);
+      p.xrc[e] = s;
+      p.xrc[p.E + e] = s * (d[0] * ir);
+      p.xrc[2 * p.E + e] = s * (d[1] * ir);
+      p.xrc[3 * p.E + e] = s * (d[2] * ir);
+    }
+  }
+  const_cast<int32_t*>(p.xbin)[e] = bin;
+}
+
+// List ranks of the real entries of every row (ridx, -1 otherwise) and their count: the
+// compact pair-gradient layout the force kernel gathers from (force.cu). Warp per row.
+__global__ void k_exact_rank(TabParams p) {
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= p.n) return;
+  const int64_t off = p.row_off[i];
+  const int len = static_cast<int>(p.row_off[i + 1] - off);
+  int cnt = 0;
+  for (int base = 0; base < len; base += 32) {
+    const int e = base + lane;
+    const bool real = e < len && p.xbin[off + e] >= 0;
+    const unsigned m = __ballot_sync(0xffffffffu, real);
+    if (e < len) p.ridx[off + e] = static_cast<int16_t>(real ? cnt + __popc(m & ((1u << lane) - 1u)) : -1);
+    cnt += __popc(m);
+  }
+  if (lane == 0) p.n_real[i] = cnt;
+}
+
 // Compact the real entries of neighbour type t of row [off, off+len) into idx (list order).
 __device__ __forceinline__ int compact_type(const TabParams& p, int64_t off, int len, int t, int* idx,
                                             int lane) {
   int cnt = 0;
   for (int base = 0; base < len; base += 32) {
     const int e = base + lane;
-    const int bin = e < len ? p.ebin[off + e] : -1;
+    const int bin = e < len ? p.xbin[off + e] : -1;
     const bool take = bin >= 0 && bin == t;
     const unsigned m = __ballot_sync(0xffffffffu, take);
     if (take) idx[cnt + __popc(m & ((1u << lane) - 1u))] = e;
@@ -168,7 +228,7 @@ __global__ void __launch_bounds__(128) k_exact_fwd(TabParams p, const EmbPtrs* n
           const bool ok = c0 + q < cnt;
           const int64_t e = off + (ok ? idx[c0 + q] : 0);
 #pragma unroll
-          for (int a = 0; a < 4; ++a) R[q][a] = ok ? p.erc[a * p.es + e] : 0.0;
+          for (int a = 0; a < 4; ++a) R[q][a] = ok ? p.xrc[a * p.E + e] : 0.0;
           s[q] = R[q][0];
         }
         double g[NP][F], g1[NP][F], g2[NP][F];
@@ -232,11 +292,12 @@ __global__ void __launch_bounds__(128) k_exact_bwd(TabParams p, const EmbPtrs* n
   for (int i = blockIdx.x * wpb + wid; i < p.n; i += gridDim.x * wpb) {
     const int64_t off = p.row_off[i];
     const int len = static_cast<int>(p.row_off[i + 1] - off);
-    for (int e = lane; e < len; e += 32) {
-      double* ge = p.g + 3 * (off + e);
-      ge[0] = ge[1] = ge[2] = 0.0;
-    }
     if (!p.center[i]) continue;
+    const int64_t ro = p.realoff[i];
+    if (ro + p.n_real[i] > p.gcap) {
+      if (lane == 0) raise_err(p.err, DEV_GCAP);
+      continue;
+    }
     // dT = adjoint of D (contract.hpp:21-38), lane features f = lane + 32 k
     const double* Ti = p.T + static_cast<size_t>(i) * 4 * p.Mp;
     double tv[4][F], dT[4][F];
@@ -293,7 +354,7 @@ __global__ void __launch_bounds__(128) k_exact_bwd(TabParams p, const EmbPtrs* n
           const bool ok = c0 + q < cnt;
           const int64_t e = off + (ok ? idx[c0 + q] : 0);
 #pragma unroll
-          for (int a = 0; a < 4; ++a) R[q][a] = ok ? p.erc[a * p.es + e] : 0.0;
+          for (int a = 0; a < 4; ++a) R[q][a] = ok ? p.xrc[a * p.E + e] : 0.0;
           s[q] = R[q][0];
         }
         double g[NP][F], g1[NP][F], g2[NP][F];
@@ -343,7 +404,7 @@ __global__ void __launch_bounds__(128) k_exact_bwd(TabParams p, const EmbPtrs* n
               if (x == y) v += ev.s * ev.ir;
               dd[3 * (1 + y) + x] = v;
             }
-          double* ge = p.g + 3 * e;
+          double* ge = p.g + 3 * (ro + p.ridx[e]); // compact slot of the real pair
 #pragma unroll
           for (int x = 0; x < 3; ++x) {
             double acc = 0.0;
@@ -546,11 +607,23 @@ void Engine::evaluate_exact() {
   }
   use_chunk(0);
   TabParams p = make_params(*this);
-  p.tn = 0;                     // env-mat only: ebin = neighbour type of a real entry
+  p.tn = 0;                     // env-mat only: xbin = neighbour type of a real entry
   p.counters = exact_ctr.p;     // the exact path does not touch the tabulation counters
   const int sms = sm_count_x(device);
+  xbin.ensure(e_cap + 1);
+  xrc.ensure(4 * e_cap + 4);
+  p.xbin = xbin.p;
+  p.xrc = xrc.p;
   phase_begin(1);
-  launch_env_exact();
+  k_env_exact<<<ceil_div(e_cap, 256), 256, 0, stream>>>(p);
+  k_exact_rank<<<ceil_div(static_cast<int64_t>(n) * 32, 256), 256, 0, stream>>>(p);
+  {
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, n_real.p, realoff.p, static_cast<int>(n), stream);
+    scan_tmp.ensure(tb + 1);
+    cub::DeviceScan::ExclusiveSum(scan_tmp.p, tb, n_real.p, realoff.p, static_cast<int>(n), stream);
+  }
+  launches += 3;
   dispatch_exact(p, emb_ptrs.p, d1, true, stream, sms);
   ++launches;
   phase_begin(2);
@@ -562,7 +635,9 @@ void Engine::evaluate_exact() {
   dispatch_exact(p, emb_ptrs.p, d1, false, stream, sms);
   ++launches;
   phase_begin(4);
+  virial_in_forces = true; // no per-real records on this path: d is re-evaluated there
   launch_forces();
+  virial_in_forces = false;
   phase_end();
 }
 

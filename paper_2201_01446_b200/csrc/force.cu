@@ -4,9 +4,10 @@
 // Reference scatter (exact.cpp:22-38): for every centre i and real slot k with neighbour j,
 //   F_i += g, F_j -= g, Xi[3x+y] += d_x g_y.
 // Every list entry (i -> j, s) has its mirror (j -> i, -s) in row j (the list is symmetric,
-// neighbor.cpp:76-79, :147-150), and g is stored per list entry (0 when the env-mat filter
-// dropped it), so each atom can GATHER its force without atomics:
-//   F_i = sum_{e in row i} g[e] - sum_{e in row i} g[rev(e)]
+// neighbor.cpp:76-79, :147-150). The pair gradient of the k-th real entry of row i (list order)
+// is stored compactly at g[realoff[i] + k]; ridx[e] = k (or -1 when the env-mat filter dropped
+// the entry), so each atom can GATHER its force without atomics:
+//   F_i = sum_{real e in row i} g(e) - sum_{e in row i, rev(e) real} g(rev(e))
 // in a fixed order.
 #include "engine.hpp"
 
@@ -14,23 +15,22 @@ namespace dpb {
 
 namespace {
 
-// One warp per atom: F_i = sum_{e in row i} g[e] - sum_{e in row i} g[rev(e)], and the
-// per-centre virial sum_e d_e (x) g_e with d_e re-evaluated exactly as the env-mat did.
-// Only real entries (ebin >= 0) contribute; the k-th real term of the row (in list order, which
-// filtering by cutoff preserves) is always summed by lane k mod 32, so the result is bitwise
-// independent of the list cutoff, as the reference's is (SURVEY.md §8.1 pitfall 1).
-#ifndef FORCES_PREFETCH
-#define FORCES_PREFETCH 1
-#endif
+// One warp per atom. The k-th own term of the row (list order, which filtering by cutoff
+// preserves) and the k-th reverse term are always summed by lane k mod 32, so the result is
+// bitwise independent of the list cutoff, as the reference's is (SURVEY.md §8.1 pitfall 1).
+// VIR: also the per-centre virial sum_k d_k (x) g_k with d re-evaluated exactly as the env-mat
+// did (exact path; the tabulated path forms it in k_tab_bwd_g from its records).
 #ifndef FORCES_MINB
-#define FORCES_MINB 3 // 3 CTAs (24 warps) per SM: 80 registers with the prefetch (91 uncapped ran 18 % slower)
+#define FORCES_MINB 3 // 3 CTAs (24 warps) per SM
 #endif
 
+template <bool VIR>
 __global__ void __launch_bounds__(256, FORCES_MINB) k_forces(int n, DevCell c, const double4* __restrict__ pos,
                                                 const int64_t* __restrict__ row_off,
                                                 const uint64_t* __restrict__ keys,
-                                                const uint32_t* __restrict__ rev,
-                                                const int32_t* __restrict__ ebin,
+                                                const uint16_t* __restrict__ rev,
+                                                const int16_t* __restrict__ ridx,
+                                                const int64_t* __restrict__ realoff,
                                                 const double* __restrict__ g,
                                                 double* __restrict__ f, double* __restrict__ vpart,
                                                 const uint8_t* __restrict__ center, int only,
@@ -49,59 +49,56 @@ __global__ void __launch_bounds__(256, FORCES_MINB) k_forces(int n, DevCell c, c
     i = static_cast<int>(w);
     if (only == 2 && !center[i]) return; // centres only (the ghosts were done from the list)
   }
-  const double3 ri = ld_pos(pos, i);
-  double acc[15];
+  double3 ri;
+  if (VIR) ri = ld_pos(pos, i);
+  constexpr int NACC = VIR ? 15 : 6;
+  double acc[NACC];
 #pragma unroll
-  for (int k = 0; k < 15; ++k) acc[k] = 0.0;
+  for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
   const int64_t e0 = row_off[i], e1 = row_off[i + 1];
+  const double* gi = g + 3 * (center[i] ? realoff[i] : 0);
   int co = 0, cr = 0;
-#if FORCES_PREFETCH
-  // the next 32 entries' key / reverse index / own bin are loaded one iteration ahead
+  // the next 32 entries' key / reverse position / own rank are loaded one iteration ahead
   uint64_t key_n = 0;
-  int64_t m_n = 0;
-  int eo_n = -1;
+  int rv_n = 0, ko_n = -1;
   if (e0 + lane < e1) {
     key_n = keys[e0 + lane];
-    m_n = rev[e0 + lane];
-    eo_n = ebin[e0 + lane];
+    rv_n = rev[e0 + lane];
+    ko_n = ridx[e0 + lane];
   }
-#endif
   for (int64_t base = e0; base < e1; base += 32) {
     const int64_t e = base + lane;
     const bool valid = e < e1;
     double go[3] = {0.0, 0.0, 0.0}, gr[3] = {0.0, 0.0, 0.0}, d[3] = {0.0, 0.0, 0.0};
     bool fo = false, fr = false;
-#if FORCES_PREFETCH
     const uint64_t key = key_n;
-    const int64_t m = m_n; // reverse entry (j -> i, -s), global index
-    const int eo = eo_n;
+    const int rv = rv_n, ko = ko_n;
     if (e + 32 < e1) {
       key_n = keys[e + 32];
-      m_n = rev[e + 32];
-      eo_n = ebin[e + 32];
+      rv_n = rev[e + 32];
+      ko_n = ridx[e + 32];
     }
-#endif
     if (valid) {
-#if !FORCES_PREFETCH
-      const uint64_t key = keys[e];
-      const int64_t m = rev[e]; // reverse entry (j -> i, -s), global index
-      const int eo = ebin[e];
-#endif
       const int j = key_j(key);
-      fo = eo >= 0;
-      fr = ebin[m] >= 0;
+      const int64_t m = row_off[j] + rv; // reverse entry (j -> i, -s)
+      const int kr = ridx[m];
+      fo = ko >= 0;
+      fr = kr >= 0;
       if (fo) {
-        go[0] = g[3 * e];
-        go[1] = g[3 * e + 1];
-        go[2] = g[3 * e + 2];
-        int sh[3];
-        key_shift(key, sh);
-        disp_exact(c, ri, ld_pos(pos, j), sh[0], sh[1], sh[2], d);
+        go[0] = gi[3 * ko];
+        go[1] = gi[3 * ko + 1];
+        go[2] = gi[3 * ko + 2];
+        if (VIR) {
+          int sh[3];
+          key_shift(key, sh);
+          disp_exact(c, ri, ld_pos(pos, j), sh[0], sh[1], sh[2], d);
+        }
       }
       if (fr) {
-        gr[0] = g[3 * m];
-        gr[1] = g[3 * m + 1];
-        gr[2] = g[3 * m + 2];
+        const double* gj = g + 3 * (realoff[j] + kr);
+        gr[0] = gj[0];
+        gr[1] = gj[1];
+        gr[2] = gj[2];
       }
     }
     const unsigned mo = __ballot_sync(0xffffffffu, fo);
@@ -114,15 +111,16 @@ __global__ void __launch_bounds__(256, FORCES_MINB) k_forces(int n, DevCell c, c
 #pragma unroll
       for (int x = 0; x < 3; ++x) {
         v[x] = __shfl_sync(0xffffffffu, go[x], src);
-        v[3 + x] = __shfl_sync(0xffffffffu, d[x], src);
+        if (VIR) v[3 + x] = __shfl_sync(0xffffffffu, d[x], src);
       }
       if (take) {
 #pragma unroll
         for (int x = 0; x < 3; ++x) acc[x] += v[x];
+        if (VIR)
 #pragma unroll
-        for (int x = 0; x < 3; ++x)
+          for (int x = 0; x < 3; ++x)
 #pragma unroll
-          for (int y = 0; y < 3; ++y) acc[6 + 3 * x + y] += v[3 + x] * v[y];
+            for (int y = 0; y < 3; ++y) acc[(6 + 3 * x + y) % NACC] += v[3 + x] * v[y];
       }
     }
     {
@@ -140,15 +138,16 @@ __global__ void __launch_bounds__(256, FORCES_MINB) k_forces(int n, DevCell c, c
     cr += __popc(mr);
   }
 #pragma unroll
-  for (int k = 0; k < 15; ++k) acc[k] = warp_sum(acc[k]);
+  for (int k = 0; k < NACC; ++k) acc[k] = warp_sum(acc[k]);
   if (lane == 0) {
 #pragma unroll
     for (int x = 0; x < 3; ++x) f[3 * i + x] = acc[x] - acc[3 + x];
     if (packed)
 #pragma unroll
       for (int x = 0; x < 3; ++x) packed[3 * w + x] = acc[x] - acc[3 + x];
+    if (VIR)
 #pragma unroll
-    for (int k = 0; k < 9; ++k) vpart[9 * static_cast<int64_t>(i) + k] = acc[6 + k];
+      for (int k = 0; k < 9; ++k) vpart[9 * static_cast<int64_t>(i) + k] = acc[(6 + k) % NACC];
   }
 }
 
@@ -285,7 +284,20 @@ __global__ void k_thermo(int64_t step, int64_t n, double vol, const double* __re
   *out = t;
 }
 
+__global__ void k_zero_ghost_vpart(int64_t n, const uint8_t* __restrict__ center, double* __restrict__ vpart) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n && !center[i])
+#pragma unroll
+    for (int k = 0; k < 9; ++k) vpart[9 * i + k] = 0.0;
+}
+
 } // namespace
+
+// ghosts are no centres: no virial partial (the tabulated path writes the centres' in k_tab_bwd_g)
+void Engine::zero_ghost_vpart() {
+  k_zero_ghost_vpart<<<ceil_div(n, 256), 256, 0, stream>>>(n, center.p, vpart.p);
+  ++launches;
+}
 
 void Engine::launch_forces() {
   const int N = static_cast<int>(n);
@@ -293,22 +305,25 @@ void Engine::launch_forces() {
   int64_t ng = 0;
   const int32_t* glist = nullptr;
   double* gsend = nullptr;
+  // the exact path has no per-real records: its virial is formed here from the re-evaluated d
+  auto kf = virial_in_forces ? k_forces<true> : k_forces<false>;
   if (dist && halo_overlap && dist_ghost_list(*this, &glist, &ng, &gsend) && ng == n - n_centers) {
     // ghost partials first, written straight into the reverse-halo send buffer and sent on
     // st_comm while the owned atoms' forces are computed
-    k_forces<<<std::max(1, ceil_div(ng, 8)), 256, 0, stream>>>(N, cell, pos4.p, row_off.p, keys.p, rev.p, ebin.p,
-                                                               g.p, forces.p, vpart.p, center.p, 1, glist, ng,
-                                                               gsend);
+    kf<<<std::max(1, ceil_div(ng, 8)), 256, 0, stream>>>(N, cell, pos4.p, row_off.p, keys.p, rev.p, ridx.p,
+                                                         realoff.p, g.p, forces.p, vpart.p, center.p, 1, glist, ng,
+                                                         gsend);
     dist_reverse_send(*this);
     // the owned atoms are the local range [0, n_centers) (dist.cu local order)
-    k_forces<<<ceil_div(n_centers, 8), 256, 0, stream>>>(N, cell, pos4.p, row_off.p, keys.p, rev.p, ebin.p,
-                                                          g.p, forces.p, vpart.p, center.p, 2, nullptr, 0, nullptr);
+    kf<<<ceil_div(n_centers, 8), 256, 0, stream>>>(N, cell, pos4.p, row_off.p, keys.p, rev.p, ridx.p, realoff.p,
+                                                    g.p, forces.p, vpart.p, center.p, 2, nullptr, 0, nullptr);
     launches += 2;
   } else {
-    k_forces<<<ceil_div(N, 8), 256, 0, stream>>>(N, cell, pos4.p, row_off.p, keys.p, rev.p, ebin.p,
-                                                  g.p, forces.p, vpart.p, center.p, 0, nullptr, 0, nullptr);
+    kf<<<ceil_div(N, 8), 256, 0, stream>>>(N, cell, pos4.p, row_off.p, keys.p, rev.p, ridx.p, realoff.p, g.p,
+                                            forces.p, vpart.p, center.p, 0, nullptr, 0, nullptr);
     ++launches;
   }
+  if (n_centers < n && !virial_in_forces) zero_ghost_vpart();
   // energy (1 column) then virial (9 columns) with fixed-order tree reductions
   red.ensure(RED_BLOCKS * 10 + 64);
   double* partial = red.p + 64;

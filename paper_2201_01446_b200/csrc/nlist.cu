@@ -19,6 +19,7 @@ namespace {
 struct NlParams {
   DevCell c;
   double cut2;
+  double rc2; // model cutoff^2: the count pass also counts the entries inside it (g capacity)
   double margin[3];
   int nb[3];
   int full[3]; // 1: visit every bin along the axis (fewer than 3 bins), 0: 3-bin stencil
@@ -84,7 +85,7 @@ __global__ void __launch_bounds__(256) k_nlist_warp(NlParams p, const double4* _
                                                     const int* __restrict__ bin_of, const int* __restrict__ bin_start,
                                                     const int* __restrict__ bin_atoms, int64_t* __restrict__ row_len,
                                                     const int64_t* __restrict__ row_off, uint64_t* __restrict__ keys,
-                                                    int32_t* __restrict__ eown, int* err, int64_t e_cap) {
+                                                    unsigned long long* __restrict__ n_inner, int* err, int64_t e_cap) {
   const int lane = threadIdx.x & 31;
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (i >= p.n) return;
@@ -108,6 +109,7 @@ __global__ void __launch_bounds__(256) k_nlist_warp(NlParams p, const double4* _
   const double3 ri = ld_pos(pos, i);
   const double fi[3] = {frac[3 * i], frac[3 * i + 1], frac[3 * i + 2]};
   int64_t count = 0;
+  int inner = 0;
   const int64_t base = WRITE ? row_off[i] : 0;
   for (int o0 = 0; o0 < cnt[0]; ++o0) {
     const int q0 = (first[0] + o0 + p.nb[0]) % p.nb[0];
@@ -149,7 +151,9 @@ __global__ void __launch_bounds__(256) k_nlist_warp(NlParams p, const double4* _
                   if (a == b && s0 == 0 && s1 == 0 && s2 == 0) continue;
                   double d[3];
                   disp_exact(p.c, ra, rb, s0, s1, s2, d);
-                  if (norm2_exact(d) <= p.cut2) ++mine;
+                  const double r2 = norm2_exact(d);
+                  if (r2 <= p.cut2) ++mine;
+                  if (!WRITE && r2 < p.rc2) ++inner;
                 }
           }
           int tot;
@@ -168,7 +172,6 @@ __global__ void __launch_bounds__(256) k_nlist_warp(NlParams p, const double4* _
                       raise_err(err, DEV_SHIFT_RANGE);
                     const int64_t at = base + count + ex + w;
                     keys[at] = make_key(types[j], j, e0, e1, e2);
-                    eown[at] = i;
                     ++w;
                   }
                 }
@@ -178,43 +181,51 @@ __global__ void __launch_bounds__(256) k_nlist_warp(NlParams p, const double4* _
       }
     }
   }
-  if (!WRITE && lane == 0) row_len[i] = count;
+  if (!WRITE) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) inner += __shfl_xor_sync(0xffffffffu, inner, o);
+    if (lane == 0) {
+      row_len[i] = count;
+      atomicAdd(n_inner, static_cast<unsigned long long>(inner));
+    }
+  }
 }
 
-// Reverse entry of every list entry (thread per entry): position of (j -> i, -s) in row j.
-// Rows of non-centre atoms (ghosts of a decomposed run) hold no real entry: ebin = -1 once per
-// list build, so the chunked evaluation only has to cover the centres' rows. Warp per row.
+// Rows of non-centre atoms (ghosts of a decomposed run) hold no real entry: ridx = -1 once per
+// list build (the per-step kernels only visit the centres' rows). Warp per row.
 __global__ void k_mark_ghost_rows(int n, const uint8_t* __restrict__ center, const int64_t* __restrict__ row_off,
-                                  int32_t* __restrict__ ebin, int64_t e_cap) {
+                                  int16_t* __restrict__ ridx) {
   const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (i >= n || center[i]) return;
-  const int64_t e1 = min(row_off[i + 1], e_cap);
-  for (int64_t e = row_off[i] + (threadIdx.x & 31); e < e1; e += 32) ebin[e] = -1;
+  for (int64_t e = row_off[i] + (threadIdx.x & 31); e < row_off[i + 1]; e += 32) ridx[e] = -1;
 }
 
-__global__ void k_reverse_e(const int64_t* __restrict__ row_off, int n, const uint64_t* __restrict__ keys,
-                            const int32_t* __restrict__ eown, const int32_t* __restrict__ types,
-                            uint32_t* __restrict__ rev, int* err, int64_t e_cap) {
-  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (e >= e_cap || e >= row_off[n]) return;
-  const int i = eown[e];
-  const uint64_t k = keys[e];
-  const int j = key_j(k);
-  const uint64_t want = reverse_key(k, types[i], i);
-  const int64_t r0 = row_off[j], r1 = row_off[j + 1];
-  int64_t lo = r0, hi = r1;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (keys[mid] < want)
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
-  if (lo >= r1 || keys[lo] != want) {
-    raise_err(err, DEV_ASYMMETRIC); // the list is not symmetric (a supplied list can be)
-    rev[e] = 0;
-  } else {
-    rev[e] = static_cast<uint32_t>(lo);
+// Reverse entry of every list entry, warp per row: the position of (j -> i, -s) inside row j
+// (rows are at most 8192 long, so 16 bits; the entry is row_off[j] + rev[e]).
+__global__ void k_reverse_rows(const int64_t* __restrict__ row_off, int n, const uint64_t* __restrict__ keys,
+                               const int32_t* __restrict__ types, uint16_t* __restrict__ rev, int* err) {
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= n) return;
+  const int ti = types[i];
+  for (int64_t e = row_off[i] + (threadIdx.x & 31); e < row_off[i + 1]; e += 32) {
+    const uint64_t k = keys[e];
+    const int j = key_j(k);
+    const uint64_t want = reverse_key(k, ti, i);
+    const int64_t r0 = row_off[j], r1 = row_off[j + 1];
+    int64_t lo = r0, hi = r1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (keys[mid] < want)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    if (lo >= r1 || keys[lo] != want) {
+      raise_err(err, DEV_ASYMMETRIC); // the list is not symmetric (a supplied list can be)
+      rev[e] = 0;
+    } else {
+      rev[e] = static_cast<uint16_t>(lo - r0);
+    }
   }
 }
 
@@ -272,7 +283,7 @@ double host_spacing(const DevCell& c, int k) {
 
 } // namespace
 
-void Engine::launch_nlist(double cutoff, bool async) {
+void Engine::launch_nlist(double cutoff) {
   if (!(cutoff > 0.0)) throw InputErr("neighbor cutoff must be positive");
   if (n >= (1ll << 28)) throw InputErr("too many atoms for the packed neighbour key (2^28)");
   NlParams p;
@@ -315,8 +326,11 @@ void Engine::launch_nlist(double cutoff, bool async) {
   DPB_CUDA(cudaMemsetAsync(bin_fill.p, 0, (nbins + 1) * sizeof(int), stream));
   k_bin_fill<<<ceil_div(N, 256), 256, 0, stream>>>(N, bin_of.p, bin_start.p, bin_fill.p, bin_atoms.p);
   ++launches;
+  inner_cnt.ensure(1);
+  DPB_CUDA(cudaMemsetAsync(inner_cnt.p, 0, sizeof(unsigned long long), stream));
+  p.rc2 = r_cut * r_cut;
   k_nlist_warp<false><<<ceil_div(static_cast<int64_t>(N) * 32, 256), 256, 0, stream>>>(
-      p, pos4.p, frac.p, types.p, bin_of.p, bin_start.p, bin_atoms.p, lens.p, nullptr, nullptr, nullptr, err.p, 0);
+      p, pos4.p, frac.p, types.p, bin_of.p, bin_start.p, bin_atoms.p, lens.p, nullptr, nullptr, inner_cnt.p, err.p, 0);
   ++launches;
   DPB_CUDA(cudaMemsetAsync(lens.p + n, 0, sizeof(int64_t), stream));
   size_t tmp2 = 0;
@@ -327,57 +341,67 @@ void Engine::launch_nlist(double cutoff, bool async) {
   DPB_CUDA(cudaMemsetAsync(row_len.p, 0, sizeof(int), stream));
   k_max_len<<<std::min(ceil_div(N, 256), 1024), 256, 0, stream>>>(N, lens.p, row_len.p);
   ++launches;
-  // Sizing. A synchronous build reads the total and the longest row back and sizes every
-  // per-entry buffer with slack; an asynchronous rebuild (MD) keeps the capacities and lets the
-  // kernels check them on the device (DEV_LIST_CAP / DEV_ROW_CAP), so the host never waits.
-  if (!async || e_cap == 0 || row_cap == 0) {
-    int64_t total = 0;
-    int mx = 0;
-    DPB_CUDA(cudaMemcpyAsync(&total, row_off.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
-    DPB_CUDA(cudaMemcpyAsync(&mx, row_len.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
-    DPB_CUDA(cudaStreamSynchronize(stream));
-    n_entries = total;
-    max_row = mx;
-    // slack for the growth of the list between synchronous builds: 25 %, 6 % above 2^28
-    // entries (a 13.5 M-atom slab holds 1.2e9; its per-entry arrays are 44 B each)
-    if (total + 1 > e_cap) e_cap = total + (total < (int64_t(1) << 28) ? total / 4 : total / 16) + 1024;
-    int rc = 2;
-    while (rc < mx + mx / 8) rc <<= 1;
-    if (rc > row_cap) row_cap = rc;
-  } else {
-    n_entries = -1; // known on the device only (row_off[n])
-  }
-  if (e_cap >= (int64_t(1) << 32)) throw NumErr("more than 2^32 neighbour entries on one GPU");
+  // Sizing: the total, the longest row and the number of entries inside r_cut are read back (one
+  // sync per build; MD rebuilds every rebuild_every steps) and every per-entry buffer is sized
+  // for this list, so no kernel can index past a capacity.
+  int64_t total = 0;
+  int mx = 0;
+  unsigned long long inner = 0;
+  DPB_CUDA(cudaMemcpyAsync(&total, row_off.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+  DPB_CUDA(cudaMemcpyAsync(&mx, row_len.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  DPB_CUDA(cudaMemcpyAsync(&inner, inner_cnt.p, sizeof(inner), cudaMemcpyDeviceToHost, stream));
+  DPB_CUDA(cudaStreamSynchronize(stream));
+  n_entries = total;
+  max_row = mx;
+  if (total + 1 > e_cap) e_cap = total + total / 16 + 1024;
+  int rc = 2;
+  while (rc < mx + mx / 8) rc <<= 1;
+  if (rc > row_cap) row_cap = rc;
+  // pair gradients are stored for real pairs only (compact, realoff[i] + rank): the pairs inside
+  // r_cut at build time + 12.5 % for their drift until the next rebuild (checked on the device)
+  set_gcap(static_cast<int64_t>(inner) + static_cast<int64_t>(inner / 8) + 4096);
   keys.ensure(e_cap + 1);
-  rev.ensure(e_cap + 1);
-  eown.ensure(e_cap + 1);
   k_nlist_warp<true><<<ceil_div(static_cast<int64_t>(N) * 32, 256), 256, 0, stream>>>(
-      p, pos4.p, frac.p, types.p, bin_of.p, bin_start.p, bin_atoms.p, nullptr, row_off.p, keys.p, eown.p, err.p,
+      p, pos4.p, frac.p, types.p, bin_of.p, bin_start.p, bin_atoms.p, nullptr, row_off.p, keys.p, nullptr, err.p,
       e_cap);
   ++launches;
   finish_list(cutoff);
 }
 
-// Rows are filled (keys, eown, row_off, capacities): sort them into the type-sectored canonical
+void Engine::set_gcap(int64_t want) {
+  want = std::min<int64_t>(want, e_cap);
+  if (want > g_cap || want < g_cap / 2) {
+    g.release();
+    g.ensure(3 * want + 3);
+    g_cap = want;
+  }
+}
+
+// Rows are filled (keys, row_off, capacities): sort them into the type-sectored canonical
 // order, index the reverse entries, mark ghost rows, snapshot the positions.
 void Engine::finish_list(double cutoff) {
   const int N = static_cast<int>(n);
   const int cap = row_cap;
   if (cap > 8192) throw NumErr("neighbour row longer than 8192 entries");
+  rev.ensure(e_cap + 1);
+  ridx.ensure(e_cap + 1);
   smem_optin(k_sort_rows, cap * sizeof(uint64_t));
   k_sort_rows<<<N, 256, cap * sizeof(uint64_t), stream>>>(N, row_off.p, keys.p, cap, err.p);
   ++launches;
-  k_reverse_e<<<ceil_div(e_cap, 256), 256, 0, stream>>>(row_off.p, N, keys.p, eown.p, types.p, rev.p, err.p, e_cap);
+  k_reverse_rows<<<ceil_div(static_cast<int64_t>(N) * 32, 256), 256, 0, stream>>>(row_off.p, N, keys.p, types.p,
+                                                                                  rev.p, err.p);
   ++launches;
   if (n_centers < n) {
-    ebin.ensure(e_cap + 1);
-    k_mark_ghost_rows<<<ceil_div(N, 8), 256, 0, stream>>>(N, center.p, row_off.p, ebin.p, e_cap);
+    k_mark_ghost_rows<<<ceil_div(N, 8), 256, 0, stream>>>(N, center.p, row_off.p, ridx.p);
     ++launches;
   }
   ref_pos.ensure(3 * n);
   DPB_CUDA(cudaMemcpyAsync(ref_pos.p, pos3.p, 3 * n * sizeof(double), cudaMemcpyDeviceToDevice, stream));
   list_cutoff = cutoff;
   list_valid = true;
+  if (pbuf_cap > 0) grow_pbuf();
+  if (plan_dirty) apply_plan();
+  ensure_entry_step_buffers();
 }
 
 // A caller-supplied NeighborList (neighbor.hpp:18-23: full, symmetric, rows canonical or not),
@@ -393,7 +417,6 @@ void Engine::import_list(const int64_t* off, const int32_t* jj, const int32_t* s
   }
   const int64_t total = off[n];
   std::vector<uint64_t> k(total + 1);
-  std::vector<int32_t> own(total + 1);
   for (int64_t i = 0; i < n; ++i)
     for (int64_t e = off[i]; e < off[i + 1]; ++e) {
       const int j = jj[e];
@@ -401,7 +424,6 @@ void Engine::import_list(const int64_t* off, const int32_t* jj, const int32_t* s
       for (int x = 0; x < 3; ++x)
         if (sh[3 * e + x] < -511 || sh[3 * e + x] > 511) throw InputErr("neighbour shift outside +-511 cells");
       k[e] = make_key(h_types[j], j, sh[3 * e], sh[3 * e + 1], sh[3 * e + 2]);
-      own[e] = static_cast<int32_t>(i);
     }
   n_entries = total;
   max_row = mx;
@@ -409,21 +431,13 @@ void Engine::import_list(const int64_t* off, const int32_t* jj, const int32_t* s
   int rc = 2;
   while (rc < mx + mx / 8) rc <<= 1;
   row_cap = std::max(row_cap, rc);
-  if (e_cap >= (int64_t(1) << 32)) throw NumErr("more than 2^32 neighbour entries on one GPU");
+  set_gcap(total + 1);
   row_off.ensure(n + 1);
   keys.ensure(e_cap + 1);
-  rev.ensure(e_cap + 1);
-  eown.ensure(e_cap + 1);
   DPB_CUDA(cudaMemcpyAsync(row_off.p, off, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, stream));
   DPB_CUDA(cudaMemcpyAsync(keys.p, k.data(), total * sizeof(uint64_t), cudaMemcpyHostToDevice, stream));
-  DPB_CUDA(cudaMemcpyAsync(eown.p, own.data(), total * sizeof(int32_t), cudaMemcpyHostToDevice, stream));
   finish_list(0.0);
   DPB_CUDA(cudaStreamSynchronize(stream)); // host staging buffers go out of scope
-  if (pbuf_cap > 0) grow_pbuf();
-  if (plan_dirty) apply_plan();
-  ebin.ensure(e_cap + 1);
-  g.ensure(3 * e_cap + 3);
-  ensure_entry_step_buffers();
 }
 
 void Engine::download_list(int64_t* offsets, int32_t* jout, int32_t* shift) {

@@ -13,21 +13,20 @@ struct TabParams {
   const double4* pos;
   const int64_t* row_off;
   const uint64_t* keys;
-  const int32_t* eown;  // [E] centre of each list entry
   const uint8_t* center; // [n] 1 = evaluated centre, 0 = ghost
-  int32_t* ebin;        // [E] global bin t*tn + interval of a real entry, -1 otherwise
-  double* erc;          // [5][E] SoA: R0..R3, u of real entries
-  int32_t* egrp;        // [E] group index of a real entry inside its centre
-  int32_t* gbin;        // [E] per row: the centre's group bins, ascending (first n_grp entries)
-  uint64_t* skeys;      // [E] per row: reals sorted by bin, (bin << 32 | entry)
+  int16_t* ridx;        // [E] list rank of a real entry within its row, -1 otherwise
+  double* rec;          // [Ec][8] per-real records R0..R3, u, d0..d2 (chunk-local, rank order)
+  uint64_t* sscr;       // [Ec] sort scratch (wide bin ranges)
+  int32_t* egrp;        // [Ec] group index of real k of a centre (chunk-local, rank order)
+  int32_t* gbin;        // [Ec] per row: the centre's group bins, ascending (first n_grp entries)
   int32_t* n_real;      // [n]
   int32_t* n_grp;       // [n+1] groups per centre -> (scanned) offsets into Pbuf
   const int64_t* goff;  // [n+1] exclusive scan of n_grp
+  const int64_t* realoff; // [n+1] first compact pair-gradient slot of each centre
   double* Pbuf;         // [sum groups][24]
   int64_t pcap;         // groups Pbuf can hold
-  int64_t* wbase;       // [n] forward W-mode: first Pbuf group of each centre's moments (-1: none)
-  unsigned long long* wcnt; // forward W-mode: group allocation counter of the chunk
-  int count_only;       // forward W-mode: groups only (first evaluation sizes Pbuf from them)
+  const int32_t* xbin;  // exact path: [E] neighbour type of a real entry, -1 otherwise
+  double* xrc;          // exact path: [4][E] R0..R3 per entry
   const double* tab;    // [type][interval][6][Mp]
   const float* tab32;   // the same in FP32 (mixed mode forward contraction) or null
   const int* max_nbr;
@@ -37,14 +36,16 @@ struct TabParams {
   int tn;
   int n, n_types, M, Mp, mlt, K0p;
   int i0, i1;           // centre range of this launch (pipelined halves); [0, n) otherwise
-  int64_t E;            // global entry capacity (bound of ebin / g)
-  int64_t es;           // SoA stride of the chunk-local entry arrays (erc, skeys, gbin, egrp)
+  int64_t E;            // global entry capacity
+  int64_t es;           // capacity of the chunk-local entry arrays (rec, egrp, gbin, sscr)
   const int32_t* slot_of;
   double* T;            // [n][4][Mp]
   double* D;            // [slots][K0p] (FP64 mode)
   float* D2;            // [slots][2*K0p] mixed mode: tf32 split (hi | lo) of D, the tcgen05 operand
   const double* dD;
-  double* g;            // [E][3]
+  double* g;            // [gcap][3] compact pair gradients
+  int64_t gcap;
+  double* vpart;        // [n][9] per-centre virial partials
   unsigned long long* counters;
   int* err;
   int scap;
@@ -54,17 +55,6 @@ __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
-}
-
-// L2 prefetch of [ptr, ptr + bytes) by the bulk-copy engine: one instruction, no destination
-// registers. The range is widened to 16-byte boundaries (the bulk-prefetch granularity); every
-// DevBuf carries at least 64 elements of slack past its end, and allocations are 256-B aligned.
-__device__ __forceinline__ void l2_prefetch(const void* ptr, size_t bytes) {
-  const uintptr_t a = reinterpret_cast<uintptr_t>(ptr) & ~uintptr_t(15);
-  const uintptr_t e = (reinterpret_cast<uintptr_t>(ptr) + bytes + 15) & ~uintptr_t(15);
-  if (e > a)
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a), "r"(static_cast<uint32_t>(e - a))
-                 : "memory");
 }
 
 __device__ __forceinline__ double node_x(double x0, double h, int th) {
@@ -213,21 +203,20 @@ inline TabParams make_params(Engine& E) {
   p.pos = E.pos4.p;
   p.row_off = E.row_off.p;
   p.keys = E.keys.p;
-  p.eown = E.eown.p;
   p.center = E.center.p;
-  p.ebin = E.ebin.p;
-  p.erc = E.we(E.erc, 5); // chunk-local entry arrays of the current buffer set
+  p.ridx = E.ridx.p;
+  p.rec = E.we(E.rec, 8); // chunk-local entry arrays of the current buffer set
+  p.sscr = E.we(E.sscr);
   p.egrp = E.we(E.egrp);
   p.gbin = E.we(E.gbin);
-  p.skeys = E.we(E.skeys);
   p.n_real = E.n_real.p;
   p.n_grp = E.n_grp.p;
   p.goff = E.goff.p;
+  p.realoff = E.realoff.p;
   p.Pbuf = E.Pbuf.p;
   p.pcap = E.pbuf_cap;
-  p.wbase = E.wbase.p;
-  p.wcnt = E.wcnt.p;
-  p.count_only = 0;
+  p.xbin = E.xbin.p;
+  p.xrc = E.xrc.p;
   p.tab = E.tab.p;
   p.tab32 = E.precision == 1 ? E.tab32.p : nullptr;
   p.max_nbr = E.d_max_nbr.p;
@@ -247,7 +236,7 @@ inline TabParams make_params(Engine& E) {
   p.Mp = E.Mp;
   p.mlt = E.mlt;
   p.K0p = E.K0p;
-  p.E = E.e_cap;   // grid bound of the global entry arrays; the live count is row_off[n]
+  p.E = E.e_cap;
   p.es = E.ck_cap_e; // chunk-local entry arrays are indexed e - row_off[i0] (see chunk_params)
   p.slot_of = E.slot_of.p;
   p.T = E.wa(E.T, 4 * E.Mp); // per-centre windows of the current chunk (Engine::use_chunk)
@@ -255,6 +244,8 @@ inline TabParams make_params(Engine& E) {
   p.D2 = E.precision == 1 ? E.ws(E.tc_d2, 2 * E.K0p) : nullptr;
   p.dD = E.ws(E.dD, E.K0p);
   p.g = E.g.p;
+  p.gcap = E.g_cap;
+  p.vpart = E.vpart.p;
   p.counters = E.counters.p;
   p.err = E.err.p;
   int scap = 32;

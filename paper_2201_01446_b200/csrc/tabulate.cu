@@ -17,12 +17,15 @@
 // so the embedding matrix G is never formed (not even one row at a time), and each touched
 // coefficient block (6 x M doubles) is read once per centre instead of once per neighbour.
 //
-// Kernels (per evaluation):
-//   k_env_fwd    one thread per list entry: env-mat, real filter, interval, (R, u)   [parallel]
-//   k_tab_fwd    one warp per centre: stable counting sort of reals by (type, interval),
-//                group moments, T = W . C, D = T<^T T
-//   k_tab_bwd_P  one warp per centre: dT from dD, interval projections P per group
-//   k_tab_bwd_g  one thread per list entry: dE_i/dd_ij from P, written at the entry   [parallel]
+// Kernels (per evaluation chunk):
+//   k_tab_fwd    one warp per centre: env-mat of the row (list order), real filter, interval,
+//                compact per-real records (R, u, d) + list ranks (ridx), stable counting sort of
+//                the reals by (type, interval), group moments, T = W . C, D = T<^T T
+//   k_tab_dT     one warp per centre: dT from dD (contract.hpp:21-38)
+//   k_tab_bwd_P2 32 centres per CTA: interval projections P per group on DMMA (k_tab_bwd_P per
+//                warp for blocks with a too wide interval union)
+//   k_tab_bwd_g  one warp per centre: dE_i/dd_ij from P and the records, written compactly at
+//                g[realoff[i] + k], and the centre's virial
 // All reductions have a fixed order, so results are bitwise reproducible run to run.
 #include <chrono>
 #include <cstdio>
@@ -37,77 +40,15 @@ namespace dpb {
 
 namespace {
 
-// ---------------------------------------------------------------- k_env_fwd (thread per entry)
-__global__ void __launch_bounds__(256) k_env_fwd(TabParams p) {
-  // entries of the centre range [i0, i1); chunk-local arrays at el = e - row_off[i0]
-  const int64_t eb = p.row_off[p.i0];
-  const int64_t el = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  const int64_t e = eb + el;
-  bool ext = false;
-  const bool in_range = e < p.E && e < p.row_off[p.i1];
-  if (in_range && el >= p.es) raise_err(p.err, DEV_LIST_CAP); // chunk entry capacity (never expected)
-  const bool live = in_range && el < p.es;
-  // owner and key loaded together (independent), then the centre flag and the positions
-  const int i = live ? p.eown[e] : 0;
-  const uint64_t key = live ? p.keys[e] : 0;
-  const bool cen = live && p.center[i];
-  if (live && !cen) p.ebin[e] = -1;
-  if (cen) {
-    int sh[3];
-    key_shift(key, sh);
-    double d[3];
-    disp_exact(p.c, ld_pos(p.pos, i), ld_pos(p.pos, key_j(key)), sh[0], sh[1], sh[2], d);
-    const double r2 = norm2_exact(d);
-    int bin = -1;
-    if (r2 < 1e-12) {
-      raise_err(p.err, DEV_OVERLAP); // env_mat.cpp:33 throws before any table lookup
-    } else if (r2 < p.rc2 && p.tn == 0) {
-      // exact path: no table; the real entry is tagged with its neighbour type
-      const double r = sqrt(r2);
-      const double ir = 1.0 / r;
-      const double s = switch_fn(r, p.rs, p.rc) * ir;
-      bin = key_type(key);
-      p.erc[el] = s;
-      p.erc[p.es + el] = s * (d[0] * ir);
-      p.erc[2 * p.es + el] = s * (d[1] * ir);
-      p.erc[3 * p.es + el] = s * (d[2] * ir);
-    } else if (r2 < p.rc2) {
-      const double r = sqrt(r2);
-      const double ir = 1.0 / r;
-      const double s = switch_fn(r, p.rs, p.rc) * ir;
-      const int th = locate(p, s, ext, p.err);
-      bin = key_type(key) * p.tn + th;
-      p.erc[el] = s;
-      p.erc[p.es + el] = s * (d[0] * ir);
-      p.erc[2 * p.es + el] = s * (d[1] * ir);
-      p.erc[3 * p.es + el] = s * (d[2] * ir);
-      p.erc[4 * p.es + el] = s - node_x(p.x0, p.h, th);
-    }
-    p.ebin[e] = bin;
-  }
-  const unsigned m = __ballot_sync(0xffffffffu, ext);
-  if ((threadIdx.x & 31) == 0 && m) atomicAdd(p.counters + 2, static_cast<unsigned long long>(__popc(m)));
-}
-
 // ---------------------------------------------------------------- per-warp shared memory
 constexpr int HCAP = 256; // counting-sort bins; wider (type, interval) ranges use a bitonic sort
 constexpr int GB = 8;     // groups per batch
 #ifndef TAB_FWD_MINB
 #define TAB_FWD_MINB 8 // 2-warp CTAs per SM: 128 registers, 16 warps per SM
 #endif
-#ifndef TAB_EBIN_PREFETCH
-#define TAB_EBIN_PREFETCH 1
-#endif
-#ifndef TAB_L2_PREFETCH
-#define TAB_L2_PREFETCH 0 // bulk L2 prefetch of the next centre's rows: measured 0.03 ms/step slower
-#endif
-#ifndef TAB_MOMENT_PAIR
-#define TAB_MOMENT_PAIR 1 // members per lane iteration of the moment sums (2: two gathers in flight, measured neutral)
-#endif
 
 struct FwdSmem {
   uint32_t* rk; // [scap] bin of real k (list order)
-  uint16_t* ex; // [scap] entry of real k
   uint16_t* rn; // [scap] stable rank of real k inside its bin
   uint16_t* od; // [scap] sorted position -> k
   int* hs;      // [HCAP + 1] bin counts -> bin starts
@@ -148,8 +89,6 @@ __device__ __forceinline__ FwdSmem carve_fwd(unsigned char* base, int scap, int 
   w.tc = reinterpret_cast<int*>(q);
   q += 64 * 4;
   w.od = reinterpret_cast<uint16_t*>(q);
-  q += static_cast<size_t>(scap) * 2;
-  w.ex = reinterpret_cast<uint16_t*>(q);
   return w;
 }
 
@@ -264,15 +203,22 @@ __device__ int sort_and_group(const FwdSmem& w, uint64_t* scratch, int nreal, in
 }
 
 // ---------------------------------------------------------------- k_tab_fwd (warp per centre)
+// prod_env_mat + tabulate_fusion forward in one pass over the centre's row (fused.cpp:182-202):
+//  A  entries in list order, 32 per step: key, neighbour position (one 32-byte gather), exact
+//     displacement and r^2, the env-mat filter r^2 < r_c^2 (env_mat.cpp:32), s = w(r)/r, the
+//     table interval (locate), R = (s, s d/r) and u = s - node. Every real entry gets its list
+//     rank k (ridx, 16 bits) and a 64-byte record rec[k] = (R0..R3, u, d0..d2) -- written
+//     densely, in rank order, into the chunk's record buffer, which the moments below and the
+//     backward pass (k_tab_bwd_g) read back; nothing else per entry reaches HBM.
+//  B  stable counting sort of the reals by (type, interval) -> groups (sort_and_group)
+//  C  group moments W[a][m] = sum_k R_k[a] u_k^m (members in sorted order), then
+//     T += W . C[interval] with lanes owning features
+//  D  T out, D = T<^T T (contract.hpp:9-17) as the fitting input
 // Features are owned in contiguous runs: lane l holds f = F*l .. F*l + F-1.
 // F32 (mixed mode, SURVEY §8d C3 "mixed-precision tabulate_fusion"): the contraction T += W . C
 // runs on FP32 coefficients and accumulators (half the coefficient traffic, 2x the FP64 rate);
 // the moments W stay FP64. FP64 mode (F32 = false) is the parity path.
-// WM (FP64 W-mode): the kernel stops after the sort and the group moments, which it
-// writes to Pbuf[wbase[i] + g][a][m] (groups allocated per centre from p.wcnt); k_tab_fwd_T2 then
-// contracts them with the coefficients on the FP64 tensor pipe and forms T and D. p.count_only:
-// n_grp only (first evaluation of a system, to size Pbuf).
-template <int F, bool F32 = false, bool WM = false>
+template <int F, bool F32 = false>
 __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
   using acc_t = typename std::conditional<F32, float, double>::type;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -287,87 +233,93 @@ __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
     const int64_t off = p.row_off[i];
     const int64_t loff = off - eb; // chunk-local entry offset
     const int len = static_cast<int>(p.row_off[i + 1] - off);
-#if TAB_L2_PREFETCH
-    {
-      // the warp's next centre: its bins (lane 0) and the five (R, u) slices (lanes 1-5)
-      const int in = i + gridDim.x * wpb;
-      if (in < p.i1 && lane < 6) {
-        const int64_t o2 = p.row_off[in];
-        const int64_t l2 = p.row_off[in + 1] - o2;
-        if (lane == 0) l2_prefetch(p.ebin + o2, static_cast<size_t>(l2) * 4);
-        else l2_prefetch(p.erc + static_cast<size_t>(lane - 1) * p.es + (o2 - eb), static_cast<size_t>(l2) * 8);
+    if (!p.center[i]) {
+      for (int e = lane; e < len; e += 32) p.ridx[off + e] = -1;
+      if (lane == 0) {
+        p.n_real[i] = 0;
+        p.n_grp[i] = 0;
       }
+      continue;
     }
-#endif
+    if (loff + len > p.es) { // chunk record capacity (sized from the list; never expected)
+      if (lane == 0) raise_err(p.err, DEV_LIST_CAP);
+      continue;
+    }
     for (int t = lane; t < 64; t += 32) w.tc[t] = 0;
     __syncwarp();
-    // --- compaction of the reals (list order), per-type counts ---
+    const double3 ri = ld_pos(p.pos, i);
+    double* recs = p.rec + loff * 8;
+    // --- A: env-mat of the row, compaction of the reals (list order) ---
     int nreal = 0, kmin = 0x7fffffff, kmax = -1;
-#if TAB_EBIN_PREFETCH
-    int bin_nx = lane < len ? p.ebin[off + lane] : -1; // next 32 bins in flight
-#endif
+    uint64_t key_nx = lane < len ? p.keys[off + lane] : 0; // next 32 keys in flight
     for (int base = 0; base < len; base += 32) {
       const int e = base + lane;
-#if TAB_EBIN_PREFETCH
-      const int bin = bin_nx;
-      if (base + 32 < len) bin_nx = e + 32 < len ? p.ebin[off + e + 32] : -1;
-#else
-      const int bin = e < len ? p.ebin[off + e] : -1;
-#endif
-      const bool real = bin >= 0;
+      const bool valid = e < len;
+      const uint64_t key = key_nx;
+      if (base + 32 < len) key_nx = e + 32 < len ? p.keys[off + e + 32] : 0;
+      double d[3] = {0.0, 0.0, 0.0};
+      double r2 = 0.0;
+      if (valid) {
+        int sh[3];
+        key_shift(key, sh);
+        disp_exact(p.c, ri, ld_pos(p.pos, key_j(key)), sh[0], sh[1], sh[2], d);
+        r2 = norm2_exact(d);
+        if (r2 < 1e-12) raise_err(p.err, DEV_OVERLAP); // env_mat.cpp:33
+      }
+      const bool real = valid && r2 >= 1e-12 && r2 < p.rc2;
+      bool ext = false;
+      int bin = -1;
+      double R[4] = {0.0, 0.0, 0.0, 0.0}, uu = 0.0;
+      if (real) {
+        const double r = sqrt(r2);
+        const double ir = 1.0 / r;
+        const double s = switch_fn(r, p.rs, p.rc) * ir;
+        const int th = locate(p, s, ext, p.err);
+        bin = key_type(key) * p.tn + th;
+        R[0] = s;
+        R[1] = s * (d[0] * ir);
+        R[2] = s * (d[1] * ir);
+        R[3] = s * (d[2] * ir);
+        uu = s - node_x(p.x0, p.h, th);
+      }
       const unsigned m = __ballot_sync(0xffffffffu, real);
+      const int k = nreal + __popc(m & ((1u << lane) - 1u));
+      if (valid) p.ridx[off + e] = static_cast<int16_t>(real ? k : -1);
       const int t = real ? bin / p.tn : -1;
       if (real) {
-        const int at = nreal + __popc(m & ((1u << lane) - 1u));
-        w.rk[at] = static_cast<uint32_t>(bin);
-        w.ex[at] = static_cast<uint16_t>(e);
+        w.rk[k] = static_cast<uint32_t>(bin);
+        double2* rp = reinterpret_cast<double2*>(recs + static_cast<int64_t>(k) * 8);
+        rp[0] = make_double2(R[0], R[1]);
+        rp[1] = make_double2(R[2], R[3]);
+        rp[2] = make_double2(uu, d[0]);
+        rp[3] = make_double2(d[1], d[2]);
         kmin = min(kmin, bin);
         kmax = max(kmax, bin);
       }
       const unsigned tm = __match_any_sync(0xffffffffu, t);
       if (real && (tm & ((1u << lane) - 1u)) == 0) w.tc[t] += __popc(tm);
+      const unsigned xm = __ballot_sync(0xffffffffu, ext);
+      if (lane == 0 && xm) atomicAdd(p.counters + 2, static_cast<unsigned long long>(__popc(xm)));
       nreal += __popc(m);
       __syncwarp();
     }
     kmin = warp_min(kmin);
     kmax = warp_max(kmax);
     for (int t = lane; t < p.n_types; t += 32)
-      if (w.tc[t] > p.max_nbr[t]) raise_err(p.err, DEV_OVERFLOW);
-    const int G = sort_and_group(w, p.skeys + loff, nreal, kmin, kmax, lane);
+      if (w.tc[t] > p.max_nbr[t]) raise_err(p.err, DEV_OVERFLOW); // env_mat.cpp:37-39
+    // --- B: groups ---
+    const int G = sort_and_group(w, p.sscr + loff, nreal, kmin, kmax, lane);
     if (lane == 0) {
-      if (!WM || !p.count_only) atomicAdd(p.counters + 0, static_cast<unsigned long long>(nreal));
+      atomicAdd(p.counters + 0, static_cast<unsigned long long>(nreal));
       p.n_real[i] = nreal;
       p.n_grp[i] = G;
     }
-    int64_t wb = -1;
-    if constexpr (WM) {
-      if (p.count_only) {
-        __syncwarp();
-        continue;
-      }
-      if (lane == 0) {
-        const int64_t b = static_cast<int64_t>(atomicAdd(p.wcnt, static_cast<unsigned long long>(G)));
-        if (b + G > p.pcap) raise_err(p.err, DEV_PBUF);
-        else wb = b;
-        p.wbase[i] = wb;
-      }
-      wb = __shfl_sync(0xffffffffu, wb, 0);
-    }
-    for (int j = lane; j < nreal; j += 32) {
-      const int k = w.od[j];
-      p.skeys[loff + j] = (static_cast<uint64_t>(w.rk[k]) << 32) | w.ex[k];
-    }
     for (int g = lane; g < G; g += 32) {
       p.gbin[loff + g] = w.gb[g];
-      for (int j = w.gs[g]; j < w.gs[g + 1]; ++j) p.egrp[loff + w.ex[w.od[j]]] = g;
+      for (int j = w.gs[g]; j < w.gs[g + 1]; ++j) p.egrp[loff + w.od[j]] = g;
     }
-    if constexpr (WM) {
-      if (wb < 0) {
-        __syncwarp();
-        continue;
-      }
-    }
-    // --- moments of each (type, interval) group, then T += W . C[interval] ---
+    __syncwarp(); // the records written above are read back by other lanes below
+    // --- C: moments of each (type, interval) group, then T += W . C[interval] ---
     acc_t tacc[4][F];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
@@ -422,31 +374,17 @@ __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
         for (int k = 0; k < 24; ++k) Wv[k] = 0.0;
         if (g < G) {
           const int j1 = w.gs[g + 1];
-          // members j, j + 4 of this lane loaded together (two gathers in flight), accumulated in
-          // member order
-          for (int j = w.gs[g] + r; j < j1; j += 4 * TAB_MOMENT_PAIR) {
-            const bool two = TAB_MOMENT_PAIR == 2 && j + 4 < j1;
-            const int64_t e = loff + w.ex[w.od[j]];
-            const int64_t e2 = two ? loff + w.ex[w.od[j + 4]] : e;
-            const double R[4] = {p.erc[e], p.erc[p.es + e], p.erc[2 * p.es + e], p.erc[3 * p.es + e]};
-            const double uu = p.erc[4 * p.es + e];
-            const double R2[4] = {p.erc[e2], p.erc[p.es + e2], p.erc[2 * p.es + e2], p.erc[3 * p.es + e2]};
-            const double uu2 = p.erc[4 * p.es + e2];
+          for (int j = w.gs[g] + r; j < j1; j += 4) {
+            const double2* rp = reinterpret_cast<const double2*>(recs + static_cast<int64_t>(w.od[j]) * 8);
+            const double2 a01 = rp[0], a23 = rp[1], ux = rp[2];
+            const double R[4] = {a01.x, a01.y, a23.x, a23.y};
+            const double uu = ux.x;
             double um = 1.0;
 #pragma unroll
             for (int mm = 0; mm < 6; ++mm) {
 #pragma unroll
               for (int a = 0; a < 4; ++a) Wv[a * 6 + mm] += R[a] * um;
               um *= uu;
-            }
-            if (two) {
-              um = 1.0;
-#pragma unroll
-              for (int mm = 0; mm < 6; ++mm) {
-#pragma unroll
-                for (int a = 0; a < 4; ++a) Wv[a * 6 + mm] += R2[a] * um;
-                um *= uu2;
-              }
             }
           }
         }
@@ -467,14 +405,6 @@ __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
             const double keep = hi ? Wv[k + 6] : Wv[k];
             Wv[k] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
           }
-        }
-        if constexpr (WM) {
-          if (g < G) {
-            double* Wg = p.Pbuf + (wb + g) * 24 + r * 6;
-#pragma unroll
-            for (int mm = 0; mm < 6; mm += 2) *reinterpret_cast<double2*>(Wg + mm) = make_double2(Wv[mm], Wv[mm + 1]);
-          }
-          continue;
         }
         if (g < G)
 #pragma unroll
@@ -498,11 +428,7 @@ __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
       }
       __syncwarp();
     }
-    if constexpr (WM) {
-      __syncwarp();
-      continue;
-    }
-    // --- T out, D = T<^T T (contract.hpp:9-17) ---
+    // --- D: T out, D = T<^T T (contract.hpp:9-17) ---
     double* ts = w.ts;
     double* Ti = p.T + static_cast<size_t>(i) * 4 * p.Mp;
 #pragma unroll
@@ -590,20 +516,6 @@ __global__ void __launch_bounds__(256, 2) k_tab_dT(TabParams p, double* __restri
         for (int q = 0; q < F; ++q) out[a * p.Mp + f0 + q] = 0.0;
       continue;
     }
-#if TAB_L2_PREFETCH
-    {
-      // the warp's next centre: its dD row (lane 0) and T rows (lane 1)
-      const int in = i + gridDim.x * wpb;
-      if (in < p.i1 && lane < 2 && p.center[in]) {
-        if (lane == 1) {
-          l2_prefetch(p.T + static_cast<size_t>(in) * 4 * p.Mp, static_cast<size_t>(4) * p.Mp * 8);
-        } else {
-          const int s2 = p.slot_of[in];
-          if (s2 >= 0) l2_prefetch(p.dD + static_cast<size_t>(s2) * p.K0p, static_cast<size_t>(p.mlt) * p.M * 8);
-        }
-      }
-    }
-#endif
     const double* Ti = p.T + static_cast<size_t>(i) * 4 * p.Mp;
     double tv[4][F], dT[4][F];
 #pragma unroll
@@ -695,13 +607,12 @@ __global__ void __launch_bounds__(64, 6) k_tab_bwd_P(TabParams p, const double* 
     const int i = fb_list ? fb_list[idx / na] + idx % na : p.i0 + idx; // fb_list holds block starts
     if (i >= p.i1) continue;
     const int64_t off = p.row_off[i];
-    const int nreal = p.n_real[i];
     int G = p.n_grp[i];
     if (p.goff[i] + G > p.pcap) {
       if (lane == 0) raise_err(p.err, DEV_PBUF);
       G = 0;
     }
-    const uint64_t* sk = p.skeys + (off - eb);
+    const int32_t* gbins = p.gbin + (off - eb); // the centre's group bins, ascending
     double* Pout = p.Pbuf + p.goff[i] * 24;
     const double* dTi = dTg + static_cast<size_t>(i) * 4 * p.Mp;
     double dT[4][F];
@@ -710,20 +621,9 @@ __global__ void __launch_bounds__(64, 6) k_tab_bwd_P(TabParams p, const double* 
 #pragma unroll
       for (int q = 0; q < F; ++q) dT[a][q] = dTi[a * p.Mp + f0 + q];
     // --- P[a][m] = sum_p dT[a][p] C[m][p] per group (reduce-scatter over the feature lanes) ---
-    int g = 0;
-    for (int base = 0; base < nreal && g < G; base += 32) {
-      const int k = base + lane;
-      bool head = false;
-      uint64_t v = 0;
-      if (k < nreal) {
-        v = sk[k];
-        head = (k == 0) || ((v >> 32) != (sk[k - 1] >> 32));
-      }
-      unsigned m = __ballot_sync(0xffffffffu, head);
-      while (m) {
-        const int src = __ffs(m) - 1;
-        m &= m - 1;
-        const int bin = static_cast<int>(__shfl_sync(0xffffffffu, v, src) >> 32);
+    for (int g = 0; g < G; ++g) {
+      {
+        const int bin = gbins[g];
         const double* C = p.tab + static_cast<size_t>(bin) * istride + f0;
         double c[6][F];
 #pragma unroll
@@ -756,7 +656,6 @@ __global__ void __launch_bounds__(64, 6) k_tab_bwd_P(TabParams p, const double* 
           Pout[g * 24 + b + 1] = part[1];
           Pout[g * 24 + b + 2] = part[2];
         }
-        ++g;
       }
     }
   }
@@ -814,20 +713,6 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_tab_bwd_P2(TabParams p, const
     }
   for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
     const int i0 = p.i0 + blk * P2_NA;
-#if TAB_L2_PREFETCH
-    {
-      // the CTA's next block: its 32 centres' dT rows (contiguous), in 16 KB pieces
-      const int n0 = i0 + gridDim.x * P2_NA;
-      const int nc = min(P2_NA, p.i1 - n0);
-      if (nc > 0) {
-        const size_t bytes = static_cast<size_t>(nc) * 4 * Mp * sizeof(double);
-        const size_t piece = size_t(16384) * tid;
-        if (piece < bytes)
-          l2_prefetch(dTg + static_cast<size_t>(n0) * 4 * Mp + piece / sizeof(double),
-                      bytes - piece < 16384 ? bytes - piece : 16384);
-      }
-    }
-#endif
     // dT rows of the 32 centres (contiguous in dTg)
     for (int q = tid; q < 4 * P2_NA * units; q += P2_THREADS) {
       const int row = q / units, c2 = q % units;
@@ -1016,400 +901,93 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_tab_bwd_P2(TabParams p, const
   }
 }
 
-// ---------------------------------------------------------------- k_tab_fwd_T2 (CTA, staged union)
-// The forward contraction T[i][a][p] = sum_groups sum_m W[i][g][a][m] C[bin(g)][m][p] of 32
-// consecutive centres per CTA: the union of their intervals is staged once in shared memory
-// (cp.async, double-buffered, 4 intervals per stage, 8 rows each) together with the matching
-// slice of the moments written by k_tab_fwd<WM>; each warp then contracts its two centres from
-// shared memory with lanes owning features. The per-warp k_tab_fwd streams 6 KB of coefficients
-// per (centre, interval) from L2 (the hot table does not fit the L1 left beside its shared
-// memory); here each staged interval serves all 32 centres. Per accumulator the FMA chain is the
-// per-warp kernel's (intervals ascending, m ascending), so T and D are bitwise identical to it.
-// (A first version contracted on DMMA with rows = (centre, a), k = (interval, m): slower, see
-// DESIGN.md §9.) Blocks whose union exceeds T2_UCAP intervals contract per warp from the moments.
-constexpr int T2_NA = 32, T2_CB = 4, T2_UCAP = 128, T2_UW = T2_UCAP / 32, T2_BMW = 256, T2_AP = 36;
-constexpr int T2_THREADS = 512; // 16 warps, one m-tile (2 centres x 4 rows) each
-
-__host__ __device__ inline size_t t2_region_bytes(int Mp) {
-  const int pitch = Mp + 4;
-  const size_t stg = (static_cast<size_t>(2) * 8 * T2_CB * pitch + static_cast<size_t>(2) * 4 * T2_NA * T2_AP) * 8;
-  const size_t ts = static_cast<size_t>(T2_THREADS / 32) * 4 * (pitch - 4) * 8; // per-warp T (wide blocks)
-  return stg > ts ? stg : ts;
-}
-
-__host__ __device__ inline size_t t2_smem_bytes(int Mp) {
-  return t2_region_bytes(Mp) + T2_NA * sizeof(int64_t) +
-         (2 * T2_BMW + T2_UCAP + T2_NA / 2 * T2_UW + 4) * sizeof(int) + T2_NA * T2_UCAP * sizeof(int16_t);
-}
-
-template <int F>
-__global__ void __launch_bounds__(T2_THREADS, 1) k_tab_fwd_T2(TabParams p) {
-  constexpr int Mp = 32 * F, pitch = Mp + 4, units = Mp / 2, NT = Mp / 8, CR = 8 * T2_CB;
-  extern __shared__ __align__(16) unsigned char smem[];
-  double* Cs = reinterpret_cast<double*>(smem);          // [2][CR][pitch] coefficient rows (k x features)
-  double* As = Cs + 2 * CR * pitch;                      // [2][128][AP] moments (rows x k)
-  int64_t* wb_s = reinterpret_cast<int64_t*>(smem + t2_region_bytes(Mp)); // [NA] first group in Pbuf
-  uint32_t* bm = reinterpret_cast<uint32_t*>(wb_s + T2_NA);              // [BMW] union bitmap
-  int* wpre = reinterpret_cast<int*>(bm + T2_BMW);                       // [BMW] popcount prefix
-  int* ubin = wpre + T2_BMW;                                             // [UCAP] union bins
-  uint32_t* mtmask = reinterpret_cast<uint32_t*>(ubin + T2_UCAP);        // [NA/2][UW] per m-tile union
-  int* misc = reinterpret_cast<int*>(mtmask + T2_NA / 2 * T2_UW);        // bmin, bmax, U
-  int16_t* gidx = reinterpret_cast<int16_t*>(misc + 4);                  // [NA][UCAP] group of slot or -1
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;         // warp = m-tile = centres 2w, 2w+1
-  const int gid = lane >> 2, tig = lane & 3;
-  const int nblk = (p.i1 - p.i0 + T2_NA - 1) / T2_NA;
-  const int64_t eb = p.row_off[p.i0];
-  for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
-    const int i0 = p.i0 + blk * T2_NA;
-    const int na = min(T2_NA, p.i1 - i0);
-    if (tid == 0) {
-      misc[0] = 0x7fffffff;
-      misc[1] = -1;
-    }
-    for (int q = tid; q < T2_NA * T2_UCAP / 2; q += T2_THREADS) reinterpret_cast<int32_t*>(gidx)[q] = -1;
-    for (int q = tid; q < T2_NA / 2 * T2_UW; q += T2_THREADS) mtmask[q] = 0u;
-    if (tid < T2_NA) wb_s[tid] = tid < na ? p.wbase[i0 + tid] : -1;
-    __syncthreads();
-    if (tid < na) {
-      const int i = i0 + tid;
-      const int G = p.n_grp[i];
-      if (G > 0) {
-        const int32_t* gb = p.gbin + (p.row_off[i] - eb);
-        atomicMin(misc, gb[0]);
-        atomicMax(misc + 1, gb[G - 1]);
-      }
-    }
-    __syncthreads();
-    const int bmin = misc[0], bmax = misc[1];
-    const int range = bmax < 0 ? 0 : bmax - bmin + 1;
-    const int nw = (range + 31) >> 5;
-    const bool wide = nw > T2_BMW;
-    if (!wide)
-      for (int w = tid; w < nw; w += T2_THREADS) bm[w] = 0u;
-    __syncthreads();
-    if (!wide) {
-      for (int al = warp * 2; al < warp * 2 + 2 && al < na; ++al) {
-        const int i = i0 + al;
-        const int G = p.n_grp[i];
-        const int32_t* gb = p.gbin + (p.row_off[i] - eb);
-        for (int g = lane; g < G; g += 32) {
-          const int b = gb[g] - bmin;
-          atomicOr(bm + (b >> 5), 1u << (b & 31));
-        }
-      }
-    }
-    __syncthreads();
-    if (!wide && warp == 0) {
-      constexpr int PER = T2_BMW / 32;
-      int c[PER], s = 0;
-#pragma unroll
-      for (int k = 0; k < PER; ++k) {
-        const int w = lane * PER + k;
-        c[k] = w < nw ? __popc(bm[w]) : 0;
-        s += c[k];
-      }
-      int tot;
-      int ex = warp_excl_scan(s, lane, &tot);
-#pragma unroll
-      for (int k = 0; k < PER; ++k) {
-        const int w = lane * PER + k;
-        if (w < nw) {
-          wpre[w] = ex;
-          uint32_t bits = bm[w];
-          int at = ex;
-          while (bits) {
-            const int bit = __ffs(bits) - 1;
-            bits &= bits - 1;
-            if (at < T2_UCAP) ubin[at] = bmin + 32 * w + bit;
-            ++at;
-          }
-        }
-        ex += c[k];
-      }
-      if (lane == 0) misc[2] = tot;
-    }
-    __syncthreads();
-    const int U = range == 0 ? 0 : misc[2];
-    if (wide || U > T2_UCAP) {
-      // per-warp contraction from the moments (groups ascending, then a, m as k_tab_fwd); lanes
-      // own features f0 .. f0 + F - 1; T[a][0..Mp) of the centre staged per warp for D
-      const int f0 = F * lane;
-      double* ts = Cs + warp * 4 * Mp;
-      for (int al = warp * 2; al < warp * 2 + 2 && al < na; ++al) {
-        double tacc[4][F];
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int q = 0; q < F; ++q) tacc[a][q] = 0.0;
-        const int i = i0 + al;
-        const int64_t wb = wb_s[al];
-        if (wb >= 0) {
-          const int G = p.n_grp[i];
-          const int32_t* gb = p.gbin + (p.row_off[i] - eb);
-          for (int g = 0; g < G; ++g) {
-            const double* C = p.tab + static_cast<size_t>(gb[g]) * 6 * Mp + f0;
-            const double* Wg = p.Pbuf + (wb + g) * 24;
-            double c[6][F];
-#pragma unroll
-            for (int mm = 0; mm < 6; ++mm)
-#pragma unroll
-              for (int q = 0; q < F; ++q) c[mm][q] = __ldg(C + mm * Mp + q);
-#pragma unroll
-            for (int a = 0; a < 4; ++a)
-#pragma unroll
-              for (int mm = 0; mm < 6; ++mm) {
-                const double wa = Wg[a * 6 + mm];
-#pragma unroll
-                for (int q = 0; q < F; ++q) tacc[a][q] += wa * c[mm][q];
-              }
-          }
-        }
-        double* Ti = p.T + static_cast<size_t>(i) * 4 * Mp;
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int q = 0; q < F; ++q) {
-            Ti[a * Mp + f0 + q] = tacc[a][q];
-            ts[a * Mp + f0 + q] = tacc[a][q];
-          }
-        __syncwarp();
-        const int slot = p.slot_of[i];
-        if (slot >= 0 && f0 < p.M) {
-          double* Drow = p.D + static_cast<size_t>(slot) * p.K0p;
-          for (int qq = 0; qq < p.mlt; ++qq) {
-            const double t0 = ts[qq], t1 = ts[Mp + qq], t2 = ts[2 * Mp + qq], t3 = ts[3 * Mp + qq];
-#pragma unroll
-            for (int q = 0; q < F; ++q) {
-              double v = t0 * tacc[0][q];
-              v += t1 * tacc[1][q];
-              v += t2 * tacc[2][q];
-              v += t3 * tacc[3][q];
-              Drow[qq * p.M + f0 + q] = v;
-            }
-          }
-        }
-        __syncwarp();
-      }
-      __syncthreads();
-      continue;
-    }
-    // slot -> group of each centre, and the union each m-tile (2 centres) really needs
-    for (int al = warp * 2; al < warp * 2 + 2 && al < na; ++al) {
-      const int i = i0 + al;
-      const int G = p.n_grp[i];
-      const int32_t* gb = p.gbin + (p.row_off[i] - eb);
-      for (int g = lane; g < G; g += 32) {
-        const int b = gb[g] - bmin;
-        const int u = wpre[b >> 5] + __popc(bm[b >> 5] & ((1u << (b & 31)) - 1u));
-        gidx[al * T2_UCAP + u] = static_cast<int16_t>(g);
-        atomicOr(mtmask + (al >> 1) * T2_UW + (u >> 5), 1u << (u & 31));
-      }
-    }
-    __syncthreads();
-    const int nch = (U + T2_CB - 1) / T2_CB;
-    auto stage = [&](int ch, int buf) {
-      double* cdst = Cs + buf * CR * pitch;
-      for (int q = tid; q < CR * units; q += T2_THREADS) {
-        const int row = q / units, c2 = q % units;
-        const int u = ch * T2_CB + (row >> 3), m = row & 7;
-        double* dst = cdst + row * pitch + 2 * c2;
-        if (m < 6 && u < U)
-          tc::cp_async16(dst, p.tab + static_cast<size_t>(ubin[u]) * 6 * Mp + m * Mp + 2 * c2);
-        else
-          dst[0] = dst[1] = 0.0;
-      }
-      double* adst = As + buf * 4 * T2_NA * T2_AP;
-      for (int q = tid; q < 4 * T2_NA * T2_CB * 4; q += T2_THREADS) {
-        const int row = q >> 4, ul = (q >> 2) & 3, piece = q & 3;
-        const int al = row >> 2, a = row & 3;
-        const int u = ch * T2_CB + ul;
-        const int g = u < U ? gidx[al * T2_UCAP + u] : -1;
-        const int64_t wb = wb_s[al];
-        double* dst = adst + row * T2_AP + ul * 8 + piece * 2;
-        if (piece < 3 && g >= 0 && wb >= 0)
-          tc::cp_async16(dst, p.Pbuf + (wb + g) * 24 + a * 6 + piece * 2);
-        else
-          dst[0] = dst[1] = 0.0;
-      }
-      tc::cp_commit();
-    };
-    // per-warp contraction of its two centres from the staged slice, lanes own features
-    // f0 .. f0 + F - 1: for each of the centre's intervals (ascending), for m, for a,
-    // T[a][f] += W[a][m] C[m][f] -- per accumulator the same FMA chain as k_tab_fwd, so T and D
-    // are bitwise those of the per-warp kernel
-    const int f0 = F * lane;
-    double tacc[2][4][F];
-#pragma unroll
-    for (int c = 0; c < 2; ++c)
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int q = 0; q < F; ++q) tacc[c][a][q] = 0.0;
-    if (nch > 0) stage(0, 0);
-    for (int ch = 0; ch < nch; ++ch) {
-      if (ch + 1 < nch) {
-        stage(ch + 1, (ch + 1) & 1);
-        tc::cp_wait<1>();
-      } else {
-        tc::cp_wait<0>();
-      }
-      __syncthreads();
-      const double* cs = Cs + (ch & 1) * CR * pitch + f0;
-      const double* as = As + (ch & 1) * 4 * T2_NA * T2_AP;
-      const bool ok0 = warp * 2 < na && wb_s[warp * 2] >= 0;
-      const bool ok1 = warp * 2 + 1 < na && wb_s[warp * 2 + 1] >= 0;
-      const int16_t* g0 = gidx + (warp * 2) * T2_UCAP + ch * T2_CB;
-      const double* w0 = as + (warp * 2) * 4 * T2_AP;
-      const double* w1 = w0 + 4 * T2_AP;
-      for (int ul = 0; ul < T2_CB && ch * T2_CB + ul < U; ++ul) {
-        // both centres of the warp share the staged coefficient rows of an interval they both have
-        const bool h0 = ok0 && g0[ul] >= 0, h1 = ok1 && g0[T2_UCAP + ul] >= 0;
-        if (!(h0 || h1)) continue;
-        const double* cr = cs + ul * 8 * pitch;
-        const double* wr0 = w0 + ul * 8;
-        const double* wr1 = w1 + ul * 8;
-#pragma unroll
-        for (int m = 0; m < 6; ++m) {
-          double cm[F];
-          if constexpr (F % 2 == 0) {
-#pragma unroll
-            for (int q = 0; q < F; q += 2) {
-              const double2 v = *reinterpret_cast<const double2*>(cr + m * pitch + q);
-              cm[q] = v.x;
-              cm[q + 1] = v.y;
-            }
-          } else {
-#pragma unroll
-            for (int q = 0; q < F; ++q) cm[q] = cr[m * pitch + q];
-          }
-          if (h0) {
-#pragma unroll
-            for (int a = 0; a < 4; ++a) {
-              const double wa = wr0[a * T2_AP + m];
-#pragma unroll
-              for (int q = 0; q < F; ++q) tacc[0][a][q] += wa * cm[q];
-            }
-          }
-          if (h1) {
-#pragma unroll
-            for (int a = 0; a < 4; ++a) {
-              const double wa = wr1[a * T2_AP + m];
-#pragma unroll
-              for (int q = 0; q < F; ++q) tacc[1][a][q] += wa * cm[q];
-            }
-          }
-        }
-      }
-      __syncthreads();
-    }
-    // T out, D = T<^T T (contract.hpp:9-17) as in k_tab_fwd (T of the centre staged per warp)
-    double* ts = Cs + warp * 4 * Mp;
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const int al = warp * 2 + c;
-      if (al >= na) break;
-      const int i = i0 + al;
-      double* Ti = p.T + static_cast<size_t>(i) * 4 * Mp;
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int q = 0; q < F; ++q) {
-          Ti[a * Mp + f0 + q] = tacc[c][a][q];
-          ts[a * Mp + f0 + q] = tacc[c][a][q];
-        }
-      __syncwarp();
-      const int slot = p.slot_of[i];
-      if (slot >= 0 && f0 < p.M) {
-        double* Drow = p.D + static_cast<size_t>(slot) * p.K0p;
-        for (int qq = 0; qq < p.mlt; ++qq) {
-          const double t0 = ts[qq], t1 = ts[Mp + qq], t2 = ts[2 * Mp + qq], t3 = ts[3 * Mp + qq];
-          double dv[F];
-#pragma unroll
-          for (int q = 0; q < F; ++q) {
-            double v = t0 * tacc[c][0][q];
-            v += t1 * tacc[c][1][q];
-            v += t2 * tacc[c][2][q];
-            v += t3 * tacc[c][3][q];
-            dv[q] = v;
-          }
-          double* dst = Drow + qq * p.M + f0;
-          if constexpr (F % 2 == 0) {
-            if ((p.M & 1) == 0) {
-#pragma unroll
-              for (int q = 0; q < F; q += 2) *reinterpret_cast<double2*>(dst + q) = make_double2(dv[q], dv[q + 1]);
-              continue;
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < F; ++q) dst[q] = dv[q];
-        }
-      }
-      __syncwarp();
-    }
-    __syncthreads();
-  }
-}
-
-// ---------------------------------------------------------------- k_tab_bwd_g (thread per entry)
+// ---------------------------------------------------------------- k_tab_bwd_g (warp per centre)
+// Gradient pass of fused_atom_energy (fused.cpp:203-242) per real neighbour k (lane k mod 32),
+// from its record (R, u, d) and its group's projections P:
+//   drow[a] = sum_m u^m P[a][m],  ds = sum_a R[a] sum_m m u^(m-1) P[a][m],  drow[0] += ds,
+//   g = sum_a drow[a] dR[a]/dd   (= dE_i/dd_ij, env_mat.cpp:55-71 derivatives)
+// written compactly at g[realoff[i] + k], plus the centre's virial sum_k d_k (x) g_k (the
+// reference scatter, exact.cpp:34) reduced in a fixed order: lane k mod 32, then a warp tree.
 __global__ void __launch_bounds__(256) k_tab_bwd_g(TabParams p) {
-  const int64_t eo = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
   const int64_t eb = p.row_off[p.i0];
-  const int64_t e = eb + eo;
-  if (e >= p.E || e >= p.row_off[p.i1]) return;
-  // bin, owner, group and key loaded together (independent; egrp is unset for non-real entries
-  // but inside the chunk buffer), so a real entry waits for one latency, not three
-  const int bin = p.ebin[e];
-  const int i = p.eown[e];
-  const int grp = p.egrp[e - eb];
-  const uint64_t key = p.keys[e];
-  double* ge = p.g + 3 * e;
-  if (bin < 0) return; // never read: k_forces gathers only real entries (own and reverse)
-  const int64_t gi = p.goff[i] + grp;
-  Env ev;
-  env_of(p, ld_pos(p.pos, i), key, ev);
-  const int th = bin % p.tn;
-  if (gi >= p.pcap) {
-    raise_err(p.err, DEV_PBUF);
-    ge[0] = ge[1] = ge[2] = 0.0;
-    return;
-  }
-  // the group's 24 projections as 12 16-byte loads (a Pbuf row is 192 B, 16-byte aligned)
-  const double2* P2 = reinterpret_cast<const double2*>(p.Pbuf + gi * 24);
-  double P[24];
+  for (int i = p.i0 + blockIdx.x * wpb + (threadIdx.x >> 5); i < p.i1; i += gridDim.x * wpb) {
+    if (!p.center[i]) continue;
+    const int nreal = p.n_real[i];
+    const int64_t loff = p.row_off[i] - eb;
+    const int64_t ro = p.realoff[i];
+    const int64_t gb0 = p.goff[i];
+    double vir[9];
 #pragma unroll
-  for (int q = 0; q < 12; ++q) {
-    const double2 v = __ldg(P2 + q);
-    P[2 * q] = v.x;
-    P[2 * q + 1] = v.y;
-  }
-  const double R[4] = {ev.s, ev.s * ev.u[0], ev.s * ev.u[1], ev.s * ev.u[2]};
-  const double uu = ev.s - node_x(p.x0, p.h, th);
-  double drow[4], dsum = 0.0;
+    for (int k = 0; k < 9; ++k) vir[k] = 0.0;
+    const bool fits = ro + nreal <= p.gcap && gb0 + p.n_grp[i] <= p.pcap;
+    if (!fits && lane == 0) raise_err(p.err, ro + nreal > p.gcap ? DEV_GCAP : DEV_PBUF);
+    for (int k = lane; fits && k < nreal; k += 32) {
+      const double2* rp = reinterpret_cast<const double2*>(p.rec + (loff + k) * 8);
+      const int grp = p.egrp[loff + k];
+      const double2 a01 = rp[0], a23 = rp[1], ud = rp[2], dd2 = rp[3];
+      const double R[4] = {a01.x, a01.y, a23.x, a23.y};
+      const double uu = ud.x;
+      const double d[3] = {ud.y, dd2.x, dd2.y};
+      // the group's 24 projections as 12 16-byte loads (a Pbuf row is 192 B, 16-byte aligned)
+      const double2* P2 = reinterpret_cast<const double2*>(p.Pbuf + (gb0 + grp) * 24);
+      double P[24];
 #pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    const double* Pa = P + a * 6;
-    drow[a] = ((((Pa[5] * uu + Pa[4]) * uu + Pa[3]) * uu + Pa[2]) * uu + Pa[1]) * uu + Pa[0];
-    const double h1 = (((5.0 * Pa[5] * uu + 4.0 * Pa[4]) * uu + 3.0 * Pa[3]) * uu + 2.0 * Pa[2]) * uu + Pa[1];
-    dsum += R[a] * h1;
-  }
-  drow[0] += dsum;
-  double dd[12];
+      for (int q = 0; q < 12; ++q) {
+        const double2 v = __ldg(P2 + q);
+        P[2 * q] = v.x;
+        P[2 * q + 1] = v.y;
+      }
+      // env-mat derivative terms from d, exactly as the forward pass evaluated them
+      const double r = sqrt(norm2_exact(d));
+      const double wv = switch_fn(r, p.rs, p.rc);
+      const double ir = 1.0 / r;
+      const double s = wv * ir;
+      const double sd = switch_deriv(r, p.rs, p.rc) * ir - wv * ir * ir;
+      const double u[3] = {d[0] * ir, d[1] * ir, d[2] * ir};
+      double drow[4], dsum = 0.0;
 #pragma unroll
-  for (int x = 0; x < 3; ++x) dd[x] = ev.sd * ev.u[x];
+      for (int a = 0; a < 4; ++a) {
+        const double* Pa = P + a * 6;
+        drow[a] = ((((Pa[5] * uu + Pa[4]) * uu + Pa[3]) * uu + Pa[2]) * uu + Pa[1]) * uu + Pa[0];
+        const double h1 = (((5.0 * Pa[5] * uu + 4.0 * Pa[4]) * uu + 3.0 * Pa[3]) * uu + 2.0 * Pa[2]) * uu + Pa[1];
+        dsum += R[a] * h1;
+      }
+      drow[0] += dsum;
+      double dR[12];
 #pragma unroll
-  for (int y = 0; y < 3; ++y)
+      for (int x = 0; x < 3; ++x) dR[x] = sd * u[x];
 #pragma unroll
-    for (int x = 0; x < 3; ++x) {
-      double v = ev.sd * ev.u[x] * ev.u[y] - ev.s * ev.ir * ev.u[x] * ev.u[y];
-      if (x == y) v += ev.s * ev.ir;
-      dd[3 * (1 + y) + x] = v;
+      for (int y = 0; y < 3; ++y)
+#pragma unroll
+        for (int x = 0; x < 3; ++x) {
+          double v = sd * u[x] * u[y] - s * ir * u[x] * u[y];
+          if (x == y) v += s * ir;
+          dR[3 * (1 + y) + x] = v;
+        }
+      double gv[3];
+#pragma unroll
+      for (int x = 0; x < 3; ++x) {
+        double acc = 0.0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) acc += drow[a] * dR[3 * a + x];
+        gv[x] = acc;
+      }
+      double* ge = p.g + 3 * (ro + k);
+      ge[0] = gv[0];
+      ge[1] = gv[1];
+      ge[2] = gv[2];
+#pragma unroll
+      for (int x = 0; x < 3; ++x)
+#pragma unroll
+        for (int y = 0; y < 3; ++y) vir[3 * x + y] += d[x] * gv[y];
     }
 #pragma unroll
-  for (int x = 0; x < 3; ++x) {
-    double acc = 0.0;
+    for (int k = 0; k < 9; ++k) vir[k] = warp_sum(vir[k]);
+    if (lane == 0)
 #pragma unroll
-    for (int a = 0; a < 4; ++a) acc += drow[a] * dd[3 * a + x];
-    ge[x] = acc;
+      for (int k = 0; k < 9; ++k) p.vpart[9 * static_cast<int64_t>(i) + k] = vir[k];
   }
 }
 
@@ -1477,17 +1055,12 @@ __global__ void k_group_total(const int32_t* __restrict__ n_grp, const int64_t* 
   if (threadIdx.x == 0 && blockIdx.x == 0) *out = i1 > i0 ? goff[i1 - 1] + n_grp[i1 - 1] : 0;
 }
 
-// env-mat of every entry of the rows [i0, i1): grid bound = the chunk's entry capacity
-void env_range(Engine& E, const TabParams& p, cudaStream_t st) {
-  const int64_t ne = std::min<int64_t>(p.es, p.E);
-  if (ne > 0) {
-    k_env_fwd<<<ceil_div(ne, 256), 256, 0, st>>>(p);
-    ++E.launches;
-  }
+// Pair-gradient base of the chunk after this one (evaluation order): its base + its real pairs.
+__global__ void k_real_end(const int32_t* __restrict__ n_real, const int64_t* __restrict__ realoff, int i0, int i1,
+                           const int64_t* __restrict__ base, int64_t* __restrict__ next) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *next = i1 > i0 ? realoff[i1 - 1] + n_real[i1 - 1] : *base;
 }
 
-// env + k_tab_fwd over centres [i0, i1) of chunk k, then the group offsets of the chunk
-// (goff[i0..i1) start at 0; the chunk's buffer set owns Pbuf[set * pbuf_cap ...]).
 // FP32 copy of the coefficient table for the mixed-mode forward contraction
 void Engine::ensure_tab32() {
   if (precision != 1 || tab32_ver == tab_ver) return;
@@ -1498,88 +1071,13 @@ void Engine::ensure_tab32() {
   tab32_ver = tab_ver;
 }
 
-// Opt-in (DPB_T2=1), results bitwise equal to the default path: measured at C2 the moments kernel
-// + k_tab_fwd_T2 take 0.19 + 0.40 ms per 16k-centre chunk against 0.42 ms for the per-warp
-// k_tab_fwd (step 5.33 vs 5.01 ms); DESIGN.md §9.
-bool Engine::t2_ok() const {
-  static const bool on = std::getenv("DPB_T2") != nullptr && std::getenv("DPB_T2")[0] == '1';
-  return on && precision == 0 && Mp <= 128;
-}
-
-template <int F>
-void launch_fwd_wm(const TabParams& p, cudaStream_t st, int sms) {
-  const size_t bytes = 2 * fwd_smem_bytes(p.scap, p.Mp);
-  if (bytes > 227 * 1024) throw NumErr("neighbour rows too long for the tabulate kernel");
-  DPB_CUDA(cudaFuncSetAttribute(k_tab_fwd<F, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(bytes)));
-  const int blocks = std::max(1, std::min(ceil_div(p.i1 - p.i0, 2), sms * 32));
-  k_tab_fwd<F, false, true><<<blocks, 64, bytes, st>>>(p);
-  DPB_CUDA(cudaGetLastError());
-}
-
-template <int F>
-void launch_fwd_t2(const TabParams& p, cudaStream_t st, int sms) {
-  const size_t bytes = t2_smem_bytes(32 * F);
-  DPB_CUDA(cudaFuncSetAttribute(k_tab_fwd_T2<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
-  const int nblk = ceil_div(p.i1 - p.i0, T2_NA);
-  k_tab_fwd_T2<F><<<std::max(1, std::min(nblk, sms)), T2_THREADS, bytes, st>>>(p);
-  DPB_CUDA(cudaGetLastError());
-}
-
-void Engine::tab_fwd_range(int k, int64_t i0, int64_t i1, cudaStream_t st) {
+// k_tab_fwd over centres [i0, i1) of chunk k (q-th in evaluation order), then the chunk's group
+// offsets (goff[i0..i1) start at 0; the chunk's buffer set owns Pbuf[set * pbuf_cap ...]) and its
+// compact pair-gradient offsets realoff[i0..i1) = rbase[q] + exclusive scan of n_real.
+void Engine::tab_fwd_range(int k, int q, int64_t i0, int64_t i1, cudaStream_t st) {
   ensure_tab32();
   TabParams p = chunk_params(*this, i0, i1);
-  env_range(*this, p, st);
   const int sms = sm_count(device);
-  // group offsets of the chunk -> goff, its total -> h_gtotal[k] (pinned, read at Pbuf sizing)
-  auto scan_groups = [&] {
-    DevBuf<unsigned char>& tmp = cur_set == 0 ? scan_tmp : scan_tmp2;
-    const int cnt = static_cast<int>(i1 - i0);
-    size_t tb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb, n_grp.p + i0, goff.p + i0, cnt, st);
-    tmp.ensure(tb + 1);
-    cub::DeviceScan::ExclusiveSum(tmp.p, tb, n_grp.p + i0, goff.p + i0, cnt, st);
-    gtot.ensure(MAX_CHUNKS);
-    k_group_total<<<1, 32, 0, st>>>(n_grp.p, goff.p, static_cast<int>(i0), static_cast<int>(i1), gtot.p + k);
-    if (!h_gtotal) {
-      DPB_CUDA(cudaMallocHost(&h_gtotal, MAX_CHUNKS * sizeof(int64_t)));
-      std::memset(h_gtotal, 0, MAX_CHUNKS * sizeof(int64_t));
-    }
-    DPB_CUDA(cudaMemcpyAsync(h_gtotal + k, gtot.p + k, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    launches += 2;
-  };
-  if (t2_ok()) {
-    // moments (k_tab_fwd<WM>) into this chunk's Pbuf region, then the tensor-pipe contraction
-    auto wm = [&](const TabParams& q) {
-      switch (Mp / 32) {
-#define DPB_WM(F) case F: launch_fwd_wm<F>(q, st, sms); break;
-        DPB_WM(1) DPB_WM(2) DPB_WM(3) DPB_WM(4)
-#undef DPB_WM
-      }
-      ++launches;
-    };
-    if (pbuf_cap == 0) {
-      // first evaluation of this system/plan: exact group total of this chunk (one sync)
-      p.count_only = 1;
-      wm(p);
-      scan_groups();
-      DPB_CUDA(cudaStreamSynchronize(st));
-      grow_pbuf();
-      p = chunk_params(*this, i0, i1);
-    }
-    wcnt.ensure(2);
-    p.wcnt = wcnt.p + cur_set;
-    DPB_CUDA(cudaMemsetAsync(p.wcnt, 0, sizeof(unsigned long long), st));
-    wm(p);
-    switch (Mp / 32) {
-#define DPB_T2(F) case F: launch_fwd_t2<F>(p, st, sms); break;
-      DPB_T2(1) DPB_T2(2) DPB_T2(3) DPB_T2(4)
-#undef DPB_T2
-    }
-    ++launches;
-    scan_groups();
-    return;
-  }
   switch (Mp / 32) {
     case 1: launch_fwd_warp<1>(p, st, sms); break;
     case 2: launch_fwd_warp<2>(p, st, sms); break;
@@ -1592,11 +1090,33 @@ void Engine::tab_fwd_range(int k, int64_t i0, int64_t i1, cudaStream_t st) {
     default: throw InputErr("feature width 4*d1 must be at most 256");
   }
   ++launches;
-  scan_groups();
+  DevBuf<unsigned char>& tmp = cur_set == 0 ? scan_tmp : scan_tmp2;
+  const int cnt = static_cast<int>(i1 - i0);
+  size_t tb = 0, tb2 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, n_grp.p + i0, goff.p + i0, cnt, st);
+  cub::DeviceScan::ExclusiveScan(nullptr, tb2, n_real.p + i0, realoff.p + i0, cuda::std::plus<int64_t>(),
+                                 cub::FutureValue<int64_t>(rbase.p + q), cnt, st);
+  tmp.ensure(std::max(tb, tb2) + 1);
+  // group offsets of the chunk -> goff, its total -> h_gtotal[k] (pinned, read at Pbuf sizing)
+  cub::DeviceScan::ExclusiveSum(tmp.p, tb, n_grp.p + i0, goff.p + i0, cnt, st);
+  gtot.ensure(MAX_CHUNKS);
+  k_group_total<<<1, 32, 0, st>>>(n_grp.p, goff.p, static_cast<int>(i0), static_cast<int>(i1), gtot.p + k);
+  if (!h_gtotal) {
+    DPB_CUDA(cudaMallocHost(&h_gtotal, MAX_CHUNKS * sizeof(int64_t)));
+    std::memset(h_gtotal, 0, MAX_CHUNKS * sizeof(int64_t));
+  }
+  DPB_CUDA(cudaMemcpyAsync(h_gtotal + k, gtot.p + k, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  // compact pair-gradient slots: realoff = base of this chunk + exclusive scan of n_real
+  cub::DeviceScan::ExclusiveScan(tmp.p, tb2, n_real.p + i0, realoff.p + i0, cuda::std::plus<int64_t>(),
+                                 cub::FutureValue<int64_t>(rbase.p + q), cnt, st);
+  k_real_end<<<1, 32, 0, st>>>(n_real.p, realoff.p, static_cast<int>(i0), static_cast<int>(i1), rbase.p + q,
+                               rbase.p + q + 1);
+  launches += 4;
 }
 
 void Engine::launch_tab_fwd() {
-  tab_fwd_range(0, 0, n, stream);
+  DPB_CUDA(cudaMemsetAsync(rbase.p, 0, sizeof(int64_t), stream));
+  tab_fwd_range(0, 0, 0, n, stream);
   size_pbuf_if_needed();
 }
 
@@ -1607,16 +1127,6 @@ void Engine::size_pbuf_if_needed() {
   if (pbuf_cap != 0) return;
   DPB_CUDA(cudaDeviceSynchronize());
   grow_pbuf();
-}
-
-void Engine::launch_env_exact() {
-  TabParams p = make_params(*this);
-  p.tn = 0;
-  p.counters = exact_ctr.p;
-  if (p.E > 0) {
-    k_env_fwd<<<ceil_div(p.E, 256), 256, 0, stream>>>(p);
-    ++launches;
-  }
 }
 
 void Engine::grow_pbuf() {
@@ -1676,9 +1186,8 @@ void Engine::tab_bwd_range(int, int64_t i0, int64_t i1, cudaStream_t st) {
     default: throw InputErr("feature width 4*d1 must be at most 256");
   }
   ++launches;
-  const int64_t ne = std::min<int64_t>(p.es, p.E);
-  if (ne > 0) {
-    k_tab_bwd_g<<<ceil_div(ne, 256), 256, 0, st>>>(p);
+  if (i1 > i0) {
+    k_tab_bwd_g<<<std::max(1, std::min(ceil_div(i1 - i0, 8), sms * 16)), 256, 0, st>>>(p);
     ++launches;
   }
 }
