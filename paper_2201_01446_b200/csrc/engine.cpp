@@ -464,7 +464,22 @@ void Engine::ensure_step_buffers() {
 // (row lengths are checked against row_cap on the device at every rebuild).
 void Engine::ensure_entry_step_buffers() {
   if (e_cap == 0) return;
-  ck_cap_e = n_chunks == 1 ? e_cap : std::min<int64_t>(e_cap, ck_cap_a * std::max(row_cap, 1));
+  if (n_chunks == 1) {
+    ck_cap_e = e_cap;
+  } else if (list_valid) {
+    // exact entry count of every chunk from the list's offsets at the chunk boundaries (the list
+    // and the plan only change together with this call): the per-real records of a 13.5 M-atom
+    // system then take 64 B x the chunk's entries, not x its atoms x the row capacity
+    std::vector<int64_t> b(n_chunks + 1);
+    for (int k = 0; k <= n_chunks; ++k)
+      DPB_CUDA(cudaMemcpyAsync(&b[k], row_off.p + ck_a[k], sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+    DPB_CUDA(cudaStreamSynchronize(stream));
+    int64_t mx = 0;
+    for (int k = 0; k < n_chunks; ++k) mx = std::max(mx, b[k + 1] - b[k]);
+    ck_cap_e = std::min<int64_t>(e_cap, mx + 1024);
+  } else {
+    ck_cap_e = std::min<int64_t>(e_cap, ck_cap_a * std::max(row_cap, 1));
+  }
   const size_t se = static_cast<size_t>(ck_sets) * ck_cap_e;
   egrp.ensure(se + 1);
   gbin.ensure(se + 1);

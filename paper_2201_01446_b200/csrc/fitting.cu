@@ -215,20 +215,13 @@ __global__ void k_scatter_energy(int64_t slots, const int32_t* __restrict__ atom
 template <int EPI, int BN, int STAGES>
 void launch_gemm(const GemmArgs& a, int rows, int N, cudaStream_t st) {
   const size_t bytes = static_cast<size_t>(STAGES) * (BM + BN) * PITCH * sizeof(double);
-  static const bool four = BN == 80 && STAGES == 2 && std::getenv("DPB_GEMM_NO4") == nullptr;
+  constexpr bool four = BN == 80 && STAGES == 2;
   auto kern = four ? k_gemm4<EPI, BN, STAGES> : k_gemm<EPI, BN, STAGES>;
   smem_optin(kern, bytes);
   GemmArgs g = a;
   g.ntn = N / BN;
   g.ntm = rows / BM;
-  int tiles = g.ntn * g.ntm, grid = tiles;
-  static const int cap = std::getenv("DPB_GEMM_CTAS") ? std::atoi(std::getenv("DPB_GEMM_CTAS")) : 0;
-  if (cap > 0) {
-    static int sms = 0;
-    if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    grid = std::min(tiles, cap * (sms > 0 ? sms : 148));
-  }
-  kern<<<grid, 128, bytes, st>>>(g);
+  kern<<<g.ntn * g.ntm, 128, bytes, st>>>(g);
   DPB_CUDA(cudaGetLastError());
 }
 
@@ -236,8 +229,7 @@ void launch_gemm(const GemmArgs& a, int rows, int N, cudaStream_t st) {
 // Short K (hidden layers): 2 stages -> 4 CTAs/SM to hide the epilogue's global latency.
 void run_gemm(int epi, const GemmArgs& a, int rows, int N, cudaStream_t st) {
   const bool b80 = N % 80 == 0;
-  static const int kshort = std::getenv("DPB_GEMM_KSHORT") ? std::atoi(std::getenv("DPB_GEMM_KSHORT")) : 256;
-  const bool s2 = a.K <= kshort;
+  const bool s2 = a.K <= 256;
   if (epi == EPI_FWD) {
     if (b80) s2 ? launch_gemm<EPI_FWD, 80, 2>(a, rows, N, st) : launch_gemm<EPI_FWD, 80, 3>(a, rows, N, st);
     else s2 ? launch_gemm<EPI_FWD, 64, 2>(a, rows, N, st) : launch_gemm<EPI_FWD, 64, 3>(a, rows, N, st);
