@@ -373,7 +373,7 @@ void Engine::set_gcap(int64_t want) {
   if (want > g_cap || want < g_cap / 2) {
     g.release();
     g.ensure(3 * want + 3);
-    g_cap = want;
+    g_cap = static_cast<int64_t>((g.n - 3) / 3); // the allocation's growth slack included
   }
 }
 

@@ -1131,9 +1131,16 @@ void Engine::size_pbuf_if_needed() {
 
 void Engine::grow_pbuf() {
   if (!h_gtotal) return;
-  // one region per buffer set, each sized for the largest chunk seen (+50 %)
-  int64_t tot = 0;
-  for (int c = 0; c < n_chunks; ++c) tot = std::max(tot, h_gtotal[c]);
+  // one region per buffer set, sized for the largest chunk: the highest groups-per-centre rate
+  // seen in any evaluated chunk x the largest chunk's centres, +50 %
+  double rate = 0.0;
+  int64_t cmax = 0;
+  for (int c = 0; c < n_chunks; ++c) {
+    const int64_t cc = ck_s[c + 1] - ck_s[c];
+    cmax = std::max(cmax, cc);
+    if (cc > 0 && h_gtotal[c] > 0) rate = std::max(rate, static_cast<double>(h_gtotal[c]) / static_cast<double>(cc));
+  }
+  const int64_t tot = static_cast<int64_t>(std::ceil(rate * static_cast<double>(cmax)));
   const int64_t want = tot + tot / 2 + 1024;
   if (want > pbuf_cap) {
     Pbuf.ensure(static_cast<size_t>(want) * 24 * ck_sets);
