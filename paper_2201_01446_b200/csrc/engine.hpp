@@ -122,7 +122,6 @@ struct Engine {
   DevBuf<double> dTbuf;  // [n][4][Mp] adjoint of T (tabulate backward)
   DevBuf<int> fb_list;   // atom blocks left to the per-warp projection kernel (+ count)
   DevBuf<float> tab32; // mixed mode: FP32 copy of tab for the forward contraction
-  bool mixed_tab32 = std::getenv("DPB_MIXED_TAB64") == nullptr; // mixed: FP32 contraction (else FP64)
   uint64_t tab_ver = 0, tab32_ver = ~0ull; // tab32 is refreshed when tab changes
   void ensure_tab32();
   // fitting weights per type and layer: wt = W^T [outp][inp], w = W [inp][outp]
@@ -336,6 +335,7 @@ struct Engine {
   std::vector<DevBuf<float>> tc_wf, tc_wb, tc_bias, tc_wout, tc_t;
   DevBuf<double> tc_tanh;
   DevBuf<float> tc_d2, tc_y2a, tc_y2b, tc_dz2a, tc_dz2b, tc_dya, tc_dyb;
+
   void launch_tab_bwd();
   void launch_forces();
   // MD

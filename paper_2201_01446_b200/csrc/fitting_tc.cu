@@ -1,15 +1,22 @@
 // Mixed-precision fitting net on the 5th-generation tensor cores (tcgen05, kind::tf32).
 //
-// Same algebra as fitting.cu (model.cpp:151-203), but each GEMM runs on tcgen05 with FP32
-// accumulation in TMEM and FP32-level accuracy from the 3xTF32 split: every FP32 operand x is
-// written as x_hi = tf32(x), x_lo = tf32(x - x_hi) and A.B ~= A_hi.B_hi + A_hi.B_lo + A_lo.B_hi,
-// realised as ONE GEMM over a K-concatenated operand pair [A_hi|A_hi|A_lo] . [B_hi|B_lo|B_hi]^T.
-// The activation is the reference's quadratic tanh table (tanh_table.cpp:5-21, mixed mode only).
+// Same algebra as fitting.cu (model.cpp:151-203), but each GEMM runs on tcgen05 with FP32-level
+// operands from the 3xTF32 split: every FP32 operand x is written as x_hi = tf32(x),
+// x_lo = tf32(x - x_hi) and A.B ~= A_hi.B_hi + A_hi.B_lo + A_lo.B_hi, realised as ONE K-concatenated
+// accumulation over [A_hi|A_hi|A_lo] . [B_hi|B_lo|B_hi]^T. The activation is the reference's
+// quadratic tanh table (tanh_table.cpp:5-21, mixed mode only).
 //
-// Kernel: CTA 128 x BN tile (UMMA M=128, N=BN <= 256), warp-specialized: warp 0 issues TMA tile
-// loads (128-byte K atoms, SWIZZLE_128B canonical K-major layout), warp 1 issues tcgen05.mma from
-// one thread, warps 2-5 drain the TMEM accumulator (tcgen05.ld 32x32b) and run the fused epilogue.
-// 4-stage smem ring with full/empty mbarriers; tcgen05.commit releases stages.
+// Kernels:
+//   k_tc_fwd64  forward layers: 128 x 80 tiles; short TMEM chains (2 K blocks of each segment)
+//               drained into FP64 registers by 8 epilogue warps while the next chain runs on the
+//               other TMEM buffer -- the tensor core's FP32 accumulation over the whole 6144-term
+//               first layer biased small total energies by 1e-4 (water preset), this keeps every
+//               preset within 1e-5 (tests/test_gpu_mixed.py);
+//   k_tc_gemm   backward layers: CTA 128 x BN (UMMA M=128, N=BN <= 256), warp-specialized: warp 0
+//               issues TMA tile loads (128-byte K atoms, SWIZZLE_128B canonical K-major layout),
+//               warp 1 issues tcgen05.mma from one thread, warps 2-5 drain the TMEM accumulator
+//               (tcgen05.ld 32x32b) and run the fused epilogue; smem ring with full/empty
+//               mbarriers; tcgen05.commit releases stages.
 #include <cuda.h>
 
 #include <mutex>
@@ -174,64 +181,19 @@ __global__ void __launch_bounds__(192, 2) k_tc_gemm(const __grid_constant__ CUte
       float* so = sout + (ci & 1) * 3 * TBM * SP;
       // stage the inputs of this chunk (coalesced)
       bool staged = false;
-      if (EPI == T_FWD) {
-        if (g.xin2) {
-          const size_t ld = 2 * static_cast<size_t>(g.ldx);
-          tile_in(sin0, g.xin2 + row0 * ld + col0, ld, et);
-          tile_in(sin1, g.xin2 + row0 * ld + g.ldx + col0, ld, et);
-          staged = true;
-        }
-      } else {
-        if (g.dyin) {
-          tile_in(sin0, g.dyin + row0 * g.ldc + col0, g.ldc, et);
-          staged = true;
-        }
-        if (g.tprev) {
-          tile_in(sin1, g.tprev + row0 * g.ldc + col0, g.ldc, et);
-          staged = true;
-        }
+      if (g.dyin) {
+        tile_in(sin0, g.dyin + row0 * g.ldc + col0, g.ldc, et);
+        staged = true;
+      }
+      if (g.tprev) {
+        tile_in(sin1, g.tprev + row0 * g.ldc + col0, g.ldc, et);
+        staged = true;
       }
       uint32_t v[CW];
       tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + c0, v);
       tmem_wait_ld();
       if (staged) epi_bar();
-      if (EPI == T_FWD) {
-        // gather phase first (all 16 table rows in flight), then the arithmetic: a per-element
-        // branchy lookup serialised the L1/L2 latency of every gather
-        double z[CW], c0v[CW], c1v[CW], c2v[CW];
-#pragma unroll
-        for (int j = 0; j < CW; ++j) {
-          z[j] = static_cast<double>(__uint_as_float(v[j])) + static_cast<double>(__ldg(g.bias + col0 + j));
-          const int k = min(static_cast<int>(fabs(z[j]) * 1024.0), 8191);
-          const double* qq = g.tanh_c + 3 * k;
-          c0v[j] = __ldg(qq);
-          c1v[j] = __ldg(qq + 1);
-          c2v[j] = __ldg(qq + 2);
-        }
-#pragma unroll
-        for (int j = 0; j < CW; ++j) {
-          // TanhTable::operator() (tanh_table.hpp:18-30)
-          const double ax = fabs(z[j]);
-          const int k = min(static_cast<int>(ax * 1024.0), 8191);
-          const double u = ax - k * (1.0 / 1024.0);
-          double td = ax > 8.0 ? 1.0 : c0v[j] + u * (c1v[j] + u * c2v[j]);
-          td = signbit(z[j]) ? -td : td;
-          double y = td;
-          if (g.xin2) y += static_cast<double>(sin0[r * SP + j]) + static_cast<double>(sin1[r * SP + j]);
-          const float yf = static_cast<float>(y);
-          const float hi = tf32r(yf);
-          so[r * SP + j] = static_cast<float>((1.0 - td) * (1.0 + td));
-          so[TBM * SP + r * SP + j] = hi;
-          so[2 * TBM * SP + r * SP + j] = tf32r(yf - hi);
-        }
-        epi_bar();
-        tile_out(g.tout + row0 * g.ldc + col0, so, g.ldc, et);
-        if (g.y2) {
-          const size_t ld = 2 * static_cast<size_t>(g.ld2);
-          tile_out(g.y2 + row0 * ld + col0, so + TBM * SP, ld, et);
-          tile_out(g.y2 + row0 * ld + g.ld2 + col0, so + 2 * TBM * SP, ld, et);
-        }
-      } else if (g.dD) {
+      if (g.dD) {
         double* sd = reinterpret_cast<double*>(so);
 #pragma unroll
         for (int j = 0; j < CW; ++j) {
@@ -272,6 +234,199 @@ __global__ void __launch_bounds__(192, 2) k_tc_gemm(const __grid_constant__ CUte
   fence_before();
   __syncthreads();
   if (warp == 0) tmem_free<TCOLS>(tmem);
+}
+
+// Forward layer with FP64 accumulation of short tcgen05 chains (mixed mode). The tensor core's
+// FP32 accumulation loses low-order bits at every add; over the 3 x 2048-term first layer (a
+// cancelling sum, |z| ~ sum|D W| / 45) that bias reached 1e-4 on small total energies (water
+// preset). Here the MMA warp accumulates only F64_CH 128-byte K blocks of each of the three
+// 3xTF32 segments (3 x 64 K terms) per chain, alternating between two TMEM accumulators; eight
+// epilogue warps (two per TMEM lane quarter, half the columns each) drain each finished chain
+// into FP64 registers while the next one runs, so the FP32 error is bounded per chain and the K
+// reduction itself is FP64. Tile 128 x BN (BN <= 128), one CTA per SM.
+constexpr int F64_ST = 8; // 8 x 26 KB stages: one N=80 stage is only ~90 ns of MMA work
+constexpr int F64_CH = 2; // K blocks per segment per chain (1: 1.5e-6 on water E, 2 measured below 1e-5)
+constexpr int F64_THREADS = 320; // TMA warp, MMA warp, 8 epilogue warps
+
+template <int BN>
+constexpr int f64_zpitch() { return BN + 2; }
+
+template <int BN>
+constexpr size_t f64_smem_body() {
+  constexpr size_t pipe = static_cast<size_t>(F64_ST) * (TBM + BN) * TBKB;
+  constexpr size_t epi = static_cast<size_t>(STAGE_BYTES) + static_cast<size_t>(TBM) * f64_zpitch<BN>() * 8;
+  return pipe > epi ? pipe : epi;
+}
+
+__device__ __forceinline__ void epi2_bar() { asm volatile("bar.sync 2, 256;\n" ::: "memory"); }
+
+template <int BN>
+__global__ void __launch_bounds__(F64_THREADS, 1) k_tc_fwd64(const __grid_constant__ CUtensorMap ta,
+                                                            const __grid_constant__ CUtensorMap tb, TArgs g) {
+  using namespace tc;
+  static_assert(BN % 16 == 0 && BN <= 128, "one 128-column TMEM buffer per chain");
+  constexpr int A_ST = TBM * TBKB, B_ST = BN * TBKB;
+  constexpr size_t BODY = f64_smem_body<BN>();
+  constexpr int ZP = f64_zpitch<BN>();
+  constexpr int HB = BN / 2; // columns per epilogue warp
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  unsigned char* sa = smem;
+  unsigned char* sb = smem + F64_ST * A_ST;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + BODY);
+  uint64_t* empty = full + F64_ST;
+  uint64_t* accf = empty + F64_ST; // [2] chain finished (MMA -> epilogue)
+  uint64_t* acce = accf + 2;       // [2] chain drained (epilogue -> MMA), 256 arrivals
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(acce + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * TBM, n0 = blockIdx.x * BN; // column tiles of a row tile adjacent: A shared in L2
+  const int KB = g.kseg / 32;                  // 128-byte K blocks per half
+  const int NC = (KB + F64_CH - 1) / F64_CH;   // chains
+  if (warp == 0) {
+    tmem_alloc<256>(tslot);
+    if (lane == 0) {
+      prefetch_tmap(&ta);
+      prefetch_tmap(&tb);
+    }
+  }
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < F64_ST; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(accf + b, 1);
+      mbar_init(acce + b, 256);
+    }
+    fence_barrier_init();
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tslot;
+  // k-block order: chain c, segment seg, block kb in [c*CH, min(KB, c*CH + CH))
+  if (warp == 0 && lane == 0) {
+    const int half = g.kseg * 4;
+    int kt = 0;
+    for (int c = 0; c < NC; ++c)
+      for (int seg = 0; seg < 3; ++seg)
+        for (int kb = c * F64_CH; kb < min(KB, c * F64_CH + F64_CH); ++kb, ++kt) {
+          const int s = kt % F64_ST;
+          if (kt >= F64_ST) mbar_wait(empty + s, ((kt / F64_ST) - 1) & 1);
+          mbar_expect_tx(full + s, A_ST + B_ST);
+          tma_load_2d(sa + s * A_ST, &ta, (seg == 2 ? half : 0) + kb * TBKB, m0, full + s);
+          tma_load_2d(sb + s * B_ST, &tb, (seg == 1 ? half : 0) + kb * TBKB, n0, full + s);
+        }
+  } else if (warp == 1 && lane == 0) {
+    constexpr uint32_t idesc = make_idesc(TBM, BN, 2, 1);
+    int kt = 0;
+    for (int c = 0; c < NC; ++c) {
+      const int b = c & 1;
+      if (c >= 2) mbar_wait(acce + b, ((c >> 1) - 1) & 1);
+      fence_after();
+      const uint32_t td = tmem + static_cast<uint32_t>(b * 128);
+      bool first = true;
+      for (int seg = 0; seg < 3; ++seg)
+        for (int kb = c * F64_CH; kb < min(KB, c * F64_CH + F64_CH); ++kb, ++kt) {
+          const int s = kt % F64_ST;
+          mbar_wait(full + s, (kt / F64_ST) & 1);
+          fence_after();
+          const uint32_t a0 = smem_u32(sa + s * A_ST), b0 = smem_u32(sb + s * B_ST);
+#pragma unroll
+          for (int k = 0; k < TBKB / 32; ++k) {
+            mma_tf32(td, make_desc_sw128(a0 + k * 32), make_desc_sw128(b0 + k * 32), idesc, first ? 0u : 1u);
+            first = false;
+          }
+          commit(empty + s);
+        }
+      commit(accf + b);
+    }
+  } else if (warp >= 2) {
+    const int q = warp & 3;             // TMEM lane quarter
+    const int hh = (warp - 2) >> 2;     // column half
+    const int r = q * 32 + lane;        // tile row
+    double acc[HB];
+#pragma unroll
+    for (int j = 0; j < HB; ++j) acc[j] = 0.0;
+    for (int c = 0; c < NC; ++c) {
+      const int b = c & 1;
+      mbar_wait(accf + b, (c >> 1) & 1);
+      fence_after();
+      const uint32_t ta0 =
+          tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(b * 128 + hh * HB);
+      uint32_t v[HB];
+#pragma unroll
+      for (int j0 = 0; j0 + 16 <= HB; j0 += 16) tmem_ld16(ta0 + j0, v + j0);
+      if constexpr (HB % 16 == 8) tmem_ld8(ta0 + (HB - 8), v + (HB - 8));
+      tmem_wait_ld();
+      fence_before();
+      mbar_arrive(acce + b);
+#pragma unroll
+      for (int j = 0; j < HB; ++j) acc[j] += static_cast<double>(__uint_as_float(v[j]));
+    }
+    // every chain is drained (the operand ring is free): z rows to shared memory, then the layer
+    // epilogue of k_tc_gemm (bias, tanh table, shortcut, hi|lo split) in 16-column chunks by the
+    // first four epilogue warps
+    double* zs = reinterpret_cast<double*>(smem + STAGE_BYTES);
+#pragma unroll
+    for (int j = 0; j < HB; ++j) zs[r * ZP + hh * HB + j] = acc[j];
+    epi2_bar();
+    if (hh == 0) {
+      const int et = threadIdx.x - 64;
+      float* sin0 = reinterpret_cast<float*>(smem);
+      float* sin1 = sin0 + TBM * SP;
+      float* sout = sin0 + 2 * TBM * SP;
+      const size_t row0 = static_cast<size_t>(m0);
+      for (int c0 = 0, ci = 0; c0 < BN; c0 += CW, ++ci) {
+        const int col0 = n0 + c0;
+        float* so = sout + (ci & 1) * 3 * TBM * SP;
+        if (g.xin2) {
+          const size_t ld = 2 * static_cast<size_t>(g.ldx);
+          tile_in(sin0, g.xin2 + row0 * ld + col0, ld, et);
+          tile_in(sin1, g.xin2 + row0 * ld + g.ldx + col0, ld, et);
+          epi_bar();
+        }
+        double z[CW], c0v[CW], c1v[CW], c2v[CW];
+#pragma unroll
+        for (int j = 0; j < CW; ++j) {
+          z[j] = zs[r * ZP + c0 + j] + static_cast<double>(__ldg(g.bias + col0 + j));
+          const int k = min(static_cast<int>(fabs(z[j]) * 1024.0), 8191);
+          const double* qq = g.tanh_c + 3 * k;
+          c0v[j] = __ldg(qq);
+          c1v[j] = __ldg(qq + 1);
+          c2v[j] = __ldg(qq + 2);
+        }
+#pragma unroll
+        for (int j = 0; j < CW; ++j) {
+          // TanhTable::operator() (tanh_table.hpp:18-30)
+          const double ax = fabs(z[j]);
+          const int k = min(static_cast<int>(ax * 1024.0), 8191);
+          const double u = ax - k * (1.0 / 1024.0);
+          double td = ax > 8.0 ? 1.0 : c0v[j] + u * (c1v[j] + u * c2v[j]);
+          td = signbit(z[j]) ? -td : td;
+          double y = td;
+          if (g.xin2) y += static_cast<double>(sin0[r * SP + j]) + static_cast<double>(sin1[r * SP + j]);
+          const float yf = static_cast<float>(y);
+          const float hi = tf32r(yf);
+          so[r * SP + j] = static_cast<float>((1.0 - td) * (1.0 + td));
+          so[TBM * SP + r * SP + j] = hi;
+          so[2 * TBM * SP + r * SP + j] = tf32r(yf - hi);
+        }
+        epi_bar();
+        tile_out(g.tout + row0 * g.ldc + col0, so, g.ldc, et);
+        if (g.y2) {
+          const size_t ld = 2 * static_cast<size_t>(g.ld2);
+          tile_out(g.y2 + row0 * ld + col0, so + TBM * SP, ld, et);
+          tile_out(g.y2 + row0 * ld + g.ld2 + col0, so + 2 * TBM * SP, ld, et);
+        }
+        if (g.xin2) epi_bar();
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_free<256>(tmem);
 }
 
 // Readout: E = b_out + y . w_out (y = hi + lo); dz_L = w_out tanh'(z_L) split (hi|lo).
@@ -328,6 +483,17 @@ CUtensorMap byte_map(const void* ptr, uint64_t rows, uint64_t row_bytes, uint32_
   return m;
 }
 
+template <int BN>
+void launch_tc_fwd64(const float* A2, const float* B2, int rows, int N, TArgs g, cudaStream_t st) {
+  const size_t smem = f64_smem_body<BN>() + 8 * (2 * F64_ST + 4) + 16 + 1024;
+  smem_optin(k_tc_fwd64<BN>, smem);
+  const uint64_t row_bytes = static_cast<uint64_t>(2) * g.kseg * 4;
+  const CUtensorMap ta = byte_map(A2, rows, row_bytes, TBM);
+  const CUtensorMap tb = byte_map(B2, N, row_bytes, BN);
+  k_tc_fwd64<BN><<<dim3(N / BN, rows / TBM), F64_THREADS, smem, st>>>(ta, tb, g);
+  DPB_CUDA(cudaGetLastError());
+}
+
 template <int EPI, int BN>
 void launch_tc(const float* A2, const float* B2, int rows, int N, TArgs g, cudaStream_t st) {
   constexpr int PIPE = TST * (TBM + BN) * TBKB;
@@ -351,9 +517,17 @@ void run_tc_epi(const float* A2, const float* B2, int rows, int N, const TArgs& 
   else throw InputErr("unsupported fitting width for the tensor-core path");
 }
 
+// Forward layer with FP64 K accumulation (k_tc_fwd64), column tiles of 80 / 64 / 128.
+void run_tc_fwd64(const float* A2, const float* B2, int rows, int N, const TArgs& g, cudaStream_t st) {
+  if (N % 80 == 0) launch_tc_fwd64<80>(A2, B2, rows, N, g, st);
+  else if (N % 128 == 0) launch_tc_fwd64<128>(A2, B2, rows, N, g, st);
+  else if (N % 64 == 0) launch_tc_fwd64<64>(A2, B2, rows, N, g, st);
+  else throw InputErr("unsupported fitting width for the tensor-core path");
+}
+
 void run_tc(int epi, const float* A2, const float* B2, int rows, int N, const TArgs& g, cudaStream_t st) {
-  if (epi == T_FWD) run_tc_epi<T_FWD>(A2, B2, rows, N, g, st);
-  else run_tc_epi<T_BWD>(A2, B2, rows, N, g, st);
+  if (epi != T_BWD) throw CudaErr("forward layers run on k_tc_fwd64");
+  run_tc_epi<T_BWD>(A2, B2, rows, N, g, st);
 }
 
 } // namespace
@@ -474,7 +648,8 @@ void Engine::fitting_type_rows_mixed(int t, int64_t r0_, int64_t rows_, cudaStre
     g.y2 = y2;
     g.ld2 = s2;
     g.tanh_c = tc_tanh.p;
-    run_tc(T_FWD, A2, tc_wf[t * L + k].p, rows, fl.outp, g, st);
+    // FP64 K accumulation (k_tc_fwd64) for the forward layers: the energy path
+    run_tc_fwd64(A2, tc_wf[t * L + k].p, rows, fl.outp, g, st);
     ++launches;
     yprev = y2;
     A2 = y2;

@@ -218,7 +218,7 @@ inline TabParams make_params(Engine& E) {
   p.xbin = E.xbin.p;
   p.xrc = E.xrc.p;
   p.tab = E.tab.p;
-  p.tab32 = E.precision == 1 && E.mixed_tab32 ? E.tab32.p : nullptr;
+  p.tab32 = E.precision == 1 ? E.tab32.p : nullptr;
   p.max_nbr = E.d_max_nbr.p;
   p.c = E.cell;
   p.rc2 = E.r_cut * E.r_cut;

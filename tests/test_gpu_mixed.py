@@ -1,11 +1,10 @@
 """Mixed-precision mode (tcgen05 3xTF32 fitting net + tanh table) against the FP64 oracle.
 
-SURVEY.md §8d asks for the FP64 metrics at 1e-5. The benchmark system (copper preset) meets 1e-5 on
-E, F, virial and E_i. The fitting GEMMs accumulate in FP32 (tcgen05 TMEM), and the unnormalised
-descriptor makes the first layer a cancelling sum (|z| ~ sum|D W| / 45), so models whose per-atom
-energies themselves cancel to ~1e-3 (water preset: E_i ~ 3e-3 eV, total -1.08 eV from 768 atoms)
-show ~1e-4 on the TOTAL energy while forces stay at ~1e-5; those cases are checked at the
-tolerances recorded below.
+SURVEY.md §8d / north_star: E, F, virial and E_i within 1e-5 of the FP64 reference on every
+preset. The unnormalised descriptor makes the first fitting layer a cancelling sum
+(|z| ~ sum|D W| / 45); the forward layers therefore accumulate K in FP64 over short tensor-core
+chains (fitting_tc.cu k_tc_fwd64), which keeps even the water preset (E ~ -1.08 eV from 768 atoms
+whose E_i cancel) at ~5e-6.
 """
 import numpy as np
 import pytest
@@ -47,7 +46,7 @@ def test_mixed_two_types(seed):
     t = dp.build_tables(m, 0.05)
     c = dp.make_random_config(10, 2, 9.0, 1.8, seed)
     ro, _ = O.or_compute(c, m, t)
-    check(dp.DeepPot(m, t, precision="mixed").compute(c), ro, {"E": 3e-5, "F": 3e-5, "V": 3e-5, "Ei": 3e-5})
+    check(dp.DeepPot(m, t, precision="mixed").compute(c), ro)
 
 
 def test_mixed_water():
@@ -55,7 +54,7 @@ def test_mixed_water():
     t = dp.build_tables(m, 0.01)
     c = dp.gen_config("water-like", 4, 4, 4, 0.1, 4)
     ro, _ = O.or_compute(c, m, t)
-    check(dp.DeepPot(m, t, precision="mixed").compute(c), ro, {"E": 3e-4, "Ei": 3e-4, "F": 1e-4, "V": 1e-4})
+    check(dp.DeepPot(m, t, precision="mixed").compute(c), ro)
 
 
 def test_mixed_md_thermo():
@@ -68,4 +67,5 @@ def test_mixed_md_thermo():
     b = O.or_run_md(c.copy(), v.copy(), m, t, mc)
     for x, y in zip(a.thermo, b.thermo):
         assert abs(x.pe - y.pe) <= TOL * abs(y.pe)
+        # KE after up to 20 steps: per-evaluation force errors (~3e-6) grow along the trajectory
         assert abs(x.ke - y.ke) <= 1e-4 * abs(y.ke)
