@@ -13,6 +13,8 @@
 // Tiles: CTA 64x64, BK 16, 4 warps of 32x32 (4x4 DMMA tiles), 3-stage cp.async pipeline; both
 // operands K-contiguous in shared memory with a 20-double row pitch (bank-conflict free).
 #include <cstdlib>
+#include <map>
+#include <mutex>
 
 #include "engine.hpp"
 
@@ -20,7 +22,7 @@ namespace dpb {
 
 namespace {
 
-constexpr int BM = 64, BK = 16, PITCH = BK + 4;
+constexpr int BK = 16, PITCH = BK + 4;
 
 enum Epi : int { EPI_FWD = 0, EPI_BWD = 1 };
 
@@ -59,9 +61,13 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 }
 
 // BN = 64 (4 DMMA column tiles per warp) or 80 (5): 240-wide layers tile exactly with 80.
-template <int EPI, int BN, int STAGES>
+// BM = 64 (warp rows 32: 4 DMMA row tiles) or 32 (2): the smaller tile is chosen when it fills
+// the waves of resident CTAs better (run_gemm); every output element accumulates its K terms in
+// the same order for either tile, so the choice never changes a result bit.
+template <int EPI, int BM, int BN, int STAGES>
 __device__ __forceinline__ void gemm_body(const GemmArgs& g) {
   constexpr int NT = BN / 16; // 8-wide column tiles per warp (2 warps across BN)
+  constexpr int MT = BM / 16; // 8-high row tiles per warp (2 warps across BM)
   extern __shared__ __align__(16) double sm[];
   double* As = sm;                                // [STAGES][BM][PITCH]
   double* Bs = sm + STAGES * BM * PITCH;          // [STAGES][BN][PITCH]
@@ -82,8 +88,8 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& g) {
     double* as = As + stage * BM * PITCH;
     double* bs = Bs + stage * BN * PITCH;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int idx = tid + c * 128; // 512 chunks of 2 doubles for the A tile
+    for (int c = 0; c < BM / 16; ++c) {
+      const int idx = tid + c * 128; // BM*8 chunks of 2 doubles for the A tile
       const int row = idx >> 3, col = (idx & 7) * 2;
       cp_async16(as + row * PITCH + col, A + static_cast<size_t>(row) * g.lda + k0 + col);
     }
@@ -95,9 +101,9 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& g) {
     }
   };
 
-  double acc[4][NT][2];
+  double acc[MT][NT][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < MT; ++i)
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
@@ -112,27 +118,27 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& g) {
     const int nk = kt + STAGES - 1;
     if (nk < KT) load_stage(nk % STAGES, nk);
     cp_commit();
-    const double* as = As + (kt % STAGES) * BM * PITCH + (wm * 32 + gid) * PITCH + tig;
+    const double* as = As + (kt % STAGES) * BM * PITCH + (wm * (BM / 2) + gid) * PITCH + tig;
     const double* bs = Bs + (kt % STAGES) * BN * PITCH + (wn * (BN / 2) + gid) * PITCH + tig;
 #pragma unroll
     for (int kk = 0; kk < BK / 4; ++kk) {
-      double af[4], bf[NT];
+      double af[MT], bf[NT];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = as[i * 8 * PITCH + kk * 4];
+      for (int i = 0; i < MT; ++i) af[i] = as[i * 8 * PITCH + kk * 4];
 #pragma unroll
       for (int j = 0; j < NT; ++j) bf[j] = bs[j * 8 * PITCH + kk * 4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < MT; ++i)
 #pragma unroll
         for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
   }
   cp_wait<0>();
 
-  // Epilogue: thread holds rows (m0 + wm*32 + i*8 + gid), cols (n0 + wn*BN/2 + j*8 + 2*tig + {0,1}).
+  // Epilogue: thread holds rows (m0 + wm*BM/2 + i*8 + gid), cols (n0 + wn*BN/2 + j*8 + 2*tig + {0,1}).
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int row = m0 + wm * 32 + i * 8 + gid;
+  for (int i = 0; i < MT; ++i) {
+    const int row = m0 + wm * (BM / 2) + i * 8 + gid;
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
       const int col = n0 + wn * (BN / 2) + j * 8 + 2 * tig;
@@ -170,16 +176,16 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& g) {
   }
 }
 
-template <int EPI, int BN, int STAGES>
+template <int EPI, int BM, int BN, int STAGES>
 __global__ void __launch_bounds__(128) k_gemm(GemmArgs g) {
-  gemm_body<EPI, BN, STAGES>(g);
+  gemm_body<EPI, BM, BN, STAGES>(g);
 }
 
 // Short-K (240-wide hidden) layers capped at 128 registers: 4 CTAs (16 warps) per SM instead of 3
 // (C2 fitting phase 2.74 -> see DESIGN.md §3)
-template <int EPI, int BN, int STAGES>
+template <int EPI, int BM, int BN, int STAGES>
 __global__ void __launch_bounds__(128, 4) k_gemm4(GemmArgs g) {
-  gemm_body<EPI, BN, STAGES>(g);
+  gemm_body<EPI, BM, BN, STAGES>(g);
 }
 
 // Readout: E = b_out + y . w_out (warp per row); dZ_L = w_out (1 - t^2); dY_L = w_out.
@@ -212,17 +218,58 @@ __global__ void k_scatter_energy(int64_t slots, const int32_t* __restrict__ atom
   if (a >= 0) e_atom[a] = e_slot[s];
 }
 
+// Resident CTAs per SM of a kernel at its dynamic shared memory (cached per kernel and size).
+int ctas_per_sm(const void* kern, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, size_t>, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find({kern, bytes});
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  DPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, 128, bytes));
+  cache[{kern, bytes}] = std::max(n, 1);
+  return std::max(n, 1);
+}
+
+int sm_count_fit() {
+  int dev = 0, s = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
+  return s > 0 ? s : 148;
+}
+
+template <int EPI, int BM, int BN, int STAGES>
+struct GemmKernel {
+  static constexpr size_t bytes = static_cast<size_t>(STAGES) * (BM + BN) * PITCH * sizeof(double);
+  static constexpr bool four = BN == 80 && STAGES == 2;
+  static auto kern() { return four ? k_gemm4<EPI, BM, BN, STAGES> : k_gemm<EPI, BM, BN, STAGES>; }
+  // fraction of the resident-CTA slots the tiles fill over the waves they need
+  static double wave_eff(int rows, int N) {
+    const int tiles = (N / BN) * (rows / BM);
+    const int slots = ctas_per_sm(reinterpret_cast<const void*>(kern()), bytes) * sm_count_fit();
+    const int waves = (tiles + slots - 1) / slots;
+    return static_cast<double>(tiles) / (static_cast<double>(waves) * slots);
+  }
+  static void launch(const GemmArgs& a, int rows, int N, cudaStream_t st) {
+    auto k = kern();
+    smem_optin(k, bytes);
+    GemmArgs g = a;
+    g.ntn = N / BN;
+    g.ntm = rows / BM;
+    k<<<g.ntn * g.ntm, 128, bytes, st>>>(g);
+    DPB_CUDA(cudaGetLastError());
+  }
+};
+
+// 64- or 32-row tiles, whichever fills the waves better (ties: 64, the higher per-tile rate)
 template <int EPI, int BN, int STAGES>
 void launch_gemm(const GemmArgs& a, int rows, int N, cudaStream_t st) {
-  const size_t bytes = static_cast<size_t>(STAGES) * (BM + BN) * PITCH * sizeof(double);
-  constexpr bool four = BN == 80 && STAGES == 2;
-  auto kern = four ? k_gemm4<EPI, BN, STAGES> : k_gemm<EPI, BN, STAGES>;
-  smem_optin(kern, bytes);
-  GemmArgs g = a;
-  g.ntn = N / BN;
-  g.ntm = rows / BM;
-  kern<<<g.ntn * g.ntm, 128, bytes, st>>>(g);
-  DPB_CUDA(cudaGetLastError());
+  using K64 = GemmKernel<EPI, 64, BN, STAGES>;
+  using K32 = GemmKernel<EPI, 32, BN, STAGES>;
+  if (rows % 64 == 0 && K64::wave_eff(rows, N) >= K32::wave_eff(rows, N) - 0.05)
+    K64::launch(a, rows, N, st);
+  else
+    K32::launch(a, rows, N, st);
 }
 
 // N is a multiple of 80 or 64 (widths are padded by pad_width()).
