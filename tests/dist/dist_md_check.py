@@ -51,6 +51,9 @@ def main():
             "ke": [[a.ke, b.ke] for a, b in zip(rd.thermo, rs.thermo)],
             "pressure": [[a.pressure, b.pressure] for a, b in zip(rd.thermo, rs.thermo)],
             "pos_normwise": nw(pos, cs.pos), "vel_normwise": nw(vel, vs),
+            # per-atom forces are summed in the single-GPU order (global-id rows + pair halo), so
+            # the whole trajectory is bitwise independent of the GPU count
+            "pos_bitwise": bool(np.array_equal(pos, cs.pos)), "vel_bitwise": bool(np.array_equal(vel, vs)),
             "force_evals": [rd.force_evals, rs.force_evals],
             "counters": [[rd.counters.rows_forward, rd.counters.rows_backward, rd.counters.extrapolations],
                          [rs.counters.rows_forward, rs.counters.rows_backward, rs.counters.extrapolations]],

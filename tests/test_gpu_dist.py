@@ -43,6 +43,7 @@ def test_two_rank_md_matches_single_gpu(tmp_path, overlap, chunk):
     for a, b in r["ke"]:
         assert abs(a - b) <= 1e-9 * abs(b)
     assert r["pos_normwise"] <= 1e-10 and r["vel_normwise"] <= 1e-8
+    assert r["pos_bitwise"] and r["vel_bitwise"], "trajectory not bitwise equal to one GPU"
 
 
 @pytest.mark.skipif(n_gpus() < 4, reason="needs >= 4 GPUs")
@@ -58,3 +59,4 @@ def test_four_rank_md_matches_single_gpu(tmp_path):
     for a, b in r["pe"]:
         assert abs(a - b) <= 1e-10 * abs(b)
     assert r["pos_normwise"] <= 1e-10 and r["vel_normwise"] <= 1e-8
+    assert r["pos_bitwise"] and r["vel_bitwise"], "trajectory not bitwise equal to one GPU"
