@@ -69,6 +69,9 @@ __host__ __device__ inline void key_shift(uint64_t k, int* s) {
   s[2] = static_cast<int>(k & 1023) - KEY_SHIFT_BIAS;
 }
 // Key of the reverse entry (j -> i, -s) as seen in row j.
+__host__ __device__ inline uint64_t with_key_j(uint64_t k, int j) {
+  return (k & ~(static_cast<uint64_t>((1u << 28) - 1) << 30)) | (static_cast<uint64_t>(j) << 30);
+}
 __host__ __device__ inline uint64_t reverse_key(uint64_t k, int type_i, int i) {
   int s[3];
   key_shift(k, s);

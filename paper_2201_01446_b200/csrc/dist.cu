@@ -8,11 +8,15 @@
 //
 // Per rank the local system is the owned atoms (ascending global id) followed by the ghosts
 // (ascending global id): the centres are one contiguous range, so the evaluation chunks never
-// span ghost rows. A row holds the global row's entries, ordered by local index (results agree
-// with one GPU to rounding, 1e-10 tested). Only owned atoms are centres. Per step:
+// span ghost rows. Rows are built and sorted in global-id space (pairs evaluated from the lower
+// global id, keys sorted by (type, global id, shift), then mapped back to local indices), so every
+// row equals the global row entry for entry and in order. Only owned atoms are centres. Per step:
 //   forward halo   owned positions -> the ranks that hold them as ghosts   (ncclSend/ncclRecv)
-//   evaluate       local kernels; ghost rows only gather the reverse pair gradients
-//   reverse halo   ghost force partials -> owners, accumulated in peer order (deterministic)
+//   evaluate       local kernels (centres = owned atoms)
+//   pair halo      for each ghost j and each entry (j -> i) with i owned here, the pair gradient
+//                  g(i -> j) -> j's owner, which sums it into F_j in its own row order
+// so each owned atom's force is summed in exactly the order one GPU sums it: forces, positions
+// and velocities are bitwise independent of the GPU count (tests/test_gpu_dist.py).
 // At a rebuild every rank all-gathers the owned (id, x, v), repartitions identically and
 // rebuilds its local system. No collective touches the data path except these exchanges.
 #include <chrono>
@@ -63,6 +67,16 @@ struct Dist {
   DevBuf<uint64_t> d_keys, d_keys2;
   DevBuf<uint8_t> d_smask, d_lcenter;
   DevBuf<int64_t> d_counts; // [0] n_local, [1 .. W] send counts, [W+1 .. 2W] recv counts
+  // pair-gradient halo (per step, after the backward pass): for every ghost j of this rank and
+  // every entry (j -> i) of its row with i owned here, the gradient g of the reverse pair
+  // (i -> j) goes to j's owner, which sums it into F_j in its own row order -- the force
+  // summation order of one GPU. Slots are fixed per rebuild (NaN marks a non-real pair).
+  DevBuf<int64_t> gs_base;   // [ghost list] first send slot of each ghost (ridx order)
+  DevBuf<int64_t> gr_base;   // [owned list] first receive slot of each owned atom (sidx order)
+  DevBuf<int32_t> rslot;     // [E] receive slot of an owned row's entry with a ghost neighbour, else -1
+  DevBuf<int64_t> d_gcnt;    // scratch counts
+  DevBuf<double> gsend, grecv;
+  std::vector<int64_t> gsoff, groff; // slot offsets per peer (send / receive)
   DevBuf<unsigned char> d_tmp;
   bool host_global_valid = true; // gpos/gvel (host) reflect the last gather
 };
@@ -177,6 +191,78 @@ __global__ void k_unpack_pos(int64_t m, const int32_t* __restrict__ idx, const d
   pos4[i] = make_double4(x, y, z, 0.0);
 }
 
+// Per ghost j of the list (t-th): number of entries of its row whose neighbour is owned here.
+__global__ void k_ghost_slots(int64_t m, const int32_t* __restrict__ list, const int64_t* __restrict__ row_off,
+                              const uint64_t* __restrict__ keys, const uint8_t* __restrict__ center,
+                              int64_t* __restrict__ cnt) {
+  const int64_t t = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= m) return;
+  const int j = list[t];
+  int c = 0;
+  for (int64_t e = row_off[j] + lane; e < row_off[j + 1]; e += 32) c += center[key_j(keys[e])] ? 1 : 0;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) cnt[t] = c;
+}
+
+// Per owned atom j of peer p's list (t-th): entries of its row whose neighbour is owned by p;
+// with fill != 0 also their receive slots, in row order (= the order p packs them in).
+__global__ void k_owned_slots(int64_t m, const int32_t* __restrict__ list, int p, const int64_t* __restrict__ row_off,
+                              const uint64_t* __restrict__ keys, const int32_t* __restrict__ gid,
+                              const int32_t* __restrict__ owner, int64_t* __restrict__ cnt,
+                              const int64_t* __restrict__ base, int64_t off, int32_t* __restrict__ rslot) {
+  const int64_t t = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= m) return;
+  const int j = list[t];
+  int c = 0;
+  for (int64_t b = row_off[j]; b < row_off[j + 1]; b += 32) {
+    const int64_t e = b + lane;
+    const bool mine = e < row_off[j + 1] && owner[gid[key_j(keys[e])]] == p;
+    const unsigned mk = __ballot_sync(0xffffffffu, mine);
+    if (rslot && mine) rslot[e] = static_cast<int32_t>(off + base[t] + c + __popc(mk & ((1u << lane) - 1u)));
+    c += __popc(mk);
+  }
+  if (!rslot && lane == 0) cnt[t] = c;
+}
+
+// Pack: for ghost j (t-th of the list) and every entry (j -> i) with i owned here, the gradient
+// of the reverse pair (i -> j) -- g[realoff[i] + k] when that pair is real (rank k), else NaN.
+__global__ void k_pack_pair_g(int64_t m, const int32_t* __restrict__ list, const int64_t* __restrict__ row_off,
+                              const uint64_t* __restrict__ keys, const uint16_t* __restrict__ rev,
+                              const int16_t* __restrict__ rank, const int64_t* __restrict__ realoff,
+                              const uint8_t* __restrict__ center, const double* __restrict__ g,
+                              const int64_t* __restrict__ base, double* __restrict__ out) {
+  const int64_t t = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= m) return;
+  const int j = list[t];
+  int64_t slot = base[t];
+  for (int64_t b = row_off[j]; b < row_off[j + 1]; b += 32) {
+    const int64_t e = b + lane;
+    int i = 0;
+    bool own = false;
+    if (e < row_off[j + 1]) {
+      i = key_j(keys[e]);
+      own = center[i] != 0;
+    }
+    const unsigned mk = __ballot_sync(0xffffffffu, own);
+    if (own) {
+      const int k = rank[row_off[i] + rev[e]];
+      double* o = out + 3 * (slot + __popc(mk & ((1u << lane) - 1u)));
+      if (k >= 0) {
+        const double* gi = g + 3 * (realoff[i] + k);
+        o[0] = gi[0];
+        o[1] = gi[1];
+        o[2] = gi[2];
+      } else {
+        o[0] = o[1] = o[2] = __longlong_as_double(0x7ff8000000000000ll);
+      }
+    }
+    slot += __popc(mk);
+  }
+}
+
 // Chunk classification: flag[k] = 1 when a centre of chunk k (atoms [cka[k], cka[k+1])) has a
 // ghost in its neighbour row. Thread per atom, chunk found by binary search.
 __global__ void k_chunk_ghost(int64_t n, int nk, const int64_t* __restrict__ cka, const uint8_t* __restrict__ center,
@@ -194,16 +280,6 @@ __global__ void k_chunk_ghost(int64_t n, int nk, const int64_t* __restrict__ cka
       flag[lo] = 1;
       return;
     }
-}
-
-__global__ void k_accum3(int64_t m, const int32_t* __restrict__ idx, const double* __restrict__ src,
-                         double* __restrict__ dst) {
-  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (k >= m) return;
-  const int64_t i = idx[k];
-  dst[3 * i] += src[3 * k];
-  dst[3 * i + 1] += src[3 * k + 1];
-  dst[3 * i + 2] += src[3 * k + 2];
 }
 
 __global__ void k_pack_state(int64_t n, const uint8_t* __restrict__ center, const int64_t* __restrict__ gid,
@@ -538,6 +614,51 @@ void make_plan(const Dist& D, int r, Plan& P) {
   P.roff[D.world] = static_cast<int64_t>(P.rv.size());
 }
 
+// Slots of the pair-gradient halo (see Dist): send slots per ghost (ridx order) and receive
+// slots per entry of the owned rows that have a ghost neighbour, with one read-back of the
+// per-peer totals. Both sides count the same set -- the entries (j -> i) of j's row with i
+// owned by the sender -- because every rank's rows equal the global rows.
+void pair_plan(Engine& E) {
+  Dist& D = *E.dist;
+  cudaStream_t st = E.stream;
+  const int W = D.world;
+  const int64_t ng = D.roff[W], no = D.soff[W];
+  D.d_gcnt.ensure(std::max(ng, no) + 2);
+  D.gs_base.ensure(ng + 2);
+  D.gr_base.ensure(no + 2);
+  std::vector<int64_t> tot(2 * (W + 1), 0);
+  // send side: ghosts in ridx order, per-peer segments are contiguous
+  DPB_CUDA(cudaMemsetAsync(D.d_gcnt.p, 0, (ng + 1) * sizeof(int64_t), st));
+  if (ng) k_ghost_slots<<<ceil_div(ng * 32, 256), 256, 0, st>>>(ng, D.ridx.p, E.row_off.p, E.keys.p, E.center.p,
+                                                                D.d_gcnt.p);
+  excl_scan(D, D.d_gcnt.p, D.gs_base.p, ng + 1, st);
+  for (int p = 0; p <= W; ++p)
+    DPB_CUDA(cudaMemcpyAsync(&tot[p], D.gs_base.p + D.roff[p], sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  // receive side: owned atoms in sidx order (peer p's segment = p's ghosts owned here)
+  DPB_CUDA(cudaMemsetAsync(D.d_gcnt.p, 0, (no + 1) * sizeof(int64_t), st));
+  for (int p = 0; p < W; ++p) {
+    const int64_t o = D.soff[p], c = D.soff[p + 1] - o;
+    if (c) k_owned_slots<<<ceil_div(c * 32, 256), 256, 0, st>>>(c, D.sidx.p + o, p, E.row_off.p, E.keys.p, D.d_lgid.p,
+                                                                D.d_owner.p, D.d_gcnt.p + o, nullptr, 0, nullptr);
+  }
+  excl_scan(D, D.d_gcnt.p, D.gr_base.p, no + 1, st);
+  D.rslot.ensure(E.e_cap + 1);
+  DPB_CUDA(cudaMemsetAsync(D.rslot.p, 0xff, (E.e_cap + 1) * sizeof(int32_t), st));
+  for (int p = 0; p < W; ++p) {
+    const int64_t o = D.soff[p], c = D.soff[p + 1] - o;
+    if (c) k_owned_slots<<<ceil_div(c * 32, 256), 256, 0, st>>>(c, D.sidx.p + o, p, E.row_off.p, E.keys.p, D.d_lgid.p,
+                                                                D.d_owner.p, nullptr, D.gr_base.p + o, 0, D.rslot.p);
+  }
+  for (int p = 0; p <= W; ++p)
+    DPB_CUDA(cudaMemcpyAsync(&tot[W + 1 + p], D.gr_base.p + D.soff[p], sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  DPB_CUDA(cudaStreamSynchronize(st));
+  D.gsoff.assign(tot.begin(), tot.begin() + W + 1);
+  D.groff.assign(tot.begin() + W + 1, tot.end());
+  D.gsend.ensure(3 * D.gsoff[W] + 3);
+  D.grecv.ensure(3 * D.groff[W] + 3);
+  E.launches += 2 + 2 * W;
+}
+
 // Build the local system for this rank from the global state and upload it.
 void build_local(Engine& E) {
   static const bool trace = std::getenv("DPB_TRACE") != nullptr;
@@ -574,8 +695,11 @@ void build_local(Engine& E) {
   E.set_config(nl, lp.data(), lt.data(), D.box, D.pbc, lc.data());
   const auto t2 = now();
   E.md_upload_atoms(lv.data());
+  E.gid_of = D.d_lgid.p;  // rows in global-id order, pairs evaluated from the lower global id
+  E.local_of = D.d_lidx.p;
   E.build_list(E.r_cut + E.md.buffer);
   E.classify_chunks();
+  pair_plan(E);
   const auto t3 = now();
   if (trace) {
     auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
@@ -620,6 +744,10 @@ void dist_destroy(Engine& E) {
   E.dist->rbuf.release();
   E.dist->gbuf_send.release();
   E.dist->gbuf_all.release();
+  for (auto* b : {&E.dist->gs_base, &E.dist->gr_base, &E.dist->d_gcnt}) b->release();
+  E.dist->rslot.release();
+  E.dist->gsend.release();
+  E.dist->grecv.release();
   Dist& D = *E.dist;
   for (auto* b : {&D.d_gpos, &D.d_gvel, &D.d_fw, &D.d_lohi, &D.d_lpos, &D.d_lvel}) b->release();
   for (auto* b : {&D.d_gtypes, &D.d_owner, &D.d_ids, &D.d_ids2, &D.d_flag, &D.d_scan, &D.d_lidx, &D.d_lgid,
@@ -691,46 +819,28 @@ void dist_halo_forward(Engine& E) {
   }
 }
 
-// Reverse halo, first half: the ghost force partials (minus the pair gradients landing on
-// them) go back to their owners on st_comm, right after the ghost-only force kernel.
-// (the ghost-only force kernel has written the partials packed into sbuf, ridx order)
-void dist_reverse_send(Engine& E) {
+// Pair-gradient halo (every evaluation, before the force kernel): pack the reverse gradients of
+// my ghosts' rows, exchange them with the peers (grouped send/recv, slot counts fixed at the
+// rebuild), and hand the receive buffer and slot map to the force kernel.
+void dist_exchange_g(Engine& E, const int32_t** rslot, const double** grecv) {
   Dist& D = *E.dist;
-  DPB_CUDA(cudaEventRecord(E.ev_gf, E.stream));
-  DPB_CUDA(cudaStreamWaitEvent(E.st_comm, E.ev_gf, 0));
-  exchange(E, D.roff, D.soff, E.st_comm);
-  DPB_CUDA(cudaEventRecord(E.ev_rx, E.st_comm));
-  E.rev_sent = true;
-}
-
-// The ghosts of this rank in reverse-halo order (ridx: peer by peer, ascending global id) and
-// the send buffer their partials are packed into.
-bool dist_ghost_list(Engine& E, const int32_t** list, int64_t* n, double** send) {
-  Dist& D = *E.dist;
-  *list = D.ridx.p;
-  *n = D.roff[D.world];
-  *send = D.sbuf.p;
-  return D.ridx.p != nullptr;
-}
-
-// Reverse halo, second half: received partials added to the owned forces in peer order.
-void dist_halo_reverse(Engine& E) {
-  Dist& D = *E.dist;
-  const int64_t ns = D.soff[D.world], nr = D.roff[D.world];
-  if (E.rev_sent) {
-    DPB_CUDA(cudaStreamWaitEvent(E.stream, E.ev_rx, 0));
-    E.rev_sent = false;
-  } else {
-    if (nr) k_pack3<<<ceil_div(nr, 256), 256, 0, E.stream>>>(nr, D.ridx.p, E.forces.p, D.sbuf.p);
-    exchange(E, D.roff, D.soff, E.stream);
-    E.launches += 1;
+  const int W = D.world;
+  const int64_t ng = D.roff[W];
+  if (ng)
+    k_pack_pair_g<<<ceil_div(ng * 32, 256), 256, 0, E.stream>>>(ng, D.ridx.p, E.row_off.p, E.keys.p, E.rev.p,
+                                                               E.ridx.p, E.realoff.p, E.center.p, E.g.p,
+                                                               D.gs_base.p, D.gsend.p);
+  DPB_NCCL(ncclGroupStart());
+  for (int p = 0; p < W; ++p) {
+    const int64_t so = D.gsoff[p], sc = D.gsoff[p + 1] - so;
+    const int64_t ro = D.groff[p], rc = D.groff[p + 1] - ro;
+    if (sc > 0) DPB_NCCL(ncclSend(D.gsend.p + 3 * so, 3 * sc, ncclDouble, p, D.comm, E.stream));
+    if (rc > 0) DPB_NCCL(ncclRecv(D.grecv.p + 3 * ro, 3 * rc, ncclDouble, p, D.comm, E.stream));
   }
-  (void)ns;
-  for (int p = 0; p < D.world; ++p) {
-    const int64_t o = D.soff[p], c = D.soff[p + 1] - o;
-    if (c) k_accum3<<<ceil_div(c, 256), 256, 0, E.stream>>>(c, D.sidx.p + o, D.rbuf.p + 3 * o, E.forces.p);
-  }
-  E.launches += D.world;
+  DPB_NCCL(ncclGroupEnd());
+  E.launches += 1;
+  *rslot = D.rslot.p;
+  *grecv = D.grecv.p;
 }
 
 // All-gather of the owned (id, x, v) into the global arrays on every rank (device resident).

@@ -103,7 +103,7 @@ void Engine::create(const dp_model_desc* md, const dp_table_desc* td, int dev, i
   DPB_CUDA(cudaSetDevice(dev));
   DPB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   DPB_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
-  for (cudaEvent_t* e : {&ev_join, &ev_fwd[0], &ev_fwd[1], &ev_kd, &ev_halo, &ev_gf, &ev_rx})
+  for (cudaEvent_t* e : {&ev_join, &ev_fwd[0], &ev_fwd[1], &ev_kd, &ev_halo})
     DPB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   DPB_CUDA(cudaStreamCreateWithFlags(&st_comm, cudaStreamNonBlocking));
   n_types = md->n_types;
@@ -256,7 +256,7 @@ void Engine::destroy() {
     }
   if (stream) cudaStreamDestroy(stream);
   stream = nullptr;
-  for (cudaEvent_t* e : {&ev_join, &ev_fwd[0], &ev_fwd[1], &ev_kd, &ev_halo, &ev_gf, &ev_rx})
+  for (cudaEvent_t* e : {&ev_join, &ev_fwd[0], &ev_fwd[1], &ev_kd, &ev_halo})
     if (*e) {
       cudaEventDestroy(*e);
       *e = nullptr;
@@ -725,7 +725,6 @@ void Engine::md_begin(const double* pos, const double* vel, const dp_md_config* 
   DPB_CUDA(cudaMemsetAsync(red.p + 11, 0, sizeof(double), stream)); // max drift seen
   reset_counters();
   evaluate();
-  if (dist) dist_halo_reverse(*this);
   md_res.force_evals = 1;
   launch_thermo(*this, 0, S.rec.p + S.n_rec++, S.mass_atom.p, S.ke.p);
   md_step = 0;
@@ -777,11 +776,6 @@ void Engine::md_steps(int64_t k) {
     phase_end();
     ++md_res.staleness_checks;
     evaluate();
-    if (dist) {
-      phase_begin(6);
-      dist_halo_reverse(*this);
-      phase_end();
-    }
     ++md_res.force_evals;
     phase_begin(5);
     launch_kick(*this, half);

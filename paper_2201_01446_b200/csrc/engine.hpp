@@ -192,10 +192,9 @@ struct Engine {
   std::vector<uint8_t> ck_ghost; // [n_chunks] 1 = some centre of the chunk has a ghost neighbour
   std::vector<int> ck_order;     // evaluation order: interior chunks first
   cudaStream_t st_comm = nullptr;
-  cudaEvent_t ev_kd = nullptr, ev_halo = nullptr, ev_gf = nullptr, ev_rx = nullptr;
+  cudaEvent_t ev_kd = nullptr, ev_halo = nullptr;
   bool halo_overlap = std::getenv("DPB_NO_HALO_OVERLAP") == nullptr;
   bool halo_pending = false; // forward halo in flight on st_comm (ev_halo marks its end)
-  bool rev_sent = false;     // reverse halo in flight on st_comm (ev_rx marks its end)
   void classify_chunks();
   void plan_chunks();
   void apply_plan();
@@ -285,6 +284,10 @@ struct Engine {
   } scratch;
 
   Dist* dist = nullptr; // non-null when this handle is one rank of a domain-decomposed run
+  // decomposed runs: local index -> global id and global id -> local index (-1), so the list rows
+  // are in the single-GPU (global id) order; null on one GPU
+  const int32_t* gid_of = nullptr;
+  const int32_t* local_of = nullptr;
   void md_upload_atoms(const double* vel_local);
 
   // lifecycle
@@ -367,9 +370,7 @@ void dist_md_begin(Engine& E, int64_t N, const double* pos, const double* vel, c
                    const double* box, const uint8_t* pbc, const dp_md_config* cfg);
 void dist_rebuild(Engine& E);
 void dist_halo_forward(Engine& E);
-void dist_halo_reverse(Engine& E);
-void dist_reverse_send(Engine& E);
-bool dist_ghost_list(Engine& E, const int32_t** list, int64_t* n, double** send);
+void dist_exchange_g(Engine& E, const int32_t** rslot, const double** grecv);
 void dist_allreduce_sum(Engine& E, double* dev, int count);
 void dist_agree_err(Engine& E); // err := max over ranks
 int64_t dist_n_total(const Engine& E);

@@ -33,22 +33,14 @@ __global__ void __launch_bounds__(256, FORCES_MINB) k_forces(int n, DevCell c, c
                                                 const int64_t* __restrict__ realoff,
                                                 const double* __restrict__ g,
                                                 double* __restrict__ f, double* __restrict__ vpart,
-                                                const uint8_t* __restrict__ center, int only,
-                                                const int32_t* __restrict__ list, int64_t nlist,
-                                                double* __restrict__ packed) {
+                                                const uint8_t* __restrict__ center,
+                                                const int32_t* __restrict__ rslot,
+                                                const double* __restrict__ grecv) {
   const int lane = threadIdx.x & 31;
   const int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5);
-  int i;
-  if (list) {
-    // the atoms of `list` (a decomposed run's ghosts, in reverse-halo order): their partials
-    // are also written packed, as the send buffer of the reverse halo
-    if (w >= nlist) return;
-    i = list[w];
-  } else {
-    if (w >= n) return;
-    i = static_cast<int>(w);
-    if (only == 2 && !center[i]) return; // centres only (the ghosts were done from the list)
-  }
+  if (w >= n) return;
+  const int i = static_cast<int>(w);
+  if (!center[i]) return; // ghosts of a decomposed run: their owners compute their forces
   double3 ri;
   if (VIR) ri = ld_pos(pos, i);
   constexpr int NACC = VIR ? 15 : 6;
@@ -100,6 +92,15 @@ __global__ void __launch_bounds__(256, FORCES_MINB) k_forces(int n, DevCell c, c
         gr[1] = gj[1];
         gr[2] = gj[2];
       }
+      if (rslot && !center[j]) {
+        // ghost neighbour: g(j -> i) was computed by j's owner and received in the pair halo
+        // (NaN: that pair is not real from j's side)
+        const double* gj = grecv + 3 * static_cast<int64_t>(rslot[e]);
+        gr[0] = gj[0];
+        gr[1] = gj[1];
+        gr[2] = gj[2];
+        fr = !isnan(gr[0]);
+      }
     }
     const unsigned mo = __ballot_sync(0xffffffffu, fo);
     const unsigned mr = __ballot_sync(0xffffffffu, fr);
@@ -142,9 +143,6 @@ __global__ void __launch_bounds__(256, FORCES_MINB) k_forces(int n, DevCell c, c
   if (lane == 0) {
 #pragma unroll
     for (int x = 0; x < 3; ++x) f[3 * i + x] = acc[x] - acc[3 + x];
-    if (packed)
-#pragma unroll
-      for (int x = 0; x < 3; ++x) packed[3 * w + x] = acc[x] - acc[3 + x];
     if (VIR)
 #pragma unroll
       for (int k = 0; k < 9; ++k) vpart[9 * static_cast<int64_t>(i) + k] = acc[(6 + k) % NACC];
@@ -302,27 +300,18 @@ void Engine::zero_ghost_vpart() {
 void Engine::launch_forces() {
   const int N = static_cast<int>(n);
   forces.ensure(3 * n);
-  int64_t ng = 0;
-  const int32_t* glist = nullptr;
-  double* gsend = nullptr;
   // the exact path has no per-real records: its virial is formed here from the re-evaluated d
   auto kf = virial_in_forces ? k_forces<true> : k_forces<false>;
-  if (dist && halo_overlap && dist_ghost_list(*this, &glist, &ng, &gsend) && ng == n - n_centers) {
-    // ghost partials first, written straight into the reverse-halo send buffer and sent on
-    // st_comm while the owned atoms' forces are computed
-    kf<<<std::max(1, ceil_div(ng, 8)), 256, 0, stream>>>(N, cell, pos4.p, row_off.p, keys.p, rev.p, ridx.p,
-                                                         realoff.p, g.p, forces.p, vpart.p, center.p, 1, glist, ng,
-                                                         gsend);
-    dist_reverse_send(*this);
-    // the owned atoms are the local range [0, n_centers) (dist.cu local order)
-    kf<<<ceil_div(n_centers, 8), 256, 0, stream>>>(N, cell, pos4.p, row_off.p, keys.p, rev.p, ridx.p, realoff.p,
-                                                    g.p, forces.p, vpart.p, center.p, 2, nullptr, 0, nullptr);
-    launches += 2;
-  } else {
-    kf<<<ceil_div(N, 8), 256, 0, stream>>>(N, cell, pos4.p, row_off.p, keys.p, rev.p, ridx.p, realoff.p, g.p,
-                                            forces.p, vpart.p, center.p, 0, nullptr, 0, nullptr);
-    ++launches;
+  const int32_t* rslot = nullptr;
+  const double* grecv = nullptr;
+  if (dist) {
+    if (virial_in_forces) throw InputErr("the exact path is single-GPU");
+    dist_exchange_g(*this, &rslot, &grecv); // owned atoms are the local range [0, n_centers)
   }
+  const int nf = dist ? static_cast<int>(n_centers) : N;
+  kf<<<ceil_div(nf, 8), 256, 0, stream>>>(nf, cell, pos4.p, row_off.p, keys.p, rev.p, ridx.p, realoff.p, g.p,
+                                          forces.p, vpart.p, center.p, rslot, grecv);
+  ++launches;
   if (n_centers < n && !virial_in_forces) zero_ghost_vpart();
   // energy (1 column) then virial (9 columns) with fixed-order tree reductions
   red.ensure(RED_BLOCKS * 10 + 64);

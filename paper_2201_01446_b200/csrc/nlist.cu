@@ -85,7 +85,8 @@ __global__ void __launch_bounds__(256) k_nlist_warp(NlParams p, const double4* _
                                                     const int* __restrict__ bin_of, const int* __restrict__ bin_start,
                                                     const int* __restrict__ bin_atoms, int64_t* __restrict__ row_len,
                                                     const int64_t* __restrict__ row_off, uint64_t* __restrict__ keys,
-                                                    unsigned long long* __restrict__ n_inner, int* err, int64_t e_cap) {
+                                                    unsigned long long* __restrict__ n_inner, int* err, int64_t e_cap,
+                                                    const int32_t* __restrict__ gid) {
   const int lane = threadIdx.x & 31;
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (i >= p.n) return;
@@ -127,7 +128,9 @@ __global__ void __launch_bounds__(256) k_nlist_warp(NlParams p, const double4* _
           double3 ra, rb;
           if (idx < qe) {
             j = bin_atoms[idx];
-            i_low = i <= j;
+            // every pair is evaluated once from its lower GLOBAL index (a decomposed run's
+            // local order differs), so all ranks and one GPU accept exactly the same entries
+            i_low = gid ? gid[i] <= gid[j] : i <= j;
             a = i_low ? i : j;
             b = i_low ? j : i;
             const double3 rj = ld_pos(pos, j);
@@ -200,17 +203,28 @@ __global__ void k_mark_ghost_rows(int n, const uint8_t* __restrict__ center, con
   for (int64_t e = row_off[i] + (threadIdx.x & 31); e < row_off[i + 1]; e += 32) ridx[e] = -1;
 }
 
+// Neighbour field of every key through a map (local index <-> global id of a decomposed run).
+__global__ void k_keys_map(const int64_t* __restrict__ row_off, int n, uint64_t* __restrict__ keys,
+                           const int32_t* __restrict__ map) {
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (e >= row_off[n]) return;
+  const uint64_t k = keys[e];
+  keys[e] = with_key_j(k, map[key_j(k)]);
+}
+
 // Reverse entry of every list entry, warp per row: the position of (j -> i, -s) inside row j
-// (rows are at most 8192 long, so 16 bits; the entry is row_off[j] + rev[e]).
+// (rows are at most 8192 long, so 16 bits; the entry is row_off[j] + rev[e]). Decomposed runs
+// sort their rows with global ids in the keys (gid/lidx map them), like one GPU does.
 __global__ void k_reverse_rows(const int64_t* __restrict__ row_off, int n, const uint64_t* __restrict__ keys,
-                               const int32_t* __restrict__ types, uint16_t* __restrict__ rev, int* err) {
+                               const int32_t* __restrict__ types, uint16_t* __restrict__ rev, int* err,
+                               const int32_t* __restrict__ gid, const int32_t* __restrict__ lidx) {
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (i >= n) return;
   const int ti = types[i];
   for (int64_t e = row_off[i] + (threadIdx.x & 31); e < row_off[i + 1]; e += 32) {
     const uint64_t k = keys[e];
-    const int j = key_j(k);
-    const uint64_t want = reverse_key(k, ti, i);
+    const int j = lidx ? lidx[key_j(k)] : key_j(k);
+    const uint64_t want = reverse_key(k, ti, gid ? gid[i] : i);
     const int64_t r0 = row_off[j], r1 = row_off[j + 1];
     int64_t lo = r0, hi = r1;
     while (lo < hi) {
@@ -330,7 +344,8 @@ void Engine::launch_nlist(double cutoff) {
   DPB_CUDA(cudaMemsetAsync(inner_cnt.p, 0, sizeof(unsigned long long), stream));
   p.rc2 = r_cut * r_cut;
   k_nlist_warp<false><<<ceil_div(static_cast<int64_t>(N) * 32, 256), 256, 0, stream>>>(
-      p, pos4.p, frac.p, types.p, bin_of.p, bin_start.p, bin_atoms.p, lens.p, nullptr, nullptr, inner_cnt.p, err.p, 0);
+      p, pos4.p, frac.p, types.p, bin_of.p, bin_start.p, bin_atoms.p, lens.p, nullptr, nullptr, inner_cnt.p, err.p, 0,
+      gid_of);
   ++launches;
   DPB_CUDA(cudaMemsetAsync(lens.p + n, 0, sizeof(int64_t), stream));
   size_t tmp2 = 0;
@@ -363,7 +378,7 @@ void Engine::launch_nlist(double cutoff) {
   keys.ensure(e_cap + 1);
   k_nlist_warp<true><<<ceil_div(static_cast<int64_t>(N) * 32, 256), 256, 0, stream>>>(
       p, pos4.p, frac.p, types.p, bin_of.p, bin_start.p, bin_atoms.p, nullptr, row_off.p, keys.p, nullptr, err.p,
-      e_cap);
+      e_cap, gid_of);
   ++launches;
   finish_list(cutoff);
 }
@@ -385,12 +400,22 @@ void Engine::finish_list(double cutoff) {
   if (cap > 8192) throw NumErr("neighbour row longer than 8192 entries");
   rev.ensure(e_cap + 1);
   ridx.ensure(e_cap + 1);
+  // decomposed runs: rows sorted in global-id order (the single-GPU order), then back to local j
+  const int64_t ne = n_entries > 0 ? n_entries : 1;
+  if (gid_of) {
+    k_keys_map<<<ceil_div(ne, 256), 256, 0, stream>>>(row_off.p, N, keys.p, gid_of);
+    ++launches;
+  }
   smem_optin(k_sort_rows, cap * sizeof(uint64_t));
   k_sort_rows<<<N, 256, cap * sizeof(uint64_t), stream>>>(N, row_off.p, keys.p, cap, err.p);
   ++launches;
   k_reverse_rows<<<ceil_div(static_cast<int64_t>(N) * 32, 256), 256, 0, stream>>>(row_off.p, N, keys.p, types.p,
-                                                                                  rev.p, err.p);
+                                                                                  rev.p, err.p, gid_of, local_of);
   ++launches;
+  if (gid_of) {
+    k_keys_map<<<ceil_div(ne, 256), 256, 0, stream>>>(row_off.p, N, keys.p, local_of);
+    ++launches;
+  }
   if (n_centers < n) {
     k_mark_ghost_rows<<<ceil_div(N, 8), 256, 0, stream>>>(N, center.p, row_off.p, ridx.p);
     ++launches;
