@@ -416,6 +416,7 @@ __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
         const double* Wg = w.W + gg * 24;
         acc_t c[6][F];
         load_c(g0 + gg, c);
+
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
 #pragma unroll
