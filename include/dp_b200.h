@@ -36,7 +36,8 @@ extern "C" {
 #define DP_RUNTIME_ERROR 3
 
 /* Fitting net of one center type (model.hpp:22-36). Layer k maps widths[k] -> widths[k+1],
- * weights row-major in x out; identity shortcut when in == out. */
+ * weights row-major in x out; identity shortcut when in == out. Each type's net has its own
+ * n_layers and widths (model.cpp:30-47 validates the nets one by one). */
 typedef struct {
   int n_layers;
   const int* widths;        /* n_layers + 1 */
@@ -105,7 +106,10 @@ typedef struct dp_handle dp_handle;
 
 /* ---- evaluation handle -------------------------------------------------------------------- */
 
-/* precision: 0 = FP64 (parity mode, 1e-10), 1 = mixed (FP32 tabulate, TF32 fitting, tanh table). */
+/* precision: 0 = FP64 (parity mode, 1e-10); 1 = mixed (1e-5): FP32 coefficient contraction in
+ * the tabulation, tcgen05 3xTF32 fitting GEMMs with FP64 accumulation of short K chains in the
+ * forward layers, the reference's tanh table. Fitting nets may differ in depth and widths per
+ * centre type (model.cpp:30-47) in FP64 mode; mixed mode needs one shape for all types. */
 int dp_create(const dp_model_desc* model, const dp_table_desc* tables, int device, int precision,
               dp_handle** out);
 int dp_destroy(dp_handle* h);
@@ -186,8 +190,9 @@ int dp_md_run(dp_handle* h, int64_t n, double* pos, double* vel, const int32_t* 
               dp_thermo* thermo, int64_t thermo_cap, int64_t* n_thermo, dp_md_result* result);
 
 /* Split form of dp_md_run for benchmarking with device-resident state: begin uploads and
- * evaluates step 0, step advances k Verlet steps asynchronously on the handle's stream,
- * end synchronizes and copies state back. */
+ * evaluates step 0, step advances k Verlet steps asynchronously on the handle's stream (the host
+ * waits once per list rebuild, to size the new list), end synchronizes and copies state back.
+ * Stepping past cfg->n_steps is an InputError. */
 int dp_md_begin(dp_handle* h, int64_t n, const double* pos, const double* vel,
                 const int32_t* types, const double box[9], const uint8_t pbc[3],
                 const dp_md_config* cfg);
@@ -197,7 +202,9 @@ int dp_md_end(dp_handle* h, double* pos, double* vel, dp_thermo* thermo, int64_t
 
 /* ---- multi-GPU: one process (one handle) per GPU, spatial domain decomposition ----------------
  * Slab partition with partition_domain semantics (domain.cpp:21-82); ghost positions go to
- * neighbours and ghost force partials come back through NCCL send/recv every step. Rank 0 creates
+ * neighbours and the pair gradients of ghost-adjacent pairs come back through NCCL send/recv
+ * every step, so forces, positions and velocities are bitwise independent of the number of GPUs
+ * (thermo sums are reduced across ranks and agree to rounding). Rank 0 creates
  * the NCCL id with dp_nccl_unique_id (128 bytes) and shares it (e.g. torch.distributed); every rank
  * then calls dp_dist_init on its handle. After that dp_md_begin takes the GLOBAL initial state on
  * every rank and dp_md_end returns the global final state on every rank; thermo records hold
@@ -218,10 +225,11 @@ int dp_dist_init(dp_handle* h, int rank, int world, const void* nccl_id);
 int dp_set_pipeline(dp_handle* h, int enable);
 
 /* Largest number of centres evaluated per chunk (a multiple of 128; 0 = default 131,072 or the
- * DPB_CHUNK environment variable). The per-step working set (descriptors, activations,
- * per-entry tabulate arrays) is sized for two chunks, so systems of tens of millions of atoms
- * fit one GPU; results are bitwise independent of the chunk size. One centre type only (systems
- * with several centre types are evaluated as one chunk). */
+ * DPB_CHUNK environment variable). The per-step working set (descriptors, activations, per-real
+ * records) is sized for two chunks; the whole-system state is 12 bytes per neighbour-list entry
+ * plus 24 bytes per real pair, so the paper's 13.5 M-atom copper system fits one B200 (157 GB).
+ * Results are bitwise independent of the chunk size. One centre type only (systems with several
+ * centre types are evaluated as one chunk). */
 int dp_set_chunk_size(dp_handle* h, int64_t centres);
 
 /* cudaStream_t of the handle (for CUDA-event timing on the launching stream). */

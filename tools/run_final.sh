@@ -2,9 +2,10 @@
 # into profiles/ by hand. Every number comes from a run without a profiler, except the ncu files.
 set -x
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/microbench/fp64_peak tools/microbench/fp64_peak.cu
-(nvidia-smi --query-gpu=timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active --format=csv -lms 200 > gpurun_out/r02f_fp64_peak_clocks.csv &) ; sleep 1
+nvidia-smi --query-gpu=timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active --format=csv -lms 200 > gpurun_out/r02f_fp64_peak_clocks.csv & SMI=$!
+sleep 1
 ./tools/microbench/fp64_peak > gpurun_out/r02f_fp64_peak.log 2>&1; ./tools/microbench/fp64_peak >> gpurun_out/r02f_fp64_peak.log 2>&1
-sleep 1; kill $(pgrep -n nvidia-smi) 2>/dev/null
+sleep 1; kill $SMI 2>/dev/null
 timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/r02f_pytest_gpu.log 2>&1; echo pytest rc=$?
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r02f_smoke.log 2>&1; echo smoke rc=$?
 timeout 400 python bench.py > gpurun_out/r02f_c2_n1.json 2> gpurun_out/r02f_c2_n1.err; echo c2n1 rc=$?
