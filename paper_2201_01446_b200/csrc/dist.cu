@@ -77,6 +77,10 @@ struct Dist {
   DevBuf<int64_t> d_gcnt;    // scratch counts
   DevBuf<double> gsend, grecv;
   std::vector<int64_t> gsoff, groff; // slot offsets per peer (send / receive)
+  // owned atoms without / with a ghost neighbour: the first set's forces run while the pair
+  // halo is in flight
+  DevBuf<int32_t> f_inner, f_bound, d_tflag, d_tscan;
+  int64_t n_inner = 0, n_bound = 0;
   DevBuf<unsigned char> d_tmp;
   bool host_global_valid = true; // gpos/gvel (host) reflect the last gather
 };
@@ -261,6 +265,26 @@ __global__ void k_pack_pair_g(int64_t m, const int32_t* __restrict__ list, const
     }
     slot += __popc(mk);
   }
+}
+
+// Owned atom i touches a ghost (some neighbour of its row is not a centre here): flag 1.
+__global__ void k_touch_ghost(int64_t n_own, const int64_t* __restrict__ row_off, const uint64_t* __restrict__ keys,
+                              const uint8_t* __restrict__ center, int32_t* __restrict__ flag) {
+  const int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= n_own) return;
+  bool t = false;
+  for (int64_t e = row_off[i] + lane; e < row_off[i + 1]; e += 32) t |= center[key_j(keys[e])] == 0;
+  t = __any_sync(0xffffffffu, t);
+  if (lane == 0) flag[i] = t ? 1 : 0;
+}
+
+__global__ void k_split_atoms(int64_t n_own, const int32_t* __restrict__ flag, const int32_t* __restrict__ scan,
+                              int32_t* __restrict__ inner, int32_t* __restrict__ bound) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n_own) return;
+  if (flag[i]) bound[scan[i]] = static_cast<int32_t>(i);
+  else inner[i - scan[i]] = static_cast<int32_t>(i);
 }
 
 // Chunk classification: flag[k] = 1 when a centre of chunk k (atoms [cka[k], cka[k+1])) has a
@@ -654,9 +678,24 @@ void pair_plan(Engine& E) {
   DPB_CUDA(cudaStreamSynchronize(st));
   D.gsoff.assign(tot.begin(), tot.begin() + W + 1);
   D.groff.assign(tot.begin() + W + 1, tot.end());
+  // interior / boundary owned atoms (local owned range [0, n_own))
+  const int64_t no_ = E.n_centers;
+  D.d_tflag.ensure(no_ + 1);
+  D.d_tscan.ensure(no_ + 1);
+  D.f_inner.ensure(no_ + 1);
+  D.f_bound.ensure(no_ + 1);
+  DPB_CUDA(cudaMemsetAsync(D.d_tflag.p + no_, 0, sizeof(int32_t), st));
+  if (no_) k_touch_ghost<<<ceil_div(no_ * 32, 256), 256, 0, st>>>(no_, E.row_off.p, E.keys.p, E.center.p, D.d_tflag.p);
+  excl_scan(D, D.d_tflag.p, D.d_tscan.p, no_ + 1, st);
+  if (no_) k_split_atoms<<<ceil_div(no_, 256), 256, 0, st>>>(no_, D.d_tflag.p, D.d_tscan.p, D.f_inner.p, D.f_bound.p);
+  int32_t nb = 0;
+  DPB_CUDA(cudaMemcpyAsync(&nb, D.d_tscan.p + no_, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   D.gsend.ensure(3 * D.gsoff[W] + 3);
   D.grecv.ensure(3 * D.groff[W] + 3);
-  E.launches += 2 + 2 * W;
+  DPB_CUDA(cudaStreamSynchronize(st));
+  D.n_bound = nb;
+  D.n_inner = no_ - nb;
+  E.launches += 4 + 2 * W;
 }
 
 // Build the local system for this rank from the global state and upload it.
@@ -822,25 +861,39 @@ void dist_halo_forward(Engine& E) {
 // Pair-gradient halo (every evaluation, before the force kernel): pack the reverse gradients of
 // my ghosts' rows, exchange them with the peers (grouped send/recv, slot counts fixed at the
 // rebuild), and hand the receive buffer and slot map to the force kernel.
-void dist_exchange_g(Engine& E, const int32_t** rslot, const double** grecv) {
+// With overlap (default) the pack and the exchange run on the communication stream, ordered after
+// the evaluation by ev_kd; ev_halo marks the received gradients. Returns the interior / boundary
+// owned-atom lists for the split force launch.
+void dist_exchange_g(Engine& E, const int32_t** rslot, const double** grecv, const int32_t** inner,
+                     int64_t* n_inner, const int32_t** bound, int64_t* n_bound) {
   Dist& D = *E.dist;
   const int W = D.world;
   const int64_t ng = D.roff[W];
+  cudaStream_t st = E.stream;
+  if (E.halo_overlap) {
+    DPB_CUDA(cudaEventRecord(E.ev_kd, E.stream));
+    DPB_CUDA(cudaStreamWaitEvent(E.st_comm, E.ev_kd, 0));
+    st = E.st_comm;
+  }
   if (ng)
-    k_pack_pair_g<<<ceil_div(ng * 32, 256), 256, 0, E.stream>>>(ng, D.ridx.p, E.row_off.p, E.keys.p, E.rev.p,
-                                                               E.ridx.p, E.realoff.p, E.center.p, E.g.p,
-                                                               D.gs_base.p, D.gsend.p);
+    k_pack_pair_g<<<ceil_div(ng * 32, 256), 256, 0, st>>>(ng, D.ridx.p, E.row_off.p, E.keys.p, E.rev.p, E.ridx.p,
+                                                         E.realoff.p, E.center.p, E.g.p, D.gs_base.p, D.gsend.p);
   DPB_NCCL(ncclGroupStart());
   for (int p = 0; p < W; ++p) {
     const int64_t so = D.gsoff[p], sc = D.gsoff[p + 1] - so;
     const int64_t ro = D.groff[p], rc = D.groff[p + 1] - ro;
-    if (sc > 0) DPB_NCCL(ncclSend(D.gsend.p + 3 * so, 3 * sc, ncclDouble, p, D.comm, E.stream));
-    if (rc > 0) DPB_NCCL(ncclRecv(D.grecv.p + 3 * ro, 3 * rc, ncclDouble, p, D.comm, E.stream));
+    if (sc > 0) DPB_NCCL(ncclSend(D.gsend.p + 3 * so, 3 * sc, ncclDouble, p, D.comm, st));
+    if (rc > 0) DPB_NCCL(ncclRecv(D.grecv.p + 3 * ro, 3 * rc, ncclDouble, p, D.comm, st));
   }
   DPB_NCCL(ncclGroupEnd());
+  if (E.halo_overlap) DPB_CUDA(cudaEventRecord(E.ev_halo, st));
   E.launches += 1;
   *rslot = D.rslot.p;
   *grecv = D.grecv.p;
+  *inner = D.f_inner.p;
+  *n_inner = D.n_inner;
+  *bound = D.f_bound.p;
+  *n_bound = D.n_bound;
 }
 
 // All-gather of the owned (id, x, v) into the global arrays on every rank (device resident).

@@ -370,7 +370,8 @@ void dist_md_begin(Engine& E, int64_t N, const double* pos, const double* vel, c
                    const double* box, const uint8_t* pbc, const dp_md_config* cfg);
 void dist_rebuild(Engine& E);
 void dist_halo_forward(Engine& E);
-void dist_exchange_g(Engine& E, const int32_t** rslot, const double** grecv);
+void dist_exchange_g(Engine& E, const int32_t** rslot, const double** grecv, const int32_t** inner,
+                     int64_t* n_inner, const int32_t** bound, int64_t* n_bound);
 void dist_allreduce_sum(Engine& E, double* dev, int count);
 void dist_agree_err(Engine& E); // err := max over ranks
 int64_t dist_n_total(const Engine& E);

@@ -35,11 +35,12 @@ __global__ void __launch_bounds__(256, FORCES_MINB) k_forces(int n, DevCell c, c
                                                 double* __restrict__ f, double* __restrict__ vpart,
                                                 const uint8_t* __restrict__ center,
                                                 const int32_t* __restrict__ rslot,
-                                                const double* __restrict__ grecv) {
+                                                const double* __restrict__ grecv,
+                                                const int32_t* __restrict__ list) {
   const int lane = threadIdx.x & 31;
   const int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (w >= n) return;
-  const int i = static_cast<int>(w);
+  const int i = list ? list[w] : static_cast<int>(w); // list: a subset of the atoms (decomposed runs)
   if (!center[i]) return; // ghosts of a decomposed run: their owners compute their forces
   double3 ri;
   if (VIR) ri = ld_pos(pos, i);
@@ -302,16 +303,27 @@ void Engine::launch_forces() {
   forces.ensure(3 * n);
   // the exact path has no per-real records: its virial is formed here from the re-evaluated d
   auto kf = virial_in_forces ? k_forces<true> : k_forces<false>;
-  const int32_t* rslot = nullptr;
-  const double* grecv = nullptr;
   if (dist) {
     if (virial_in_forces) throw InputErr("the exact path is single-GPU");
-    dist_exchange_g(*this, &rslot, &grecv); // owned atoms are the local range [0, n_centers)
+    // pair halo in flight (communication stream) while the owned atoms without ghost neighbours
+    // get their forces; the boundary atoms wait for the received gradients
+    const int32_t *rslot = nullptr, *inner = nullptr, *bound = nullptr;
+    const double* grecv = nullptr;
+    int64_t ni = 0, nb = 0;
+    dist_exchange_g(*this, &rslot, &grecv, &inner, &ni, &bound, &nb);
+    if (ni)
+      kf<<<ceil_div(ni, 8), 256, 0, stream>>>(static_cast<int>(ni), cell, pos4.p, row_off.p, keys.p, rev.p, ridx.p,
+                                               realoff.p, g.p, forces.p, vpart.p, center.p, rslot, grecv, inner);
+    if (halo_overlap) DPB_CUDA(cudaStreamWaitEvent(stream, ev_halo, 0));
+    if (nb)
+      kf<<<ceil_div(nb, 8), 256, 0, stream>>>(static_cast<int>(nb), cell, pos4.p, row_off.p, keys.p, rev.p, ridx.p,
+                                               realoff.p, g.p, forces.p, vpart.p, center.p, rslot, grecv, bound);
+    launches += 2;
+  } else {
+    kf<<<ceil_div(N, 8), 256, 0, stream>>>(N, cell, pos4.p, row_off.p, keys.p, rev.p, ridx.p, realoff.p, g.p,
+                                            forces.p, vpart.p, center.p, nullptr, nullptr, nullptr);
+    ++launches;
   }
-  const int nf = dist ? static_cast<int>(n_centers) : N;
-  kf<<<ceil_div(nf, 8), 256, 0, stream>>>(nf, cell, pos4.p, row_off.p, keys.p, rev.p, ridx.p, realoff.p, g.p,
-                                          forces.p, vpart.p, center.p, rslot, grecv);
-  ++launches;
   if (n_centers < n && !virial_in_forces) zero_ghost_vpart();
   // energy (1 column) then virial (9 columns) with fixed-order tree reductions
   red.ensure(RED_BLOCKS * 10 + 64);
