@@ -160,7 +160,7 @@ struct Engine {
   DevBuf<int16_t> ridx; // per step: list-order rank of a real entry within its row, -1 otherwise
   DevBuf<unsigned long long> inner_cnt; // list build: entries inside r_cut (pair-gradient capacity)
   int64_t g_cap = 0;    // compact pair-gradient capacity (pairs)
-  void set_gcap(int64_t pairs);
+  void set_gcap(int64_t need, int64_t want);
   DevBuf<int32_t> bin_of, bin_start, bin_atoms, bin_fill;
   DevBuf<double> frac;
   DevBuf<double> ref_pos;

@@ -374,7 +374,7 @@ void Engine::launch_nlist(double cutoff) {
   if (rc > row_cap) row_cap = rc;
   // pair gradients are stored for real pairs only (compact, realoff[i] + rank): the pairs inside
   // r_cut at build time + 12.5 % for their drift until the next rebuild (checked on the device)
-  set_gcap(static_cast<int64_t>(inner) + static_cast<int64_t>(inner / 8) + 4096);
+  set_gcap(static_cast<int64_t>(inner), static_cast<int64_t>(inner) + static_cast<int64_t>(inner / 8) + 4096);
   keys.ensure(e_cap + 1);
   k_nlist_warp<true><<<ceil_div(static_cast<int64_t>(N) * 32, 256), 256, 0, stream>>>(
       p, pos4.p, frac.p, types.p, bin_of.p, bin_start.p, bin_atoms.p, nullptr, row_off.p, keys.p, nullptr, err.p,
@@ -383,9 +383,11 @@ void Engine::launch_nlist(double cutoff) {
   finish_list(cutoff);
 }
 
-void Engine::set_gcap(int64_t want) {
+// Grow only when the pairs inside r_cut at this build exceed the capacity (a rebuild in an MD
+// run must not reallocate tens of GB for a 0.1 % change); shrink when far too large.
+void Engine::set_gcap(int64_t need, int64_t want) {
   want = std::min<int64_t>(want, e_cap);
-  if (want > g_cap || want < g_cap / 2) {
+  if (need > g_cap || want < g_cap / 2) {
     g.release();
     g.ensure(3 * want + 3);
     g_cap = static_cast<int64_t>((g.n - 3) / 3); // the allocation's growth slack included
@@ -456,7 +458,7 @@ void Engine::import_list(const int64_t* off, const int32_t* jj, const int32_t* s
   int rc = 2;
   while (rc < mx + mx / 8) rc <<= 1;
   row_cap = std::max(row_cap, rc);
-  set_gcap(total + 1);
+  set_gcap(total + 1, total + 1);
   row_off.ensure(n + 1);
   keys.ensure(e_cap + 1);
   DPB_CUDA(cudaMemcpyAsync(row_off.p, off, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, stream));

@@ -413,17 +413,19 @@ __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
       __syncwarp();
       const int gn = min(GB, G - g0);
       for (int gg = 0; gg < gn; ++gg) {
-        const double* Wg = w.W + gg * 24;
+        const double2* Wg2 = reinterpret_cast<const double2*>(w.W + gg * 24); // 16-byte broadcasts
         acc_t c[6][F];
         load_c(g0 + gg, c);
-
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
 #pragma unroll
-          for (int mm = 0; mm < 6; ++mm) {
-            const acc_t wa = static_cast<acc_t>(Wg[a * 6 + mm]);
+          for (int mp = 0; mp < 3; ++mp) {
+            const double2 wv = Wg2[a * 3 + mp];
+            const acc_t w0 = static_cast<acc_t>(wv.x), w1 = static_cast<acc_t>(wv.y);
 #pragma unroll
-            for (int q = 0; q < F; ++q) tacc[a][q] += wa * c[mm][q];
+            for (int q = 0; q < F; ++q) tacc[a][q] += w0 * c[2 * mp][q];
+#pragma unroll
+            for (int q = 0; q < F; ++q) tacc[a][q] += w1 * c[2 * mp + 1][q];
           }
         }
       }
