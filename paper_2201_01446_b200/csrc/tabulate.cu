@@ -502,7 +502,7 @@ __device__ __forceinline__ double rs16(double* v, int lane) {
 // dT = adjoint of D = T<^T T (contract.hpp:21-38): dT[a][p] = sum_{q<mlt} dD[q][p] T[a][q]
 // + [p < mlt] sum_r dD[p][r] T[a][r]. Written to dTg[i][4][Mp] for the projection kernels.
 template <int F>
-__global__ void __launch_bounds__(256, 2) k_tab_dT(TabParams p, double* __restrict__ dTg) {
+__global__ void __launch_bounds__(256, 1) k_tab_dT(TabParams p, double* __restrict__ dTg) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
@@ -534,45 +534,53 @@ __global__ void __launch_bounds__(256, 2) k_tab_dT(TabParams p, double* __restri
     const double* dDrow = p.dD + static_cast<size_t>(slot < 0 ? 0 : slot) * p.K0p;
     const bool fon = f0 < p.M && slot >= 0;
     const bool vec = ((p.M | p.K0p) & 1) == 0; // 16-byte aligned dD pairs
-    for (int q0 = 0; q0 < p.mlt; q0 += 4) {
-      double part[16];
+    // the dD rows of up to QB features q are loaded together (all 16 rows of the Cu model at F = 4:
+    // 16 KB in flight per warp, so HBM sees enough requests), then contracted in ascending q
+    constexpr int QB = (64 / F) < 16 ? (64 / F) : 16;
+    for (int q0 = 0; q0 < p.mlt; q0 += QB) {
+      double dq[QB][F];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) part[k] = 0.0;
-#pragma unroll
-      for (int ql = 0; ql < 4; ++ql) {
+      for (int ql = 0; ql < QB; ++ql) {
         const int qq = q0 + ql;
-        if (qq < p.mlt) {
-          double dq[F];
-          if constexpr (F % 2 == 0) {
-            if (vec) {
+        const bool on = fon && qq < p.mlt;
+        if constexpr (F % 2 == 0) {
+          if (vec) {
 #pragma unroll
-              for (int q = 0; q < F; q += 2) {
-                const double2 v = fon ? *reinterpret_cast<const double2*>(dDrow + qq * p.M + f0 + q)
-                                      : make_double2(0.0, 0.0);
-                dq[q] = v.x;
-                dq[q + 1] = v.y;
-              }
-            } else {
-#pragma unroll
-              for (int q = 0; q < F; ++q) dq[q] = fon ? dDrow[qq * p.M + f0 + q] : 0.0;
+            for (int q = 0; q < F; q += 2) {
+              const double2 v = on ? __ldg(reinterpret_cast<const double2*>(dDrow + qq * p.M + f0 + q))
+                                   : make_double2(0.0, 0.0);
+              dq[ql][q] = v.x;
+              dq[ql][q + 1] = v.y;
             }
-          } else {
-#pragma unroll
-            for (int q = 0; q < F; ++q) dq[q] = fon ? dDrow[qq * p.M + f0 + q] : 0.0;
+            continue;
           }
+        }
 #pragma unroll
-          for (int a = 0; a < 4; ++a) {
-            const double ta = ts[a * p.Mp + qq];
+        for (int q = 0; q < F; ++q) dq[ql][q] = on ? dDrow[qq * p.M + f0 + q] : 0.0;
+      }
 #pragma unroll
-            for (int q = 0; q < F; ++q) {
-              dT[a][q] += dq[q] * ta;
-              part[ql * 4 + a] += dq[q] * tv[a][q];
+      for (int qb = 0; qb < QB; qb += 4) {
+        double part[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) part[k] = 0.0;
+#pragma unroll
+        for (int ql = 0; ql < 4; ++ql) {
+          const int qq = q0 + qb + ql;
+          if (qb + ql < QB && qq < p.mlt) {
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+              const double ta = ts[a * p.Mp + qq];
+#pragma unroll
+              for (int q = 0; q < F; ++q) {
+                dT[a][q] += dq[qb + ql][q] * ta;
+                part[ql * 4 + a] += dq[qb + ql][q] * tv[a][q];
+              }
             }
           }
         }
+        const double sv = rs16(part, lane);
+        if (lane < 16 && q0 + qb + (lane >> 2) < p.mlt) S[(q0 + qb + (lane >> 2)) * 4 + (lane & 3)] = sv;
       }
-      const double s = rs16(part, lane);
-      if (lane < 16 && q0 + (lane >> 2) < p.mlt) S[(q0 + (lane >> 2)) * 4 + (lane & 3)] = s;
     }
     __syncwarp();
 #pragma unroll
