@@ -7,7 +7,7 @@
 // quadratic tanh table (tanh_table.cpp:5-21, mixed mode only).
 //
 // Kernels:
-//   k_tc_fwd64  forward layers: 128 x 80 tiles; short TMEM chains (2 K blocks of each segment)
+//   k_tc_fwd64  forward layers: 128 x 80 tiles; short TMEM chains (1 K block of each segment)
 //               drained into FP64 registers by 8 epilogue warps while the next chain runs on the
 //               other TMEM buffer -- the tensor core's FP32 accumulation over the whole 6144-term
 //               first layer biased small total energies by 1e-4 (water preset), this keeps every
@@ -245,7 +245,8 @@ __global__ void __launch_bounds__(192, 2) k_tc_gemm(const __grid_constant__ CUte
 // into FP64 registers while the next one runs, so the FP32 error is bounded per chain and the K
 // reduction itself is FP64. Tile 128 x BN (BN <= 128), one CTA per SM.
 constexpr int F64_ST = 8; // 8 x 26 KB stages: one N=80 stage is only ~90 ns of MMA work
-constexpr int F64_CH = 2; // K blocks per segment per chain (1: 1.5e-6 on water E, 2 measured below 1e-5)
+constexpr int F64_CH = 1; // K blocks per segment per chain: water E 3.1e-6 and 3.26 ms/step at C2
+                          // (2 blocks: 5.3e-6 and 3.31 ms; FP32 hidden layers: 1.1e-5, over 1e-5)
 constexpr int F64_THREADS = 320; // TMA warp, MMA warp, 8 epilogue warps
 
 template <int BN>

@@ -1,5 +1,14 @@
-# Full GPU verification on 4 GPUs: every -m gpu test (incl. 2- and 4-rank), smoke, default bench
+# Final verification on one 4-GPU box (gpurun --gpus 4): every -m gpu test (incl. 2- and 4-rank),
+# smoke, default bench line, reference arm, C2 weak 2/4, C4 strong 2/4, mixed C2, launch list.
 set -x
-timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/verify_pytest.log 2>&1; echo pytest rc=$?
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/verify_smoke.log 2>&1; echo smoke rc=$?
-timeout 400 python bench.py > gpurun_out/verify_bench.log 2>&1; echo bench rc=$?
+timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/r02v_pytest_gpu.log 2>&1; echo pytest rc=$?
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r02v_smoke.log 2>&1; echo smoke rc=$?
+timeout 400 python bench.py > gpurun_out/r02v_c2_n1.json 2> gpurun_out/r02v_c2_n1.err; echo c2n1 rc=$?
+timeout 300 python bench.py --impl reference > gpurun_out/r02v_reference.json 2> gpurun_out/r02v_reference.err; echo ref rc=$?
+timeout 300 python bench.py --precision mixed --no-cpu > gpurun_out/r02v_c2_n1_mixed.json 2> gpurun_out/r02v_mixed.err; echo mixed rc=$?
+for n in 2 4; do timeout 400 python bench.py --gpus $n > gpurun_out/r02v_c2_n$n.json 2> gpurun_out/r02v_c2_n$n.err; echo c2n$n rc=$?; done
+for n in 2 4; do timeout 1500 python bench.py --gpus $n --config c4 --steps 3 --warmup 3 --no-cpu --no-e2e > gpurun_out/r02v_c4_n$n.json 2> gpurun_out/r02v_c4_n$n.err; echo c4n$n rc=$?; done
+BENCH_NO_CLOCKS=1 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/r02v_launches.csv python bench.py --steps 4 --warmup 3 --no-e2e --no-cpu > gpurun_out/r02v_ncu_launch.log 2>&1; echo ncu rc=$?
+python tools/launch_summary.py gpurun_out/r02v_launches.csv > gpurun_out/r02v_launches_summary.txt
+for f in gpurun_out/r02v_*.json; do python -c "import json; d=json.loads(open('$f').read().strip().splitlines()[-1]); print('$f', d.get('n_gpus'), d.get('ms_per_step'), d.get('value'), (d.get('e2e') or {}).get('value'))" 2>/dev/null; done
+tail -3 gpurun_out/r02v_pytest_gpu.log
