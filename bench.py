@@ -339,7 +339,8 @@ def run_ours(args, world, rank, local, dist):
         except Exception:
             peak = 1125.0
             peak_src = "nominal B200 dense TF32 (MEASURED_PEAKS.json unavailable)"
-        kernel = "fitting-net tcgen05 kind::tf32 3xTF32 GEMMs (k_tc_gemm, 6 launches/step)"
+        kernel = ("fitting-net tcgen05 kind::tf32 3xTF32 GEMMs (k_tc_fwd64 forward with FP64-accumulated "
+                  "chains, k_tc_gemm backward; 6 launches per chunk)")
     else:
         achieved = fit_flop_launch / (fit_launch_ms / 1e3) / 1e12
         peak = 37.15
