@@ -98,11 +98,25 @@ __device__ __forceinline__ double norm2_exact(const double* d) {
   return __dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])), __dmul_rn(d[2], d[2]));
 }
 
+// 32-byte vector accesses (sm_100: LDG.E.ENL2.256 / STG.E.ENL2.256): one instruction per lane
+// instead of two 16-byte ones; the address must be 32-byte aligned.
+__device__ __forceinline__ double4 ldg4(const double* p) {
+  double4 v;
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double4 ldc4(const double* p) { // coherent (data written earlier by this kernel)
+  double4 v;
+  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st4(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
 __device__ __forceinline__ double3 ld_pos(const double4* p, int j) {
-  const double2* q = reinterpret_cast<const double2*>(p + j);
-  const double2 a = __ldg(q);
-  const double2 b = __ldg(q + 1);
-  return make_double3(a.x, a.y, b.x);
+  const double4 v = ldg4(reinterpret_cast<const double*>(p + j));
+  return make_double3(v.x, v.y, v.z);
 }
 
 __device__ __forceinline__ void raise_err(int* err, int code) { atomicCAS(err, 0, code); }

@@ -288,11 +288,9 @@ __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
       const int t = real ? bin / p.tn : -1;
       if (real) {
         w.rk[k] = static_cast<uint32_t>(bin);
-        double2* rp = reinterpret_cast<double2*>(recs + static_cast<int64_t>(k) * 8);
-        rp[0] = make_double2(R[0], R[1]);
-        rp[1] = make_double2(R[2], R[3]);
-        rp[2] = make_double2(uu, d[0]);
-        rp[3] = make_double2(d[1], d[2]);
+        double* rp = recs + static_cast<int64_t>(k) * 8;
+        st4(rp, R[0], R[1], R[2], R[3]);
+        st4(rp + 4, uu, d[0], d[1], d[2]);
         kmin = min(kmin, bin);
         kmax = max(kmax, bin);
       }
@@ -351,7 +349,16 @@ __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
       const double* C = reinterpret_cast<const double*>(p.tab) + static_cast<size_t>(w.gb[gidx]) * istride + f0;
 #pragma unroll
       for (int mm = 0; mm < 6; ++mm) {
-        if constexpr (F % 2 == 0) {
+        if constexpr (F % 4 == 0) {
+#pragma unroll
+          for (int q = 0; q < F; q += 4) {
+            const double4 v = ldg4(C + mm * p.Mp + q);
+            cn[mm][q] = static_cast<acc_t>(v.x);
+            cn[mm][q + 1] = static_cast<acc_t>(v.y);
+            cn[mm][q + 2] = static_cast<acc_t>(v.z);
+            cn[mm][q + 3] = static_cast<acc_t>(v.w);
+          }
+        } else if constexpr (F % 2 == 0) {
 #pragma unroll
           for (int q = 0; q < F; q += 2) {
             const double2 v = __ldg(reinterpret_cast<const double2*>(C + mm * p.Mp + q));
@@ -375,10 +382,10 @@ __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
         if (g < G) {
           const int j1 = w.gs[g + 1];
           for (int j = w.gs[g] + r; j < j1; j += 4) {
-            const double2* rp = reinterpret_cast<const double2*>(recs + static_cast<int64_t>(w.od[j]) * 8);
-            const double2 a01 = rp[0], a23 = rp[1], ux = rp[2];
-            const double R[4] = {a01.x, a01.y, a23.x, a23.y};
-            const double uu = ux.x;
+            const double* rp = recs + static_cast<int64_t>(w.od[j]) * 8;
+            const double4 rv = ldc4(rp);
+            const double R[4] = {rv.x, rv.y, rv.z, rv.w};
+            const double uu = rp[4];
             double um = 1.0;
 #pragma unroll
             for (int mm = 0; mm < 6; ++mm) {
@@ -435,12 +442,17 @@ __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
     double* ts = w.ts;
     double* Ti = p.T + static_cast<size_t>(i) * 4 * p.Mp;
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < 4; ++a) {
+      if constexpr (F % 4 == 0) {
 #pragma unroll
-      for (int q = 0; q < F; ++q) {
-        Ti[a * p.Mp + f0 + q] = tacc[a][q];
-        ts[a * p.Mp + f0 + q] = tacc[a][q];
+        for (int q = 0; q < F; q += 4) st4(Ti + a * p.Mp + f0 + q, tacc[a][q], tacc[a][q + 1], tacc[a][q + 2], tacc[a][q + 3]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < F; ++q) Ti[a * p.Mp + f0 + q] = tacc[a][q];
       }
+#pragma unroll
+      for (int q = 0; q < F; ++q) ts[a * p.Mp + f0 + q] = tacc[a][q];
+    }
     __syncwarp();
     const int slot = p.slot_of[i];
     double* Drow = p.D + static_cast<size_t>(slot < 0 ? 0 : slot) * p.K0p;
@@ -468,6 +480,13 @@ __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
           continue;
         }
         double* dst = Drow + qq * p.M + f0;
+        if constexpr (F % 4 == 0) {
+          if ((p.M & 3) == 0) {
+#pragma unroll
+            for (int q = 0; q < F; q += 4) st4(dst + q, dv[q], dv[q + 1], dv[q + 2], dv[q + 3]);
+            continue;
+          }
+        }
         if constexpr (F % 2 == 0) {
           if ((p.M & 1) == 0) {
 #pragma unroll
@@ -522,18 +541,32 @@ __global__ void __launch_bounds__(256, 1) k_tab_dT(TabParams p, double* __restri
     const double* Ti = p.T + static_cast<size_t>(i) * 4 * p.Mp;
     double tv[4][F], dT[4][F];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < 4; ++a) {
+      if constexpr (F % 4 == 0) {
+#pragma unroll
+        for (int q = 0; q < F; q += 4) {
+          const double4 v = ldg4(Ti + a * p.Mp + f0 + q);
+          tv[a][q] = v.x;
+          tv[a][q + 1] = v.y;
+          tv[a][q + 2] = v.z;
+          tv[a][q + 3] = v.w;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < F; ++q) tv[a][q] = Ti[a * p.Mp + f0 + q];
+      }
 #pragma unroll
       for (int q = 0; q < F; ++q) {
-        tv[a][q] = Ti[a * p.Mp + f0 + q];
         ts[a * p.Mp + f0 + q] = tv[a][q];
         dT[a][q] = 0.0;
       }
+    }
     __syncwarp();
     const int slot = p.slot_of[i];
     const double* dDrow = p.dD + static_cast<size_t>(slot < 0 ? 0 : slot) * p.K0p;
     const bool fon = f0 < p.M && slot >= 0;
     const bool vec = ((p.M | p.K0p) & 1) == 0; // 16-byte aligned dD pairs
+    const bool vec4 = ((p.M | p.K0p) & 3) == 0; // 32-byte aligned dD quads
     // the dD rows of up to QB features q are loaded together (all 16 rows of the Cu model at F = 4:
     // 16 KB in flight per warp, so HBM sees enough requests), then contracted in ascending q
     constexpr int QB = (64 / F) < 16 ? (64 / F) : 16;
@@ -543,6 +576,19 @@ __global__ void __launch_bounds__(256, 1) k_tab_dT(TabParams p, double* __restri
       for (int ql = 0; ql < QB; ++ql) {
         const int qq = q0 + ql;
         const bool on = fon && qq < p.mlt;
+        if constexpr (F % 4 == 0) {
+          if (vec4) {
+#pragma unroll
+            for (int q = 0; q < F; q += 4) {
+              const double4 v = on ? ldg4(dDrow + qq * p.M + f0 + q) : make_double4(0.0, 0.0, 0.0, 0.0);
+              dq[ql][q] = v.x;
+              dq[ql][q + 1] = v.y;
+              dq[ql][q + 2] = v.z;
+              dq[ql][q + 3] = v.w;
+            }
+            continue;
+          }
+        }
         if constexpr (F % 2 == 0) {
           if (vec) {
 #pragma unroll
@@ -591,9 +637,15 @@ __global__ void __launch_bounds__(256, 1) k_tab_dT(TabParams p, double* __restri
         for (int a = 0; a < 4; ++a) dT[a][q] += S[f * 4 + a];
     }
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < 4; ++a) {
+      if constexpr (F % 4 == 0) {
 #pragma unroll
-      for (int q = 0; q < F; ++q) out[a * p.Mp + f0 + q] = dT[a][q];
+        for (int q = 0; q < F; q += 4) st4(out + a * p.Mp + f0 + q, dT[a][q], dT[a][q + 1], dT[a][q + 2], dT[a][q + 3]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < F; ++q) out[a * p.Mp + f0 + q] = dT[a][q];
+      }
+    }
     __syncwarp();
     if (lane == 0) atomicAdd(p.counters + 1, static_cast<unsigned long long>(p.n_real[i]));
   }
@@ -935,20 +987,22 @@ __global__ void __launch_bounds__(256) k_tab_bwd_g(TabParams p) {
     const bool fits = ro + nreal <= p.gcap && gb0 + p.n_grp[i] <= p.pcap;
     if (!fits && lane == 0) raise_err(p.err, ro + nreal > p.gcap ? DEV_GCAP : DEV_PBUF);
     for (int k = lane; fits && k < nreal; k += 32) {
-      const double2* rp = reinterpret_cast<const double2*>(p.rec + (loff + k) * 8);
+      const double* rp = p.rec + (loff + k) * 8;
       const int grp = p.egrp[loff + k];
-      const double2 a01 = rp[0], a23 = rp[1], ud = rp[2], dd2 = rp[3];
-      const double R[4] = {a01.x, a01.y, a23.x, a23.y};
-      const double uu = ud.x;
-      const double d[3] = {ud.y, dd2.x, dd2.y};
-      // the group's 24 projections as 12 16-byte loads (a Pbuf row is 192 B, 16-byte aligned)
-      const double2* P2 = reinterpret_cast<const double2*>(p.Pbuf + (gb0 + grp) * 24);
+      const double4 ra = ldg4(rp), rb = ldg4(rp + 4);
+      const double R[4] = {ra.x, ra.y, ra.z, ra.w};
+      const double uu = rb.x;
+      const double d[3] = {rb.y, rb.z, rb.w};
+      // the group's 24 projections as 6 32-byte loads (a Pbuf row is 192 B, 32-byte aligned)
+      const double* Pg = p.Pbuf + (gb0 + grp) * 24;
       double P[24];
 #pragma unroll
-      for (int q = 0; q < 12; ++q) {
-        const double2 v = __ldg(P2 + q);
-        P[2 * q] = v.x;
-        P[2 * q + 1] = v.y;
+      for (int q = 0; q < 6; ++q) {
+        const double4 v = ldg4(Pg + 4 * q);
+        P[4 * q] = v.x;
+        P[4 * q + 1] = v.y;
+        P[4 * q + 2] = v.z;
+        P[4 * q + 3] = v.w;
       }
       // env-mat derivative terms from d, exactly as the forward pass evaluated them
       const double r = sqrt(norm2_exact(d));
