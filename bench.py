@@ -87,8 +87,9 @@ class ClockSampler:
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
                0x4: "sw_power_cap"}
 
-    def __init__(self, gpu: int, period: float = float(os.environ.get("BENCH_CLK_PERIOD", "0.1"))):
-        self.gpu, self.period = gpu, period
+    def __init__(self, gpu: int, period: float = float(os.environ.get("BENCH_CLK_PERIOD", "0.1")),
+                 enabled: bool = True):
+        self.gpu, self.period, self.enabled = gpu, period, enabled
         self.samples = []
         self._p = None
         try:
@@ -99,7 +100,7 @@ class ClockSampler:
             self.bus = ""
 
     def __enter__(self):
-        if os.environ.get("BENCH_NO_CLOCKS"):
+        if os.environ.get("BENCH_NO_CLOCKS") or not self.enabled:
             return self
         try:
             self._p = subprocess.Popen([sys.executable, "-c", _SAMPLER, self.bus, str(self.period), str(self.gpu)],
@@ -274,7 +275,8 @@ def run_ours(args, world, rank, local, dist):
     l0 = pot.launch_count
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    # clocks sampled by rank 0 only (one NVML process per box; every rank's GPU runs the same step)
+    with ClockSampler(local, enabled=rank == 0) as clk:
         ev0.record(stream)
         pot.md_step(args.steps)
         ev1.record(stream)
