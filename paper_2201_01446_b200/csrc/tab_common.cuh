@@ -32,7 +32,7 @@ struct TabParams {
   const int* max_nbr;
   DevCell c;
   double rc2, rs, rc;
-  double x0, h, x_end;
+  double x0, h, x_end, ih; // ih = 1 / h (first guess of locate only)
   int tn;
   int n, n_types, M, Mp, mlt, K0p;
   int i0, i1;           // centre range of this launch (pipelined halves); [0, n) otherwise
@@ -69,7 +69,8 @@ __device__ __forceinline__ int locate(const TabParams& p, double x, bool& ext, i
     ext = false;
     return 0;
   }
-  const double tf = floor(__ddiv_rn(__dsub_rn(x, p.x0), p.h));
+  // first guess by a multiply (at most one interval off); the nudge loops below fix th exactly
+  const double tf = floor(__dmul_rn(__dsub_rn(x, p.x0), p.ih));
   if (!(tf < static_cast<double>(p.tn) + 2.0)) {  // far past the end (or inf): clamp directly
     ext = true;
     return p.tn - 1;
@@ -226,6 +227,7 @@ inline TabParams make_params(Engine& E) {
   p.rc = E.r_cut;
   p.x0 = E.tab_x0;
   p.h = E.tab_h;
+  p.ih = 1.0 / E.tab_h;
   p.x_end = E.tab_x0 + E.tab_h * static_cast<double>(E.tab_n);
   p.tn = static_cast<int>(E.tab_n);
   p.n = static_cast<int>(E.n);

@@ -251,18 +251,26 @@ __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
     double* recs = p.rec + loff * 8;
     // --- A: env-mat of the row, compaction of the reals (list order) ---
     int nreal = 0, kmin = 0x7fffffff, kmax = -1;
-    uint64_t key_nx = lane < len ? p.keys[off + lane] : 0; // next 32 keys in flight
+    // software pipeline over 32-entry steps: keys two steps ahead, neighbour positions one
+    uint64_t key_nx = lane < len ? p.keys[off + lane] : 0;
+    uint64_t key_nx2 = 32 + lane < len ? p.keys[off + 32 + lane] : 0;
+    double3 pj_nx = lane < len ? ld_pos(p.pos, key_j(key_nx)) : ri;
     for (int base = 0; base < len; base += 32) {
       const int e = base + lane;
       const bool valid = e < len;
       const uint64_t key = key_nx;
-      if (base + 32 < len) key_nx = e + 32 < len ? p.keys[off + e + 32] : 0;
+      const double3 pj = pj_nx;
+      if (base + 32 < len) {
+        key_nx = key_nx2;
+        if (e + 32 < len) pj_nx = ld_pos(p.pos, key_j(key_nx));
+        if (base + 64 < len) key_nx2 = e + 64 < len ? p.keys[off + e + 64] : 0;
+      }
       double d[3] = {0.0, 0.0, 0.0};
       double r2 = 0.0;
       if (valid) {
         int sh[3];
         key_shift(key, sh);
-        disp_exact(p.c, ri, ld_pos(p.pos, key_j(key)), sh[0], sh[1], sh[2], d);
+        disp_exact(p.c, ri, pj, sh[0], sh[1], sh[2], d);
         r2 = norm2_exact(d);
         if (r2 < 1e-12) raise_err(p.err, DEV_OVERLAP); // env_mat.cpp:33
       }
@@ -381,17 +389,35 @@ __global__ void __launch_bounds__(64, TAB_FWD_MINB) k_tab_fwd(TabParams p) {
         for (int k = 0; k < 24; ++k) Wv[k] = 0.0;
         if (g < G) {
           const int j1 = w.gs[g + 1];
-          for (int j = w.gs[g] + r; j < j1; j += 4) {
+          // members j, j + 4 (, j + 8, ...) of this lane in order; the records of two members
+          // are requested before either is used
+          for (int j = w.gs[g] + r; j < j1; j += 8) {
+            const bool two = j + 4 < j1;
             const double* rp = recs + static_cast<int64_t>(w.od[j]) * 8;
+            const double* rq = recs + static_cast<int64_t>(w.od[two ? j + 4 : j]) * 8;
             const double4 rv = ldc4(rp);
-            const double R[4] = {rv.x, rv.y, rv.z, rv.w};
             const double uu = rp[4];
-            double um = 1.0;
+            const double4 rw = ldc4(rq);
+            const double uw = rq[4];
+            {
+              const double R[4] = {rv.x, rv.y, rv.z, rv.w};
+              double um = 1.0;
 #pragma unroll
-            for (int mm = 0; mm < 6; ++mm) {
+              for (int mm = 0; mm < 6; ++mm) {
 #pragma unroll
-              for (int a = 0; a < 4; ++a) Wv[a * 6 + mm] += R[a] * um;
-              um *= uu;
+                for (int a = 0; a < 4; ++a) Wv[a * 6 + mm] += R[a] * um;
+                um *= uu;
+              }
+            }
+            if (two) {
+              const double R[4] = {rw.x, rw.y, rw.z, rw.w};
+              double um = 1.0;
+#pragma unroll
+              for (int mm = 0; mm < 6; ++mm) {
+#pragma unroll
+                for (int a = 0; a < 4; ++a) Wv[a * 6 + mm] += R[a] * um;
+                um *= uw;
+              }
             }
           }
         }
