@@ -21,7 +21,8 @@
 //   k_tab_fwd    one warp per centre: env-mat of the row (list order), real filter, interval,
 //                compact per-real records (R, u, d) + list ranks (ridx), stable counting sort of
 //                the reals by (type, interval), group moments, T = W . C, D = T<^T T
-//   k_tab_dT     one warp per centre: dT from dD (contract.hpp:21-38)
+//   k_tab_dT2    two warps per centre: dT from dD (contract.hpp:21-38), dD and T rows streamed into
+//                shared memory by bulk copies (k_tab_dT: the register-load version, fallback)
 //   k_tab_bwd_P2 32 centres per CTA: interval projections P per group on DMMA (k_tab_bwd_P per
 //                warp for blocks with a too wide interval union)
 //   k_tab_bwd_g  one warp per centre: dE_i/dd_ij from P and the records, written compactly at
@@ -677,6 +678,156 @@ __global__ void __launch_bounds__(256, 1) k_tab_dT(TabParams p, double* __restri
   }
 }
 
+// ---------------------------------------------------------------- k_tab_dT2 (bulk-copy stream)
+// k_tab_dT with the centre's dD row (mlt x M) and T row (4 x Mp) brought into shared memory by
+// one bulk copy each (cp.async.bulk + mbarrier), double-buffered per CTA: the copies of the next
+// centre are in flight while the current one is contracted. DT2_W warps per centre, each summing
+// its share of the q rows of dT[a][p] = sum_q dD[q][p] T[a][q] (shares combined in warp order)
+// and the S[q][a] = sum_p dD[q][p] T[a][p] of its own q; lane owns features p = lane + 32 f.
+constexpr int DT2_W = 2;
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   tc::smem_u32(smem)),
+               "l"(gmem), "r"(bytes), "r"(tc::smem_u32(mbar))
+               : "memory");
+}
+
+__host__ __device__ inline size_t dt2_cta_doubles(int M, int Mp, int mlt) {
+  // two buffers (dD row + T row), S, the dT shares of warps 1.., two mbarriers
+  return 2 * (static_cast<size_t>(mlt) * M + 4 * static_cast<size_t>(Mp)) + 4 * static_cast<size_t>(mlt) +
+         (DT2_W - 1) * 4 * static_cast<size_t>(Mp) + 2;
+}
+
+template <int F>
+__global__ void __launch_bounds__(32 * DT2_W) k_tab_dT2(TabParams p, double* __restrict__ dTg) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  const size_t bufd = static_cast<size_t>(p.mlt) * p.M + 4 * static_cast<size_t>(p.Mp);
+  double* base = reinterpret_cast<double*>(smem);
+  double* S = base + 2 * bufd;       // [mlt][4]
+  double* H = S + 4 * p.mlt;         // [W - 1][4][Mp] dT shares of warps 1..
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(H + (DT2_W - 1) * 4 * p.Mp);
+  const uint32_t dbytes = static_cast<uint32_t>(p.mlt) * p.M * 8, tbytes = 4u * p.Mp * 8;
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&mbar[0], 1);
+    tc::mbar_init(&mbar[1], 1);
+    tc::fence_barrier_init();
+  }
+  __syncthreads();
+  const int qh = (((p.mlt + DT2_W - 1) / DT2_W) + 3) & ~3; // multiple of 4 (rs16 blocks)
+  const int qa = wid * qh, qb = min(p.mlt, qa + qh); // this warp's q rows
+  const int stride = gridDim.x;
+  auto issue = [&](int i, int b, bool cen, int slot) {
+    if (threadIdx.x == 0 && cen) {
+      double* db = base + b * bufd;
+      tc::mbar_expect_tx(&mbar[b], dbytes + tbytes);
+      bulk_g2s(db, p.dD + static_cast<size_t>(slot) * p.K0p, dbytes, &mbar[b]);
+      bulk_g2s(db + static_cast<size_t>(p.mlt) * p.M, p.T + static_cast<size_t>(i) * 4 * p.Mp, tbytes, &mbar[b]);
+    }
+  };
+  uint32_t phase[2] = {0u, 0u};
+  // centre flag, slot and real count of the centre after next are loaded one step ahead
+  int i = p.i0 + blockIdx.x;
+  bool cen_c = false, cen_n = false;
+  int slot_n = 0, nr_c = 0, nr_n = 0;
+  unsigned long long rows = 0; // rows_backward of this CTA's centres, added once at the end
+  if (i < p.i1) {
+    cen_c = p.center[i];
+    nr_c = p.n_real[i];
+    issue(i, 0, cen_c, p.slot_of[i]);
+  }
+  if (i + stride < p.i1) {
+    cen_n = p.center[i + stride];
+    slot_n = p.slot_of[i + stride];
+    nr_n = p.n_real[i + stride];
+  }
+  for (int n = 0; i < p.i1; ++n, i += stride) {
+    const int b = n & 1;
+    const bool cen = cen_c;
+    const int nr = nr_c;
+    if (i + stride < p.i1) issue(i + stride, b ^ 1, cen_n, slot_n);
+    cen_c = cen_n;
+    nr_c = nr_n;
+    if (i + 2 * stride < p.i1) {
+      cen_n = p.center[i + 2 * stride];
+      slot_n = p.slot_of[i + 2 * stride];
+      nr_n = p.n_real[i + 2 * stride];
+    }
+    double* out = dTg + static_cast<size_t>(i) * 4 * p.Mp;
+    if (!cen) {
+      if (wid == 0)
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int f = 0; f < F; ++f) out[a * p.Mp + lane + 32 * f] = 0.0;
+      continue;
+    }
+    tc::mbar_wait(&mbar[b], phase[b]);
+    phase[b] ^= 1u;
+    const double* db = base + b * bufd;
+    const double* tb = db + static_cast<size_t>(p.mlt) * p.M;
+    double tv[4][F], dT[4][F];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        tv[a][f] = tb[a * p.Mp + lane + 32 * f];
+        dT[a][f] = 0.0;
+      }
+    for (int q0 = qa; q0 < qb; q0 += 4) {
+      double part[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) part[k] = 0.0;
+#pragma unroll
+      for (int ql = 0; ql < 4; ++ql) {
+        const int qq = q0 + ql;
+        if (qq < qb) {
+          double dq[F];
+#pragma unroll
+          for (int f = 0; f < F; ++f) dq[f] = lane + 32 * f < p.M ? db[qq * p.M + lane + 32 * f] : 0.0;
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            const double ta = tb[a * p.Mp + qq];
+#pragma unroll
+            for (int f = 0; f < F; ++f) {
+              dT[a][f] += dq[f] * ta;
+              part[ql * 4 + a] += dq[f] * tv[a][f];
+            }
+          }
+        }
+      }
+      const double sv = rs16(part, lane);
+      if (lane < 16 && q0 + (lane >> 2) < qb) S[(q0 + (lane >> 2)) * 4 + (lane & 3)] = sv;
+    }
+    if (wid > 0)
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int f = 0; f < F; ++f) H[((wid - 1) * 4 + a) * p.Mp + lane + 32 * f] = dT[a][f];
+    __syncthreads();
+    if (wid == 0) {
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        const int pp = lane + 32 * f;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          double v = dT[a][f];
+#pragma unroll
+          for (int w = 1; w < DT2_W; ++w) v += H[((w - 1) * 4 + a) * p.Mp + pp];
+          if (pp < p.mlt) v += S[pp * 4 + a];
+          out[a * p.Mp + pp] = v;
+        }
+      }
+      rows += static_cast<unsigned long long>(nr);
+    }
+    // shared-memory reads of this buffer (and of S, H) are done before they are overwritten
+    tc::fence_proxy_async();
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && rows) atomicAdd(p.counters + 1, rows);
+}
+
 // ---------------------------------------------------------------- k_tab_bwd_P (warp per centre)
 // Per-warp projections P[a][m] = sum_p dT[a][p] C[th][m][p] of every group of a centre (FMA +
 // reduce-scatter). Used for the atom blocks whose interval union is too wide for the tensor-core
@@ -1121,6 +1272,17 @@ void launch_bwd_warp(const TabParams& p, const double* dTg, const int* fb_list, 
 
 template <int F>
 void launch_dT(const TabParams& p, double* dTg, cudaStream_t st, int sms) {
+  static const bool legacy = std::getenv("DPB_DT_LEGACY") != nullptr;
+  const size_t b2 = dt2_cta_doubles(p.M, p.Mp, p.mlt) * sizeof(double);
+  if (!legacy && b2 <= 110 * 1024 && (p.M & 1) == 0 && (p.Mp & 1) == 0 && (p.K0p & 1) == 0) {
+    smem_optin(k_tab_dT2<F>, b2);
+    int per_sm = 1;
+    DPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tab_dT2<F>, 32 * DT2_W, b2));
+    const int blocks = std::max(1, std::min(p.i1 - p.i0, sms * std::max(per_sm, 1)));
+    k_tab_dT2<F><<<blocks, 32 * DT2_W, b2, st>>>(p, dTg);
+    DPB_CUDA(cudaGetLastError());
+    return;
+  }
   const size_t bytes = 8 * (4 * static_cast<size_t>(p.Mp) + 4 * p.mlt) * sizeof(double);
   DPB_CUDA(cudaFuncSetAttribute(k_tab_dT<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
   const int blocks = std::max(1, std::min(ceil_div(p.i1 - p.i0, 8), sms * 8));
