@@ -269,14 +269,18 @@ def run_ours(args, world, rank, local, dist):
     pot.md_begin(gcfg, gvel, mc)
     pot.md_step(args.warmup)
     stream = torch.cuda.ExternalStream(pot.stream, device=torch.device("cuda", local))
-    torch.cuda.synchronize()
-    barrier(dist)
-    torch.cuda.synchronize()
-    l0 = pot.launch_count
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    # clocks sampled by rank 0 only (one NVML process per box; every rank's GPU runs the same step)
+    # clocks sampled by rank 0 only (one NVML process per box; every rank's GPU runs the same
+    # step). The sampler process is started BEFORE the barrier: started after it, its ~0.1 s
+    # start-up delayed rank 0's first launches while the other ranks' windows were already
+    # open, and they waited for rank 0 in the first halo exchange (C2 on 2 GPUs: rank windows
+    # 467 vs 579 ms for 100 steps).
     with ClockSampler(local, enabled=rank == 0) as clk:
+        torch.cuda.synchronize()
+        barrier(dist)
+        torch.cuda.synchronize()
+        l0 = pot.launch_count
         ev0.record(stream)
         pot.md_step(args.steps)
         ev1.record(stream)
@@ -285,6 +289,8 @@ def run_ours(args, world, rank, local, dist):
     barrier(dist)
     launches = pot.launch_count - l0
     ms_window = ev0.elapsed_time(ev1)
+    if world > 1:
+        print(f"[bench rank {rank}] window {ms_window:.2f} ms for {args.steps} steps", file=sys.stderr, flush=True)
     # Rebuild amortization: the list is rebuilt every 50 steps, so a K-step window should carry
     # K/50 rebuilds; it carries as many as multiples of 50 fall inside it (often none). Time the
     # next rebuild step alone against single ordinary steps and add the difference for the
@@ -357,8 +363,9 @@ def run_ours(args, world, rank, local, dist):
             traffic = per_atom * n if per_atom else None
         except Exception:
             traffic = None
-    n_real = res.counters.rows_forward / max(res.force_evals, 1) / n
-    alg = algorithmic_flops_per_atom(m, n_real) * n
+    # real pairs per atom of the whole job (md_end sums the counters over the ranks)
+    n_real = res.counters.rows_forward / max(res.force_evals, 1) / n_total
+    alg = algorithmic_flops_per_atom(m, n_real) * n_total  # FLOP per step, all ranks
     total_phase_ms = sum(v[0] for v in phases.values())
 
     # e2e through the reference-facing C-ABI with host buffers
@@ -437,9 +444,9 @@ def run_ours(args, world, rank, local, dist):
                          "peak_source": peak_src,
                          "traffic": traffic, "flop_per_launch_group": fit_flop_launch,
                          "group_ms_per_step": fit_launch_ms},
-            "step_roofline": {"algorithmic_flop_per_atom_step": alg / n,
-                              "achieved_tflops": alg * args.steps / (ms / 1e3) / 1e12,
-                              "frac_of_fp64_peak": alg * args.steps / (ms / 1e3) / 1e12 / 37.15},
+            "step_roofline": {"algorithmic_flop_per_atom_step": alg / n_total,
+                              "achieved_tflops": alg * args.steps / (ms_max / 1e3) / 1e12,
+                              "frac_of_fp64_peak": alg * args.steps / (ms_max / 1e3) / 1e12 / (37.15 * world)},
             "phases_ms_per_step": {k: v[0] / nb for k, v in phases.items()},
             "phase_sum_ms_per_step": total_phase_ms / nb,
             "phases_note": "breakdown pass of %d further steps with the two-stream pipelining off" % nb,
