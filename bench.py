@@ -446,7 +446,10 @@ def run_ours(args, world, rank, local, dist):
                          "group_ms_per_step": fit_launch_ms},
             "step_roofline": {"algorithmic_flop_per_atom_step": alg / n_total,
                               "achieved_tflops": alg * args.steps / (ms_max / 1e3) / 1e12,
-                              "frac_of_fp64_peak": alg * args.steps / (ms_max / 1e3) / 1e12 / (37.15 * world)},
+                              "frac_of_fp64_peak": alg * args.steps / (ms_max / 1e3) / 1e12 / (37.15 * world),
+                              "note": ("FP64-equivalent FLOP of the whole step against the FP64 peak of all GPUs"
+                                       + ("; mixed mode runs the fitting on the tf32 tensor cores, so values "
+                                          "above 1 are possible" if args.precision == "mixed" else ""))},
             "phases_ms_per_step": {k: v[0] / nb for k, v in phases.items()},
             "phase_sum_ms_per_step": total_phase_ms / nb,
             "phases_note": "breakdown pass of %d further steps with the two-stream pipelining off" % nb,
