@@ -248,3 +248,32 @@ def test_caller_supplied_list_matches_reference_operator(cu):
     with pytest.raises(dp.InputError):
         pot.compute_with_list(c, bad)
     check(pot.compute(c), ro, pot.counters, co)
+
+
+def test_legacy_dT_kernel_matches_oracle(tmp_path):
+    """The register-load k_tab_dT (fallback of the bulk-copy k_tab_dT2 for wide rows), forced by
+    DPB_DT_LEGACY=1 in a fresh process (the switch is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys
+sys.path.insert(0, "tests")
+import oracle_lib as O
+import paper_2201_01446_b200 as dp
+m = dp.gen_model("copper-like", 7)
+t = dp.build_tables(m, 0.01)
+c = dp.gen_config("copper-like", 8, 8, 8, 0.1, 11)
+ro, co = O.or_compute(c, m, t)
+pot = dp.DeepPot(m, t)
+r = pot.compute(c)
+e = abs(r.energy - ro.energy) / abs(ro.energy)
+f = O.normwise(r.forces, ro.forces)
+v = O.normwise(r.virial, ro.virial)
+assert max(e, f, v) <= 1e-10 and pot.counters == co, (e, f, v)
+print("ok", e, f, v)
+'''
+    env = dict(os.environ, DPB_DT_LEGACY="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and out.stdout.startswith("ok"), out.stdout + out.stderr
