@@ -909,12 +909,14 @@ __global__ void __launch_bounds__(64, 6) k_tab_bwd_P(TabParams p, const double* 
 // kernel re-read 6 KB of coefficients per (centre, interval) through L1 and reduced with shuffles;
 // here coefficient traffic drops by ~20x and the MACs run on the tensor pipe. Only the (centre,
 // interval) pairs the centre really has are written (Pbuf, same layout as the per-warp kernel).
-constexpr int P2_NA = 32, P2_CB = 4, P2_UCAP = 128, P2_UW = P2_UCAP / 32, P2_BMW = 256;
-constexpr int P2_THREADS = 512; // 16 warps, one m-tile (2 centres x 4 rows) each
+constexpr int P2_NA = 16, P2_CB = 4, P2_UCAP = 128, P2_UW = P2_UCAP / 32, P2_BMW = 256;
+// 8 warps, one m-tile (2 centres x 4 rows) each, whose dT rows live in registers as DMMA A
+// fragments; two CTAs per SM, so one block's union set-up overlaps the other's MMAs
+constexpr int P2_THREADS = 256;
 
 __host__ __device__ inline size_t p2_smem_bytes(int Mp) {
   const int pitch = Mp + 4;
-  return static_cast<size_t>(4 * P2_NA + 2 * 6 * P2_CB) * pitch * sizeof(double) +
+  return static_cast<size_t>(2 * 6 * P2_CB) * pitch * sizeof(double) +
          (2 * P2_BMW + P2_UCAP + P2_NA / 2 * P2_UW + 4) * sizeof(int) + P2_NA * P2_UCAP * sizeof(int16_t);
 }
 
@@ -925,12 +927,11 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 }
 
 template <int F>
-__global__ void __launch_bounds__(P2_THREADS, 1) k_tab_bwd_P2(TabParams p, const double* __restrict__ dTg,
+__global__ void __launch_bounds__(P2_THREADS, 2) k_tab_bwd_P2(TabParams p, const double* __restrict__ dTg,
                                                        int* __restrict__ fb_list, int* __restrict__ fb_count) {
   constexpr int Mp = 32 * F, pitch = Mp + 4, units = Mp / 2;
   extern __shared__ __align__(16) unsigned char smem[];
-  double* dTs = reinterpret_cast<double*>(smem);                         // [128][pitch]
-  double* Cs = dTs + 4 * P2_NA * pitch;                                  // [2][24][pitch]
+  double* Cs = reinterpret_cast<double*>(smem);                          // [2][24][pitch]
   uint32_t* bm = reinterpret_cast<uint32_t*>(Cs + 2 * 6 * P2_CB * pitch); // [BMW] union bitmap
   int* wpre = reinterpret_cast<int*>(bm + P2_BMW);                       // [BMW] popcount prefix
   int* ubin = wpre + P2_BMW;                                             // [UCAP] union bins
@@ -953,16 +954,16 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_tab_bwd_P2(TabParams p, const
     }
   for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
     const int i0 = p.i0 + blk * P2_NA;
-    // dT rows of the 32 centres (contiguous in dTg)
-    for (int q = tid; q < 4 * P2_NA * units; q += P2_THREADS) {
-      const int row = q / units, c2 = q % units;
-      double* dst = dTs + row * pitch + 2 * c2;
-      if (i0 + (row >> 2) < p.i1)
-        tc::cp_async16(dst, dTg + (static_cast<size_t>(i0) * 4 + row) * Mp + 2 * c2);
-      else
-        dst[0] = dst[1] = 0.0;
+    // this warp's m-tile of dT (rows warp*8 + gid, contiguous in dTg) as DMMA A fragments:
+    // afr[j] = dT[row][4 j + tig]; in flight during the union set-up below
+    double afr[Mp / 4];
+    {
+      const int r = warp * 8 + gid;
+      const bool ok = i0 + (r >> 2) < p.i1;
+      const double* src = dTg + (static_cast<size_t>(i0) * 4 + r) * Mp + tig;
+#pragma unroll
+      for (int j = 0; j < Mp / 4; ++j) afr[j] = ok ? __ldg(src + 4 * j) : 0.0;
     }
-    tc::cp_commit();
     if (tid == 0) {
       misc[0] = 0x7fffffff;
       misc[1] = -1;
@@ -1097,7 +1098,6 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_tab_bwd_P2(TabParams p, const
       double acc[1][3][2];
 #pragma unroll
       for (int nt = 0; nt < 3; ++nt) acc[0][nt][0] = acc[0][nt][1] = 0.0;
-      const double* a0 = dTs + (warp * 8 + gid) * pitch + tig;
       const double* b0 = cs + gid * pitch + tig;
       // n-tile nt covers chunk slots {nt, nt+1} (columns 8 nt .. 8 nt + 7 of 6 per slot); the
       // m-tile needs it only if one of its two centres has one of those intervals
@@ -1105,18 +1105,20 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_tab_bwd_P2(TabParams p, const
       const unsigned n0 = (mtmask[warp * P2_UW + wd] >> sh) & 15u;
       const unsigned use = ((n0 & 3u) ? 1u : 0u) | ((n0 & 6u) ? 2u : 0u) | ((n0 & 12u) ? 4u : 0u);
       if (use == 7u) {
-#pragma unroll 4
-        for (int k = 0; k < Mp; k += 4) {
-          const double av0 = a0[k];
+#pragma unroll
+        for (int j = 0; j < Mp / 4; ++j) {
+          const int k = 4 * j;
+          const double av0 = afr[j];
           const double bv0 = b0[k], bv1 = b0[8 * pitch + k], bv2 = b0[16 * pitch + k];
           dmma884(acc[0][0][0], acc[0][0][1], av0, bv0);
           dmma884(acc[0][1][0], acc[0][1][1], av0, bv1);
           dmma884(acc[0][2][0], acc[0][2][1], av0, bv2);
         }
       } else if (use) {
-#pragma unroll 2
-        for (int k = 0; k < Mp; k += 4) {
-          const double av0 = a0[k];
+#pragma unroll
+        for (int j = 0; j < Mp / 4; ++j) {
+          const int k = 4 * j;
+          const double av0 = afr[j];
           const double bv0 = b0[k], bv1 = b0[8 * pitch + k], bv2 = b0[16 * pitch + k];
           if (use & 1u) dmma884(acc[0][0][0], acc[0][0][1], av0, bv0);
           if (use & 2u) dmma884(acc[0][1][0], acc[0][1][1], av0, bv1);
@@ -1429,7 +1431,7 @@ void Engine::tab_bwd_range(int, int64_t i0, int64_t i1, cudaStream_t st) {
   case F:                                                                                                     \
     DPB_CUDA(cudaFuncSetAttribute(k_tab_bwd_P2<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
                                   static_cast<int>(bytes)));                                                  \
-    k_tab_bwd_P2<F><<<std::max(1, std::min(nblk, sms)), P2_THREADS, bytes, st>>>(p, dTw, fbl, fbl + nblk_all);   \
+    k_tab_bwd_P2<F><<<std::max(1, std::min(nblk, 2 * sms)), P2_THREADS, bytes, st>>>(p, dTw, fbl, fbl + nblk_all);   \
     break;
       DPB_P2(1) DPB_P2(2) DPB_P2(3) DPB_P2(4)
 #undef DPB_P2
