@@ -1131,11 +1131,15 @@ __global__ void __launch_bounds__(P2_THREADS, 2) k_tab_bwd_P2(TabParams p, const
         if (!r_ok[mt]) continue;
         const int16_t* gi = gidx + r_al[mt] * P2_UCAP + ch * P2_CB;
         double* pb = p.Pbuf + r_base[mt] * 24 + r_a[mt] * 6;
+        // columns 2 tig, 2 tig + 1 of an n-tile are (slot, m), (slot, m + 1) with m even: one
+        // 16-byte store per n-tile (P rows are 192 B, m pairs 16-byte aligned)
 #pragma unroll
-        for (int k = 0; k < 6; ++k) {
-          const int u = ch * P2_CB + cslot[k];
-          const int g = u < U ? gi[cslot[k]] : -1;
-          if (g >= 0) pb[static_cast<int64_t>(g) * 24 + cm[k]] = acc[mt][k >> 1][k & 1];
+        for (int nt = 0; nt < 3; ++nt) {
+          const int u = ch * P2_CB + cslot[2 * nt];
+          const int g = u < U ? gi[cslot[2 * nt]] : -1;
+          if (g >= 0)
+            *reinterpret_cast<double2*>(pb + static_cast<int64_t>(g) * 24 + cm[2 * nt]) =
+                make_double2(acc[mt][nt][0], acc[mt][nt][1]);
         }
       }
       __syncthreads();
