@@ -1453,7 +1453,11 @@ void Engine::tab_bwd_range(int, int64_t i0, int64_t i1, cudaStream_t st) {
   }
   ++launches;
   if (i1 > i0) {
-    k_tab_bwd_g<<<std::max(1, std::min(ceil_div(i1 - i0, 8), sms * 16)), 256, 0, st>>>(p);
+    // persistent: one resident wave of CTAs striding over the centres (non-persistent 8-centre
+    // CTAs: C2 4.244 -> 4.227 ms/step)
+    int per_sm = 1;
+    DPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tab_bwd_g, 256, 0));
+    k_tab_bwd_g<<<std::max(1, std::min(ceil_div(i1 - i0, 8), sms * std::max(per_sm, 1))), 256, 0, st>>>(p);
     ++launches;
   }
 }
