@@ -25,7 +25,7 @@ namespace {
 #endif
 
 template <bool VIR>
-__global__ void __launch_bounds__(256, FORCES_MINB) k_forces(int n, DevCell c, const double4* __restrict__ pos,
+__device__ __forceinline__ void force_row(int64_t w, int n, DevCell c, const double4* __restrict__ pos,
                                                 const int64_t* __restrict__ row_off,
                                                 const uint64_t* __restrict__ keys,
                                                 const uint16_t* __restrict__ rev,
@@ -38,8 +38,6 @@ __global__ void __launch_bounds__(256, FORCES_MINB) k_forces(int n, DevCell c, c
                                                 const double* __restrict__ grecv,
                                                 const int32_t* __restrict__ list) {
   const int lane = threadIdx.x & 31;
-  const int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (w >= n) return;
   const int i = list ? list[w] : static_cast<int>(w); // list: a subset of the atoms (decomposed runs)
   if (!center[i]) return; // ghosts of a decomposed run: their owners compute their forces
   double3 ri;
@@ -148,6 +146,25 @@ __global__ void __launch_bounds__(256, FORCES_MINB) k_forces(int n, DevCell c, c
 #pragma unroll
       for (int k = 0; k < 9; ++k) vpart[9 * static_cast<int64_t>(i) + k] = acc[(6 + k) % NACC];
   }
+}
+
+// persistent: one resident wave of CTAs, a warp per atom striding over the atoms
+template <bool VIR>
+__global__ void __launch_bounds__(256, FORCES_MINB) k_forces(int n, DevCell c, const double4* __restrict__ pos,
+                                                const int64_t* __restrict__ row_off,
+                                                const uint64_t* __restrict__ keys,
+                                                const uint16_t* __restrict__ rev,
+                                                const int16_t* __restrict__ ridx,
+                                                const int64_t* __restrict__ realoff,
+                                                const double* __restrict__ g,
+                                                double* __restrict__ f, double* __restrict__ vpart,
+                                                const uint8_t* __restrict__ center,
+                                                const int32_t* __restrict__ rslot,
+                                                const double* __restrict__ grecv,
+                                                const int32_t* __restrict__ list) {
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t w = blockIdx.x * wpb + (threadIdx.x >> 5); w < n; w += gridDim.x * wpb)
+    force_row<VIR>(w, n, c, pos, row_off, keys, rev, ridx, realoff, g, f, vpart, center, rslot, grecv, list);
 }
 
 // Deterministic two-level reduction of `width` interleaved columns over n rows.
@@ -303,6 +320,12 @@ void Engine::launch_forces() {
   forces.ensure(3 * n);
   // the exact path has no per-real records: its virial is formed here from the re-evaluated d
   auto kf = virial_in_forces ? k_forces<true> : k_forces<false>;
+  int per_sm = 1;
+  DPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, 256, 0));
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  const int64_t fmax = static_cast<int64_t>(sms > 0 ? sms : 148) * std::max(per_sm, 1);
+  auto fgrid = [&](int64_t m) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, 8), fmax))); };
   if (dist) {
     if (virial_in_forces) throw InputErr("the exact path is single-GPU");
     // pair halo in flight (communication stream) while the owned atoms without ghost neighbours
@@ -312,15 +335,15 @@ void Engine::launch_forces() {
     int64_t ni = 0, nb = 0;
     dist_exchange_g(*this, &rslot, &grecv, &inner, &ni, &bound, &nb);
     if (ni)
-      kf<<<ceil_div(ni, 8), 256, 0, stream>>>(static_cast<int>(ni), cell, pos4.p, row_off.p, keys.p, rev.p, ridx.p,
+      kf<<<fgrid(ni), 256, 0, stream>>>(static_cast<int>(ni), cell, pos4.p, row_off.p, keys.p, rev.p, ridx.p,
                                                realoff.p, g.p, forces.p, vpart.p, center.p, rslot, grecv, inner);
     if (halo_overlap) DPB_CUDA(cudaStreamWaitEvent(stream, ev_halo, 0));
     if (nb)
-      kf<<<ceil_div(nb, 8), 256, 0, stream>>>(static_cast<int>(nb), cell, pos4.p, row_off.p, keys.p, rev.p, ridx.p,
+      kf<<<fgrid(nb), 256, 0, stream>>>(static_cast<int>(nb), cell, pos4.p, row_off.p, keys.p, rev.p, ridx.p,
                                                realoff.p, g.p, forces.p, vpart.p, center.p, rslot, grecv, bound);
     launches += 2;
   } else {
-    kf<<<ceil_div(N, 8), 256, 0, stream>>>(N, cell, pos4.p, row_off.p, keys.p, rev.p, ridx.p, realoff.p, g.p,
+    kf<<<fgrid(N), 256, 0, stream>>>(N, cell, pos4.p, row_off.p, keys.p, rev.p, ridx.p, realoff.p, g.p,
                                             forces.p, vpart.p, center.p, nullptr, nullptr, nullptr);
     ++launches;
   }
