@@ -40,7 +40,8 @@ struct GemmArgs {
   const double* tprev;// tanh output of the previous layer [M][ldc] or null
   double* dyout;      // [M][ldc]
   double* dzout;      // [M][ldc] or null
-  int ldc, ldx, ldd; // ldd: pitch of dyin / tprev / dzout
+  int ldc, ldx, ldd; // ldd: pitch of tprev / dzout
+  int ldy;            // pitch of dyin (0: one row for all rows, the readout's dY_L = w_out)
   int ntn, ntm;       // column / row tiles
 };
 
@@ -158,7 +159,7 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& g) {
       } else {
         double v0 = acc[i][j][0], v1 = acc[i][j][1];
         if (g.dyin) {
-          const double2 d = *reinterpret_cast<const double2*>(g.dyin + static_cast<size_t>(row) * g.ldd + col);
+          const double2 d = *reinterpret_cast<const double2*>(g.dyin + static_cast<size_t>(row) * g.ldy + col);
           v0 = d.x + v0;
           v1 = d.y + v1;
         }
@@ -195,11 +196,11 @@ __global__ void __launch_bounds__(128, 6) k_gemm6(GemmArgs g) {
   gemm_body<EPI, BM, BN, STAGES>(g);
 }
 
-// Readout: E = b_out + y . w_out (warp per row); dZ_L = w_out (1 - t^2); dY_L = w_out.
+// Readout: E = b_out + y . w_out (warp per row); dZ_L = w_out (1 - t^2). dY_L = w_out is the
+// same row for every centre: the first backward GEMM reads it from w_out itself (ldy = 0).
 __global__ void k_readout(int rows, int ld, int width, const double* __restrict__ y,
                           const double* __restrict__ t, const double* __restrict__ wout,
-                          double bout, double* __restrict__ e, double* __restrict__ dz,
-                          double* __restrict__ dy) {
+                          double bout, double* __restrict__ e, double* __restrict__ dz) {
   const int lane = threadIdx.x & 31;
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= rows) return;
@@ -211,7 +212,6 @@ __global__ void k_readout(int rows, int ld, int width, const double* __restrict_
     acc += yr[c] * w;
     const double tt = tr[c];
     dz[static_cast<size_t>(r) * ld + c] = w * (1.0 - tt * tt);
-    dy[static_cast<size_t>(r) * ld + c] = w;
   }
   acc = warp_sum(acc);
   if (lane == 0) e[r] = bout + acc;
@@ -364,7 +364,7 @@ void Engine::fitting_type_rows(int t, int64_t r0_, int64_t rows_, cudaStream_t s
   double* dyn = ws(dy2, wpm) + r0 * wpm;
   k_readout<<<ceil_div(rows, 4), 128, 0, st>>>(rows, wpm, last.out, ws(act_y[L - 1], wpm) + r0 * wpm,
                                                    ws(act_t[L - 1], wpm) + r0 * wpm, fit_wout[t].p,
-                                                   b_out[t], e_slot.p + r0, dzc, dyc);
+                                                   b_out[t], e_slot.p + r0, dzc);
   ++launches;
   // backward
   for (int k = L - 1; k >= 0; --k) {
@@ -375,7 +375,8 @@ void Engine::fitting_type_rows(int t, int64_t r0_, int64_t rows_, cudaStream_t s
     a.Bt = fit_w[fo + k].p; // W [inp][outp]: K = outp contiguous
     a.ldb = fl.outp;
     a.K = fl.outp;
-    a.dyin = fl.shortcut ? dyc : nullptr;
+    a.dyin = fl.shortcut ? (k == L - 1 ? fit_wout[t].p : dyc) : nullptr;
+    a.ldy = k == L - 1 ? 0 : wpm;
     a.ldd = wpm;
     if (k > 0) {
       a.tprev = ws(act_t[k - 1], wpm) + r0 * wpm;
