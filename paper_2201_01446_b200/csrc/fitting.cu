@@ -278,9 +278,9 @@ template <int EPI, int BN, int STAGES>
 void launch_gemm(const GemmArgs& a, int rows, int N, cudaStream_t st) {
   using K64 = GemmKernel<EPI, 64, BN, STAGES>;
   using K32 = GemmKernel<EPI, 32, BN, STAGES>;
-  // long K (the layer-0 forward): the 64-row tile's fewer resident CTAs leave the other stream's
-  // tabulate kernels room to overlap, which the pipelined step gains even where the GEMM's own
-  // wave fill is worse (C2: 0.845 vs 0.921, GEMM time equal, step 4.285 -> 4.246 ms)
+  // long K (the layer-0 forward): the 64-row tile wins in the running step even where its wave
+  // fill is worse (C2: 0.845 vs 0.921; 4.207 vs 4.234 ms/step with two chunks, 4.205 vs 4.233
+  // with one), although ncu's cold, serialised launch of it is slower (586 vs 559 us)
   const double tol = a.K > 256 ? 0.10 : 0.05;
   if (rows % 64 == 0 && K64::wave_eff(rows, N) >= K32::wave_eff(rows, N) - tol)
     K64::launch(a, rows, N, st);
